@@ -1,0 +1,199 @@
+/*
+ * loom_b200.h -- C ABI of the B200-native plan-evaluation library.
+ *
+ * This is the ONE boundary the B200 build adds to the reference (SURVEY.md
+ * §1, §8b).  The reference ("loom", header-only C++20) has no process or
+ * device boundary; its plugin point is the function symbol.  Each entry point
+ * below names the reference interface it replaces:
+ *
+ *   loom_search_argmin        loom::exhaustive_search     optimizer.hpp:173-188
+ *                             (ConfigEnumerator 110-150 + estimate estimator.hpp:43-78
+ *                              + meets_quality_floor 118-121 + objective_less 93-116)
+ *   loom_search_argmin_batch  a loop of exhaustive_search over many jobs (config 4)
+ *   loom_search_pareto        loom::pareto_filter         optimizer.hpp:153-171
+ *                             applied to estimate(p) for p in ConfigEnumerator order
+ *   loom_winner_reduce        objective_less as a total-order reduce (multi-GPU combine)
+ *   loom_evaluate_plan        loom::estimate               estimator.hpp:43-78 (one plan)
+ *   loom_lower                node_options optimizer.hpp:51-107 + plan_node_execution
+ *                             chunking.hpp:85-184 + ConfigPoint::identifier config.hpp:49-61
+ *   loom_exhaustive_search_json   the whole drop-in call on reference-format JSON
+ *
+ * Conventions: POD arguments only, caller-owned buffers, int status return
+ * (LOOM_OK / LOOM_INFEASIBLE / LOOM_INVALID / LOOM_DEVICE_ERROR), and a
+ * thread-local message from loom_last_error() formatted like the reference's
+ * loom::Error::what() ("<ErrorClass>: <message>", errors.hpp:17-19).  One
+ * loom_ctx per host thread; a ctx is bound to one CUDA device and stream.
+ * There is no CPU fallback: compute entry points fail with LOOM_DEVICE_ERROR
+ * when no sm_100 device is present.
+ */
+#ifndef LOOM_B200_H
+#define LOOM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOOM_B200_ABI_VERSION 1
+
+/* Status codes.  INFEASIBLE <-> NoFeasibleConfigError (optimizer.hpp:184-186);
+ * INVALID <-> InvalidConfigError / SchemaError / CycleError / UnknownCapabilityError. */
+#define LOOM_OK 0
+#define LOOM_INFEASIBLE 1
+#define LOOM_INVALID 2
+#define LOOM_DEVICE_ERROR 3
+
+/* Criterion, workflow.hpp:67 (same enumerator order). */
+#define LOOM_MIN_COST_DOLLARS 0
+#define LOOM_MIN_ENERGY 1
+#define LOOM_MIN_LATENCY 2
+#define LOOM_MAX_QUALITY 3
+
+/*
+ * A lowered plan space.  Nodes are in dag.nodes order, which is the
+ * ConfigEnumerator order (node 0 most significant digit, last node fastest,
+ * optimizer.hpp:136-141) and also the left-fold order of the energy / dollar
+ * sums in estimate (estimator.hpp:50-60).  Option arrays are node-major:
+ * option o of node i sits at index offset(i) + o with offset(i) = sum of
+ * radix[0..i).  Per-option values are the reference's per-node plan values
+ * ALREADY multiplied by path_count exactly as estimate does (estimator.hpp:51-53).
+ */
+typedef struct loom_problem {
+  int32_t n_nodes;
+  int32_t n_edges;
+  const int32_t* radix;        /* [n_nodes] node_options(...).size()                    */
+  const int64_t* wall_us;      /* [sum radix] NodePlan.wall_us (chunking.hpp:171)         */
+  const double* gpu_wh;        /* [sum radix] NodePlan.gpu_wh * path_count                */
+  const double* cpu_wh;        /* [sum radix] NodePlan.cpu_wh * path_count                */
+  const double* dollars;       /* [sum radix] NodePlan.dollars * path_count               */
+  const int32_t* quality;      /* [sum radix] node_quality (estimator.hpp:32-37)          */
+  const int32_t* lexrank;      /* [sum radix] rank of the option's identifier substring
+                                  among the node's options (config.hpp:49-61)           */
+  const uint64_t* lex_weight;  /* [n_nodes] mixed-radix weight of the node in sorted
+                                  node-id order: product of radix over nodes whose id
+                                  sorts after it (std::map order, config.hpp:46)        */
+  const int32_t* edge_from;    /* [n_edges] node indices (dag.nodes order)                */
+  const int32_t* edge_to;      /* [n_edges]                                               */
+} loom_problem;
+
+/* ObjectiveHierarchy (workflow.hpp:81-86) + the config-3 latency-SLO extension. */
+typedef struct loom_objective {
+  int32_t n_criteria;          /* 0..4 */
+  int32_t criteria[4];         /* LOOM_MIN_* / LOOM_MAX_QUALITY, most significant first */
+  int32_t has_quality_floor;
+  int32_t quality_floor;
+  int32_t has_latency_slo;     /* extension, not in the reference: latency_us <= slo */
+  int32_t reserved;
+  int64_t latency_slo_us;
+} loom_objective;
+
+/* The selected plan: ConfigEstimate (estimator.hpp:20-30) minus the strings,
+ * plus its enumeration index and identifier rank.  64 bytes, POD, so it can be
+ * all-gathered across ranks as raw bytes. */
+typedef struct loom_winner {
+  uint64_t plan_index;         /* position in ConfigEnumerator order              */
+  uint64_t lexkey;             /* rank of ConfigPoint::identifier() in the space  */
+  int64_t latency_us;
+  double gpu_wh;
+  double cpu_wh;
+  double total_wh;
+  double dollars;
+  int32_t quality;
+  int32_t found;               /* 0: no feasible plan in the searched range       */
+} loom_winner;
+
+typedef struct loom_ctx loom_ctx;
+typedef struct loom_device_problem loom_device_problem;
+typedef struct loom_lowered loom_lowered;
+
+/* ---- library / errors -------------------------------------------------- */
+int loom_abi_version(void);
+const char* loom_last_error(void);
+
+/* ---- host-only helpers (no device needed) ------------------------------ */
+/* Product of radices (ConfigEnumerator::total_count, optimizer.hpp:124-129);
+ * LOOM_INVALID on overflow past 2^64 (the reference wraps silently). */
+int loom_problem_total(const loom_problem* problem, uint64_t* total);
+/* Exact reference estimate of one plan (estimator.hpp:43-78) into a winner record. */
+int loom_evaluate_plan(const loom_problem* problem, uint64_t plan_index, loom_winner* out);
+/* objective_less over winner records; found==0 records lose.  Deterministic. */
+int loom_winner_less(const loom_winner* a, const loom_winner* b, const loom_objective* objective);
+int loom_winner_reduce(const loom_winner* winners, int32_t n, const loom_objective* objective,
+                       loom_winner* out);
+/* Parse an objective JSON: {"constraint": "MIN_COST"} or {"criteria": [...]},
+ * optional "quality_floor", optional "latency_slo_us" (workflow.hpp:91-106, 182-183). */
+int loom_objective_parse(const char* objective_json, loom_objective* out);
+
+/* ---- lowering of reference-format JSON (host) -------------------------- */
+/* dag_json: WorkflowDag JSON (workflow.hpp:303-363); library_json: library
+ * bundle (agent_library.hpp:327-344); bounds_json: SearchBounds as
+ * {"max_fanout":4,"max_paths":2,"sku_pool_cap":{..},"sku_total_cap":{..}}. */
+int loom_lower(const char* dag_json, const char* library_json, const char* bounds_json,
+               loom_lowered** out);
+const loom_problem* loom_lowered_problem(const loom_lowered* lowered);
+/* ConfigPoint JSON (config.hpp:88-95) + "identifier" for a plan index. */
+int loom_lowered_config_json(const loom_lowered* lowered, uint64_t plan_index, char* buf,
+                             size_t cap, size_t* needed);
+/* NodeAssignment JSON + identifier substring of one option. */
+int loom_lowered_option_json(const loom_lowered* lowered, int32_t node, int32_t option, char* buf,
+                             size_t cap, size_t* needed);
+void loom_lowered_destroy(loom_lowered* lowered);
+
+/* ---- device context ---------------------------------------------------- */
+/* cuda_stream: a cudaStream_t to launch on (NULL: the ctx creates its own;
+ * (void*)1 = cudaStreamLegacy, the legacy default stream). */
+int loom_ctx_create(int32_t device, void* cuda_stream, loom_ctx** out);
+int loom_ctx_destroy(loom_ctx* ctx);
+/* Kernel launches issued by this ctx since creation (evidence for benches). */
+uint64_t loom_ctx_launch_count(const loom_ctx* ctx);
+
+/* ---- search (device) ---------------------------------------------------- */
+/* Argmin over plan indices [begin, end) (end clamped to the total).  Fills
+ * every field of *out from the winning index.  LOOM_INFEASIBLE when nothing in
+ * the range is feasible (out->found == 0). */
+int loom_search_argmin(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
+                       uint64_t begin, uint64_t end, loom_winner* out);
+
+/* Same, selecting the evaluation algorithm: 0 = hierarchical (default),
+ * 1 = one-plan-per-thread full re-evaluation (independent cross-check). */
+int loom_search_argmin_algo(loom_ctx* ctx, const loom_problem* problem,
+                            const loom_objective* objective, uint64_t begin, uint64_t end,
+                            int32_t algo, loom_winner* out);
+
+/* Per-job argmin over whole plan spaces (config 4).  status[j] gets the
+ * per-job status; the call returns LOOM_OK unless the batch itself failed. */
+int loom_search_argmin_batch(loom_ctx* ctx, const loom_problem* problems,
+                             const loom_objective* objectives, int32_t n_jobs,
+                             loom_winner* out, int32_t* status);
+
+/* Resident problems: upload once, search many times (bench "value" path). */
+int loom_problem_upload(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
+                        loom_device_problem** out);
+int loom_problem_release(loom_device_problem* dp);
+/* Enqueue a search on the ctx stream without synchronising. */
+int loom_search_argmin_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t begin, uint64_t end);
+/* Wait for the last enqueued search of dp and decode its result. */
+int loom_search_argmin_result(loom_ctx* ctx, loom_device_problem* dp, loom_winner* out);
+
+/* Pareto frontier of the plans in [begin, end) under pareto_filter's
+ * dominance (raw doubles: dollars, gpu_wh; latency_us; quality, higher
+ * better).  Indices are returned ascending (enumeration order).  Size query:
+ * call with capacity 0 to get *count. */
+int loom_search_pareto(loom_ctx* ctx, const loom_problem* problem, uint64_t begin, uint64_t end,
+                       uint64_t* out_index, uint64_t capacity, uint64_t* count);
+
+/* ---- the drop-in call on reference-format JSON -------------------------- */
+/* exhaustive_search(dag, library, objective, bounds) -> ConfigEstimate JSON:
+ * {"identifier","config","latency_us","gpu_wh","cpu_wh","total_wh","dollars",
+ *  "quality","plan_index","plans"}.  On error the JSON is {"error","message"}. */
+int loom_exhaustive_search_json(loom_ctx* ctx, const char* dag_json, const char* library_json,
+                                const char* objective_json, const char* bounds_json, char* out_json,
+                                size_t cap, size_t* needed);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOOM_B200_H */

@@ -1,0 +1,420 @@
+// Host half of the C ABI (no device code): errors, problem validation, the
+// exact single-plan estimate used to fill winners, the objective order over
+// winner records (multi-rank combine), reference-format JSON lowering, and the
+// drop-in entry points loom::exhaustive_search / loom_exhaustive_search_json.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "json.hpp"
+#include "loom_b200.h"
+#include "loom_b200/loom.hpp"
+
+namespace loomi {
+
+thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+int fail(int status, const std::string& msg) {
+  g_error = msg;
+  return status;
+}
+
+int check_problem(const loom_problem* p, uint64_t* total) {
+  if (!p) return fail(LOOM_INVALID, "InvalidConfigError: null problem");
+  if (p->n_nodes < 0 || p->n_edges < 0) return fail(LOOM_INVALID, "InvalidConfigError: negative sizes");
+  if (p->n_nodes == 0) {
+    *total = 0;  // empty dag: no configs (optimizer.hpp:120)
+    return LOOM_OK;
+  }
+  if (!p->radix) return fail(LOOM_INVALID, "InvalidConfigError: null radix");
+  uint64_t t = 1;
+  int64_t n_opts = 0;
+  for (int i = 0; i < p->n_nodes; ++i) {
+    if (p->radix[i] < 0) return fail(LOOM_INVALID, "InvalidConfigError: negative radix");
+    n_opts += p->radix[i];
+    if (p->radix[i] == 0) t = 0;
+    else if (t && t > UINT64_MAX / static_cast<uint64_t>(p->radix[i]))
+      return fail(LOOM_INVALID, "InvalidConfigError: plan space exceeds 2^64 plans");
+    else t *= static_cast<uint64_t>(p->radix[i]);
+  }
+  if (n_opts && (!p->wall_us || !p->gpu_wh || !p->cpu_wh || !p->dollars || !p->quality || !p->lexrank))
+    return fail(LOOM_INVALID, "InvalidConfigError: null option table");
+  if (!p->lex_weight) return fail(LOOM_INVALID, "InvalidConfigError: null lex_weight");
+  if (p->n_edges && (!p->edge_from || !p->edge_to)) return fail(LOOM_INVALID, "InvalidConfigError: null edges");
+  for (int e = 0; e < p->n_edges; ++e)
+    if (p->edge_from[e] < 0 || p->edge_from[e] >= p->n_nodes || p->edge_to[e] < 0 || p->edge_to[e] >= p->n_nodes)
+      return fail(LOOM_INVALID, "CycleError: edge references unknown node");
+  *total = t;
+  return LOOM_OK;
+}
+
+namespace {
+
+std::vector<int> topo(const loom_problem* p) {
+  const int n = p->n_nodes;
+  std::vector<int> indeg(n, 0), order;
+  std::vector<std::vector<int>> succ(n);
+  for (int e = 0; e < p->n_edges; ++e) {
+    succ[p->edge_from[e]].push_back(p->edge_to[e]);
+    ++indeg[p->edge_to[e]];
+  }
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) order.push_back(i);
+  for (std::size_t k = 0; k < order.size(); ++k)
+    for (int s : succ[order[k]])
+      if (--indeg[s] == 0) order.push_back(s);
+  return order;
+}
+
+}  // namespace
+
+int fill_winner(const loom_problem* p, loom_winner* w) {
+  uint64_t total = 0;
+  if (int rc = check_problem(p, &total)) return rc;
+  if (w->plan_index >= total) return fail(LOOM_INVALID, "InvalidConfigError: plan index out of range");
+  const int n = p->n_nodes;
+  std::vector<int> opt(n), off(n + 1, 0);
+  for (int i = 0; i < n; ++i) off[i + 1] = off[i] + p->radix[i];
+  uint64_t x = w->plan_index;
+  for (int i = n - 1; i >= 0; --i) {
+    opt[i] = off[i] + static_cast<int>(x % static_cast<uint64_t>(p->radix[i]));
+    x /= static_cast<uint64_t>(p->radix[i]);
+  }
+  // estimator.hpp:46-67: left folds in dag.nodes order starting from 0.0
+  double gpu = 0.0, cpu = 0.0, dol = 0.0;
+  int q = INT_MAX;
+  uint64_t lex = 0;
+  for (int i = 0; i < n; ++i) {
+    gpu += p->gpu_wh[opt[i]];
+    cpu += p->cpu_wh[opt[i]];
+    dol += p->dollars[opt[i]];
+    q = std::min(q, p->quality[opt[i]]);
+    lex += static_cast<uint64_t>(p->lexrank[opt[i]]) * p->lex_weight[i];
+  }
+  // estimator.hpp:69-76: finish(v) = max over in-edges of finish(u) + wall(v)
+  std::vector<std::vector<int>> preds(n);
+  for (int e = 0; e < p->n_edges; ++e) preds[p->edge_to[e]].push_back(p->edge_from[e]);
+  const std::vector<int> order = topo(p);
+  if (static_cast<int>(order.size()) != n) return fail(LOOM_INVALID, "CycleError: dag has a cycle");
+  std::vector<int64_t> fin(n, 0);
+  int64_t lat = 0;
+  for (int v : order) {
+    int64_t s = 0;
+    for (int u : preds[v]) s = std::max(s, fin[u]);
+    fin[v] = s + p->wall_us[opt[v]];
+    lat = std::max(lat, fin[v]);
+  }
+  w->latency_us = lat;
+  w->gpu_wh = gpu;
+  w->cpu_wh = cpu;
+  w->total_wh = gpu + cpu;
+  w->dollars = dol;
+  w->quality = q;
+  w->lexkey = lex;
+  w->found = 1;
+  return LOOM_OK;
+}
+
+}  // namespace loomi
+
+namespace {
+
+std::int64_t quantize(double v) { return static_cast<std::int64_t>(std::llround(v * 1e9)); }
+
+int status_of(const loom::Error& e) {
+  if (e.code() == "NoFeasibleConfigError") return LOOM_INFEASIBLE;
+  return LOOM_INVALID;
+}
+
+loom_objective to_objective(const loom::ObjectiveHierarchy& h, std::optional<loom::Micros> slo) {
+  loom_objective o;
+  std::memset(&o, 0, sizeof o);
+  if (h.criteria.size() > 4) throw loom::InvalidConfigError("more than 4 criteria");
+  o.n_criteria = static_cast<int32_t>(h.criteria.size());
+  for (std::size_t i = 0; i < h.criteria.size(); ++i) {
+    switch (h.criteria[i]) {
+      case loom::Criterion::min_cost_dollars: o.criteria[i] = LOOM_MIN_COST_DOLLARS; break;
+      case loom::Criterion::min_energy: o.criteria[i] = LOOM_MIN_ENERGY; break;
+      case loom::Criterion::min_latency: o.criteria[i] = LOOM_MIN_LATENCY; break;
+      case loom::Criterion::max_quality: o.criteria[i] = LOOM_MAX_QUALITY; break;
+    }
+  }
+  if (h.quality_floor) {
+    o.has_quality_floor = 1;
+    o.quality_floor = *h.quality_floor;
+  }
+  if (slo) {
+    o.has_latency_slo = 1;
+    o.latency_slo_us = *slo;
+  }
+  return o;
+}
+
+struct ParsedObjective {
+  loom::ObjectiveHierarchy hierarchy;
+  std::optional<loom::Micros> slo;
+};
+
+ParsedObjective parse_objective_json(const std::string& text) {
+  ParsedObjective out;
+  loomjson::Value j;
+  try {
+    j = loomjson::parse(text);
+  } catch (const loomjson::ParseError& e) {
+    throw loom::SchemaError(std::string("malformed objective: ") + e.what());
+  }
+  try {
+    if (const loomjson::Value* c = j.find("criteria")) {
+      for (const auto& v : c->items()) {
+        const std::string& s = v.as_string("criteria");
+        if (s == "min_cost_dollars") out.hierarchy.criteria.push_back(loom::Criterion::min_cost_dollars);
+        else if (s == "min_energy") out.hierarchy.criteria.push_back(loom::Criterion::min_energy);
+        else if (s == "min_latency") out.hierarchy.criteria.push_back(loom::Criterion::min_latency);
+        else if (s == "max_quality") out.hierarchy.criteria.push_back(loom::Criterion::max_quality);
+        else throw loom::SchemaError("unknown criterion '" + s + "'");
+      }
+    } else {
+      out.hierarchy = loom::objective_from_token(j.at("constraint").as_string("constraint"));
+    }
+    if (const loomjson::Value* f = j.find("quality_floor"); f && !f->is_null())
+      out.hierarchy.quality_floor = static_cast<int>(f->as_int("quality_floor"));
+    if (const loomjson::Value* s = j.find("latency_slo_us"); s && !s->is_null())
+      out.slo = s->as_int("latency_slo_us");
+  } catch (const loomjson::ParseError& e) {
+    throw loom::SchemaError(std::string("objective: ") + e.what());
+  }
+  return out;
+}
+
+int copy_out(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+    if (n < s.size()) return loomi::fail(LOOM_INVALID, "InvalidConfigError: output buffer too small");
+  }
+  return LOOM_OK;
+}
+
+std::string estimate_json(const loom::ConfigEstimate& e, uint64_t plan_index, uint64_t plans) {
+  using loomjson::Value;
+  Value v = Value::make_object();
+  v.set("identifier", Value::make_string(e.config.identifier()));
+  v.set("config", loomjson::parse(e.config.to_json_text()));
+  v.set("latency_us", Value::make_int(e.latency_us));
+  v.set("gpu_wh", Value::make_real(e.gpu_wh));
+  v.set("cpu_wh", Value::make_real(e.cpu_wh));
+  v.set("total_wh", Value::make_real(e.total_wh));
+  v.set("dollars", Value::make_real(e.dollars));
+  v.set("quality", Value::make_int(e.quality));
+  v.set("plan_index", Value::make_int(static_cast<int64_t>(plan_index)));
+  v.set("plans", Value::make_int(static_cast<int64_t>(plans)));
+  return v.dump();
+}
+
+std::string error_json(const std::string& what) {
+  using loomjson::Value;
+  Value v = Value::make_object();
+  const auto colon = what.find(':');
+  v.set("error", Value::make_string(colon == std::string::npos ? "Error" : what.substr(0, colon)));
+  v.set("message", Value::make_string(what));
+  return v.dump();
+}
+
+}  // namespace
+
+struct loom_lowered {
+  loom::LoweredProblem L;
+  loom_problem view;
+};
+
+namespace loom {
+
+// Process-wide context for the 4-argument overload (device 0, own stream).
+namespace {
+std::mutex g_ctx_mu;
+loom_ctx* g_ctx = nullptr;
+}  // namespace
+
+ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
+                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds) {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  if (!g_ctx && loom_ctx_create(0, nullptr, &g_ctx) != LOOM_OK)
+    throw std::runtime_error(loom_last_error());
+  return exhaustive_search(dag, library, objective, bounds, g_ctx);
+}
+
+ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
+                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds, loom_ctx* ctx,
+                                 std::optional<Micros> latency_slo_us) {
+  const LoweredProblem L = lower(dag, library, bounds);
+  if (L.total == 0) throw NoFeasibleConfigError("no configuration satisfies the quality floor and bounds");
+  const loom_problem view = L.view();
+  const loom_objective obj = to_objective(objective, latency_slo_us);
+  loom_winner w;
+  const int rc = loom_search_argmin(ctx, &view, &obj, 0, L.total, &w);
+  if (rc == LOOM_INFEASIBLE) throw NoFeasibleConfigError("no configuration satisfies the quality floor and bounds");
+  if (rc != LOOM_OK) throw std::runtime_error(loom_last_error());
+  // The selected plan is re-estimated with the reference arithmetic on the
+  // reference types; the GPU's latency and identifier rank must agree.
+  ConfigEstimate e = estimate(L.config_of(w.plan_index), dag, library);
+  if (e.latency_us != w.latency_us || e.gpu_wh != w.gpu_wh || e.dollars != w.dollars)
+    throw std::runtime_error("DeviceError: GPU winner disagrees with host estimate");
+  return e;
+}
+
+}  // namespace loom
+
+extern "C" {
+
+int loom_abi_version(void) { return LOOM_B200_ABI_VERSION; }
+
+const char* loom_last_error(void) { return loomi::g_error.c_str(); }
+
+int loom_problem_total(const loom_problem* p, uint64_t* total) {
+  if (!total) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null out");
+  return loomi::check_problem(p, total);
+}
+
+int loom_evaluate_plan(const loom_problem* p, uint64_t plan_index, loom_winner* out) {
+  if (!out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null out");
+  std::memset(out, 0, sizeof *out);
+  out->plan_index = plan_index;
+  return loomi::fill_winner(p, out);
+}
+
+int loom_winner_less(const loom_winner* a, const loom_winner* b, const loom_objective* o) {
+  if (!a->found) return 0;
+  if (!b->found) return 1;
+  for (int i = 0; i < o->n_criteria; ++i) {
+    switch (o->criteria[i]) {
+      case LOOM_MIN_COST_DOLLARS:
+        if (quantize(a->dollars) != quantize(b->dollars)) return quantize(a->dollars) < quantize(b->dollars);
+        break;
+      case LOOM_MIN_ENERGY:
+        if (quantize(a->gpu_wh) != quantize(b->gpu_wh)) return quantize(a->gpu_wh) < quantize(b->gpu_wh);
+        break;
+      case LOOM_MIN_LATENCY:
+        if (a->latency_us != b->latency_us) return a->latency_us < b->latency_us;
+        break;
+      default:
+        if (a->quality != b->quality) return a->quality > b->quality;
+        break;
+    }
+  }
+  return a->lexkey < b->lexkey;
+}
+
+int loom_winner_reduce(const loom_winner* ws, int32_t n, const loom_objective* o, loom_winner* out) {
+  if (!out || !o || (n > 0 && !ws)) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  std::memset(out, 0, sizeof *out);
+  for (int i = 0; i < n; ++i)
+    if (loom_winner_less(&ws[i], out, o)) *out = ws[i];
+  if (!out->found)
+    return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+  return LOOM_OK;
+}
+
+int loom_objective_parse(const char* text, loom_objective* out) {
+  if (!text || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  try {
+    const ParsedObjective p = parse_objective_json(text);
+    *out = to_objective(p.hierarchy, p.slo);
+    return LOOM_OK;
+  } catch (const loom::Error& e) {
+    return loomi::fail(status_of(e), e.what());
+  }
+}
+
+int loom_lower(const char* dag_json, const char* library_json, const char* bounds_json, loom_lowered** out) {
+  if (!out || !dag_json || !library_json || !bounds_json)
+    return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  *out = nullptr;
+  try {
+    auto lw = std::make_unique<loom_lowered>();
+    lw->L = loom::lower(loom::WorkflowDag::from_json_text(dag_json), loom::AgentLibrary::from_json_text(library_json),
+                        loom::SearchBounds::from_json_text(bounds_json));
+    lw->view = lw->L.view();
+    *out = lw.release();
+    return LOOM_OK;
+  } catch (const loom::Error& e) {
+    return loomi::fail(status_of(e), e.what());
+  } catch (const std::exception& e) {
+    return loomi::fail(LOOM_INVALID, std::string("InvalidConfigError: ") + e.what());
+  }
+}
+
+const loom_problem* loom_lowered_problem(const loom_lowered* lw) { return lw ? &lw->view : nullptr; }
+
+int loom_lowered_config_json(const loom_lowered* lw, uint64_t plan_index, char* buf, size_t cap, size_t* needed) {
+  if (!lw) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null lowered");
+  if (plan_index >= lw->L.total) return loomi::fail(LOOM_INVALID, "InvalidConfigError: plan index out of range");
+  const loom::ConfigPoint c = lw->L.config_of(plan_index);
+  loomjson::Value v = loomjson::parse(c.to_json_text());
+  v.set("identifier", loomjson::Value::make_string(c.identifier()));
+  return copy_out(v.dump(), buf, cap, needed);
+}
+
+int loom_lowered_option_json(const loom_lowered* lw, int32_t node, int32_t option, char* buf, size_t cap,
+                             size_t* needed) {
+  if (!lw) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null lowered");
+  if (node < 0 || node >= static_cast<int>(lw->L.options.size()) || option < 0 ||
+      option >= static_cast<int>(lw->L.options[node].size()))
+    return loomi::fail(LOOM_INVALID, "InvalidConfigError: option out of range");
+  loom::ConfigPoint c;
+  c.nodes[lw->L.node_ids[node]] = lw->L.options[node][option];
+  loomjson::Value v = loomjson::parse(c.to_json_text()).at("nodes").at(lw->L.node_ids[node]);
+  v.set("identifier", loomjson::Value::make_string(c.identifier()));
+  return copy_out(v.dump(), buf, cap, needed);
+}
+
+void loom_lowered_destroy(loom_lowered* lw) { delete lw; }
+
+int loom_exhaustive_search_json(loom_ctx* ctx, const char* dag_json, const char* library_json,
+                                const char* objective_json, const char* bounds_json, char* out_json, size_t cap,
+                                size_t* needed) {
+  int rc = LOOM_OK;
+  std::string result;
+  try {
+    const loom::WorkflowDag dag = loom::WorkflowDag::from_json_text(dag_json ? dag_json : "");
+    const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json ? library_json : "");
+    const loom::SearchBounds bounds = loom::SearchBounds::from_json_text(bounds_json ? bounds_json : "{}");
+    const ParsedObjective obj = parse_objective_json(objective_json ? objective_json : "");
+    const loom::LoweredProblem L = loom::lower(dag, lib, bounds);
+    if (L.total == 0) throw loom::NoFeasibleConfigError("no configuration satisfies the quality floor and bounds");
+    const loom_problem view = L.view();
+    const loom_objective o = to_objective(obj.hierarchy, obj.slo);
+    loom_winner w;
+    rc = loom_search_argmin(ctx, &view, &o, 0, L.total, &w);
+    if (rc == LOOM_OK) {
+      const loom::ConfigEstimate e = loom::estimate(L.config_of(w.plan_index), dag, lib);
+      if (e.latency_us != w.latency_us || e.gpu_wh != w.gpu_wh || e.dollars != w.dollars)
+        rc = loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: GPU winner disagrees with host estimate");
+      else
+        result = estimate_json(e, w.plan_index, L.total);
+    }
+    if (rc != LOOM_OK) result = error_json(loom_last_error());
+  } catch (const loom::Error& e) {
+    rc = loomi::fail(status_of(e), e.what());
+    result = error_json(e.what());
+  } catch (const std::exception& e) {
+    rc = loomi::fail(LOOM_INVALID, std::string("InvalidConfigError: ") + e.what());
+    result = error_json(loom_last_error());
+  }
+  const std::string err = loom_last_error();
+  const int crc = copy_out(result, out_json, cap, needed);
+  if (rc == LOOM_OK) return crc;
+  loomi::set_error(err);
+  return rc;
+}
+
+}  // extern "C"

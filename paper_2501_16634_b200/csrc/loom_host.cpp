@@ -1,0 +1,688 @@
+// Host side of the drop-in: reference-format parsing, the per-node lowering
+// (node_options + plan_node_execution + identifier ranks) and the exact
+// single-plan arithmetic used to fill the winner.  Everything here runs once
+// per search or once per winner; the per-plan loop is on the GPU
+// (loom_search.cu).
+//
+// Reference lines followed (paths under /root/reference/proj/include/loom/):
+//   to_micros                time.hpp:15-17
+//   chunk_capacity           chunking.hpp:26-29
+//   split_task               chunking.hpp:17-24
+//   water_fill_split         chunking.hpp:35-58
+//   plan_node_execution      chunking.hpp:85-184
+//   placement_fits           optimizer.hpp:31-43
+//   node_options             optimizer.hpp:51-107
+//   implementations_for      agent_library.hpp:273-289
+//   profiles_for             agent_library.hpp:291-297
+//   node_quality             estimator.hpp:32-37
+//   estimate                 estimator.hpp:43-78
+//   quantize/objective_less  estimator.hpp:85-116
+//   meets_quality_floor      estimator.hpp:118-121
+//   pareto_filter            optimizer.hpp:153-171
+//   identifier               config.hpp:49-61
+//   objective_from_token     workflow.hpp:91-106
+//   topological_order        workflow.hpp:467-498
+//
+// Build note: compiled with -ffp-contract=off so that products such as
+// units * watts * hours round exactly like the reference's default x86-64
+// (SSE2, no FMA) build.
+#include "loom_b200/loom.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <numeric>
+#include <queue>
+#include <sstream>
+
+#include "json.hpp"
+
+namespace loom {
+
+using loomjson::Value;
+
+Micros to_micros(double seconds) { return static_cast<Micros>(std::llround(seconds * 1e6)); }
+
+Error::Error(ErrorCategory category, std::string code, const std::string& message)
+    : std::runtime_error(code + ": " + message), category_(category), code_(std::move(code)) {}
+
+// ---------------------------------------------------------------------------
+// library bundle
+// ---------------------------------------------------------------------------
+namespace {
+
+HardwareClass class_of(const std::string& s) {
+  if (s == "cpu") return HardwareClass::cpu;
+  if (s == "gpu") return HardwareClass::gpu;
+  throw SchemaError("unknown hardware class '" + s + "'");
+}
+
+const Value& array_or_empty(const Value& j, const char* key) {
+  static const Value empty = Value::make_array();
+  const Value* v = j.find(key);
+  return v ? *v : empty;
+}
+
+double num_or(const Value& j, const char* key, double dflt) {
+  const Value* v = j.find(key);
+  return v ? v->as_double(key) : dflt;
+}
+
+}  // namespace
+
+void AgentLibrary::add_capability(const std::string& capability) {
+  if (capabilities_.count(capability))
+    throw DuplicateKeyError("agent '" + capability + "' is already registered");
+  capabilities_[capability] = true;
+}
+
+void AgentLibrary::add_sku(HardwareSku s) {
+  if (s.busy_watts_per_unit < 0 || s.idle_watts_per_unit < 0 || s.dollars_per_unit_hour < 0)
+    throw ValidationError("sku '" + s.id + "': power and rate must be >= 0");
+  if (s.busy_watts_per_unit < s.idle_watts_per_unit)
+    throw ValidationError("sku '" + s.id + "': busy power must be >= idle power");
+  if (skus_.count(s.id)) throw DuplicateKeyError("sku '" + s.id + "' is already registered");
+  skus_.emplace(s.id, std::move(s));
+}
+
+void AgentLibrary::add_implementation(Implementation impl) {
+  if (!impl.supports_cpu && !impl.supports_gpu)
+    throw ValidationError("implementation '" + impl.name + "': must support at least one hardware class");
+  if (impl.quality < 0) throw ValidationError("implementation '" + impl.name + "': quality must be >= 0");
+  if (!capabilities_.count(impl.capability))
+    throw DanglingReferenceError("implementation '" + impl.name + "' references unknown capability '" +
+                                 impl.capability + "'");
+  if (impls_.count(impl.name))
+    throw DuplicateKeyError("implementation '" + impl.name + "' is already registered");
+  impls_.emplace(impl.name, std::move(impl));
+}
+
+void AgentLibrary::add_profile(ExecutionProfile p) {
+  const std::string who = "profile (" + p.implementation + ", " + p.sku + ")";
+  if (p.throughput <= 0) throw ValidationError(who + ": throughput must be > 0");
+  if (p.setup_seconds < 0) throw ValidationError(who + ": setup latency must be >= 0");
+  if (p.units < 1) throw ValidationError(who + ": units must be >= 1");
+  if (!impls_.count(p.implementation))
+    throw DanglingReferenceError("profile references unknown implementation '" + p.implementation + "'");
+  if (!skus_.count(p.sku)) throw DanglingReferenceError("profile references unknown sku '" + p.sku + "'");
+  auto key = std::make_tuple(p.implementation, p.sku, p.units);
+  if (profiles_.count(key))
+    throw DuplicateKeyError("profile (" + p.implementation + ", " + p.sku + ", " +
+                            std::to_string(p.units) + ") is already registered");
+  profiles_.emplace(std::move(key), std::move(p));
+}
+
+AgentLibrary AgentLibrary::from_json_text(const std::string& text) {
+  AgentLibrary lib;
+  try {
+    const Value j = loomjson::parse(text);
+    for (const Value& s : array_or_empty(j, "skus").items()) {
+      HardwareSku sku;
+      sku.id = s.at("id").as_string("id");
+      sku.hardware_class = class_of(s.at("class").as_string("class"));
+      sku.busy_watts_per_unit = s.at("busy_watts_per_unit").as_double("busy_watts_per_unit");
+      sku.idle_watts_per_unit = s.at("idle_watts_per_unit").as_double("idle_watts_per_unit");
+      sku.dollars_per_unit_hour = s.at("dollars_per_unit_hour").as_double("dollars_per_unit_hour");
+      lib.add_sku(std::move(sku));
+    }
+    for (const Value& a : array_or_empty(j, "agents").items())
+      lib.add_capability(a.at("capability").as_string("capability"));
+    for (const Value& i : array_or_empty(j, "implementations").items()) {
+      Implementation impl;
+      impl.name = i.at("name").as_string("name");
+      impl.capability = i.at("capability").as_string("capability");
+      impl.quality = static_cast<int>(i.at("quality").as_int("quality"));
+      for (const Value& c : i.at("supported_classes").items()) {
+        if (class_of(c.as_string("supported_classes")) == HardwareClass::cpu) impl.supports_cpu = true;
+        else impl.supports_gpu = true;
+      }
+      lib.add_implementation(std::move(impl));
+    }
+    for (const Value& p : array_or_empty(j, "profiles").items()) {
+      ExecutionProfile prof;
+      prof.implementation = p.at("implementation").as_string("implementation");
+      prof.sku = p.at("sku").as_string("sku");
+      prof.units = static_cast<int>(p.at("units").as_int("units"));
+      prof.throughput = p.at("throughput").as_double("throughput");
+      prof.setup_seconds = num_or(p, "setup_seconds", 0.0);
+      lib.add_profile(std::move(prof));
+    }
+  } catch (const loomjson::ParseError& e) {
+    throw SchemaError(std::string("malformed library bundle: ") + e.what());
+  }
+  return lib;
+}
+
+const HardwareSku* AgentLibrary::sku(const std::string& id) const {
+  auto it = skus_.find(id);
+  return it == skus_.end() ? nullptr : &it->second;
+}
+const Implementation* AgentLibrary::implementation(const std::string& name) const {
+  auto it = impls_.find(name);
+  return it == impls_.end() ? nullptr : &it->second;
+}
+const ExecutionProfile* AgentLibrary::profile(const std::string& impl, const std::string& sku, int units) const {
+  auto it = profiles_.find(std::make_tuple(impl, sku, units));
+  return it == profiles_.end() ? nullptr : &it->second;
+}
+
+std::vector<const Implementation*> AgentLibrary::implementations_for(const std::string& capability) const {
+  if (!capabilities_.count(capability))
+    throw UnknownCapabilityError("capability '" + capability + "' is not registered");
+  std::vector<const Implementation*> out;
+  for (const auto& kv : impls_)
+    if (kv.second.capability == capability) out.push_back(&kv.second);
+  std::sort(out.begin(), out.end(), [](const Implementation* a, const Implementation* b) {
+    return a->quality != b->quality ? a->quality > b->quality : a->name < b->name;
+  });
+  return out;
+}
+
+std::vector<const ExecutionProfile*> AgentLibrary::profiles_for(const std::string& implementation) const {
+  std::vector<const ExecutionProfile*> out;
+  // The map key is (implementation, sku, units): start at the first key of
+  // this implementation and walk while it matches.
+  for (auto it = profiles_.lower_bound(std::make_tuple(implementation, std::string(), INT_MIN));
+       it != profiles_.end() && std::get<0>(it->first) == implementation; ++it)
+    out.push_back(&it->second);
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// dag / bounds / objective
+// ---------------------------------------------------------------------------
+WorkflowDag WorkflowDag::from_json_text(const std::string& text) {
+  WorkflowDag dag;
+  try {
+    const Value j = loomjson::parse(text);
+    for (const Value& n : j.at("nodes").items()) {
+      DagNode node;
+      node.id = n.at("id").as_string("id");
+      node.capability = n.at("capability").as_string("capability");
+      node.work_units = n.at("work_units").as_double("work_units");
+      node.splittable = n.at("splittable").as_bool("splittable");
+      node.min_chunk = num_or(n, "min_chunk", 0.0);
+      if (const Value* mp = n.find("multi_path")) node.multi_path = mp->as_bool("multi_path");
+      if (const Value* c = n.find("path_quality_ceiling"); c && !c->is_null())
+        node.path_quality_ceiling = static_cast<int>(c->as_int("path_quality_ceiling"));
+      dag.nodes.push_back(std::move(node));
+    }
+    for (const Value& e : j.at("edges").items())
+      dag.edges.push_back({e.at("from").as_string("from"), e.at("to").as_string("to")});
+  } catch (const loomjson::ParseError& e) {
+    throw SchemaError(std::string("malformed dag file: ") + e.what());
+  }
+  return dag;
+}
+
+SearchBounds SearchBounds::from_json_text(const std::string& text) {
+  SearchBounds b;
+  try {
+    const Value j = loomjson::parse(text);
+    if (const Value* v = j.find("max_fanout")) b.max_fanout = static_cast<int>(v->as_int("max_fanout"));
+    if (const Value* v = j.find("max_paths")) b.max_paths = static_cast<int>(v->as_int("max_paths"));
+    if (const Value* v = j.find("sku_pool_cap"))
+      for (const auto& [k, cap] : v->members()) b.sku_pool_cap[k] = static_cast<int>(cap.as_int(k.c_str()));
+    if (const Value* v = j.find("sku_total_cap"))
+      for (const auto& [k, cap] : v->members()) b.sku_total_cap[k] = static_cast<int>(cap.as_int(k.c_str()));
+  } catch (const loomjson::ParseError& e) {
+    throw SchemaError(std::string("malformed bounds: ") + e.what());
+  }
+  return b;
+}
+
+ObjectiveHierarchy objective_from_token(const std::string& token) {
+  using C = Criterion;
+  ObjectiveHierarchy h;
+  if (token == "MIN_COST") h.criteria = {C::min_energy, C::min_latency};
+  else if (token == "MIN_DOLLARS") h.criteria = {C::min_cost_dollars, C::min_latency};
+  else if (token == "MIN_LATENCY") h.criteria = {C::min_latency, C::min_energy};
+  else if (token == "MAX_QUALITY") h.criteria = {C::max_quality, C::min_energy, C::min_latency};
+  else throw SchemaError("unknown constraint token '" + token + "'");
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+int NodeAssignment::fan_out() const {
+  int n = 0;
+  for (const Placement& p : placements) n += p.workers;
+  return n;
+}
+
+std::string assignment_token(const std::string& node_id, const NodeAssignment& a) {
+  std::string s = node_id + "=" + a.implementation + "[";
+  for (std::size_t i = 0; i < a.placements.size(); ++i) {
+    if (i) s += "+";
+    s += a.placements[i].sku + ":" + std::to_string(a.placements[i].units) + "x" +
+         std::to_string(a.placements[i].workers);
+  }
+  s += "]p" + std::to_string(a.path_count) + ";";
+  return s;
+}
+
+std::string ConfigPoint::identifier() const {
+  std::string s;
+  for (const auto& [id, a] : nodes) s += assignment_token(id, a);
+  return s;
+}
+
+namespace {
+Value assignment_json(const NodeAssignment& a) {
+  Value v = Value::make_object();
+  v.set("implementation", Value::make_string(a.implementation));
+  Value ps = Value::make_array();
+  for (const Placement& p : a.placements) {
+    Value pj = Value::make_object();
+    pj.set("sku", Value::make_string(p.sku));
+    pj.set("units", Value::make_int(p.units));
+    pj.set("workers", Value::make_int(p.workers));
+    ps.push(std::move(pj));
+  }
+  v.set("placements", std::move(ps));
+  v.set("path_count", Value::make_int(a.path_count));
+  return v;
+}
+}  // namespace
+
+std::string ConfigPoint::to_json_text() const {
+  Value v = Value::make_object();
+  v.set("label", Value::make_string(label));
+  Value ns = Value::make_object();
+  for (const auto& [id, a] : nodes) ns.set(id, assignment_json(a));
+  v.set("nodes", std::move(ns));
+  return v.dump();
+}
+
+// ---------------------------------------------------------------------------
+// chunking + node plan
+// ---------------------------------------------------------------------------
+int chunk_capacity(double work, double min_chunk) {
+  if (min_chunk <= 0) return 1;
+  return std::max(1, static_cast<int>(std::floor(work / min_chunk)));
+}
+
+namespace {
+// Equal split: count = clamp(min(fan_out, floor(work / min_chunk)), 1, ..).
+std::vector<double> equal_split(double work, int fan_out, double min_chunk) {
+  int count = 1;
+  if (fan_out > 1 && min_chunk > 0)
+    count = std::max(1, std::min(fan_out, static_cast<int>(std::floor(work / min_chunk))));
+  return std::vector<double>(static_cast<std::size_t>(count), work / count);
+}
+}  // namespace
+
+std::vector<double> water_fill_split(double work, double min_chunk, const std::vector<double>& speeds) {
+  // Quanta of work/quanta each go to the worker that would finish it first;
+  // strict '<' keeps ties on the lower worker index.
+  const int quanta = chunk_capacity(work, min_chunk);
+  const double quantum = work / quanta;
+  std::vector<double> done_at(speeds.size(), 0.0);
+  std::vector<int> taken(speeds.size(), 0);
+  for (int q = 0; q < quanta; ++q) {
+    std::size_t pick = 0;
+    double pick_t = done_at[0] + quantum / speeds[0];
+    for (std::size_t w = 1; w < speeds.size(); ++w) {
+      const double t = done_at[w] + quantum / speeds[w];
+      if (t < pick_t) {
+        pick = w;
+        pick_t = t;
+      }
+    }
+    done_at[pick] = pick_t;
+    ++taken[pick];
+  }
+  std::vector<double> out(speeds.size());
+  for (std::size_t w = 0; w < speeds.size(); ++w) out[w] = taken[w] * quantum;
+  return out;
+}
+
+int node_quality(const DagNode& node, const Implementation& impl, int path_count) {
+  const int q = impl.quality + (path_count - 1);
+  return node.path_quality_ceiling ? std::min(q, *node.path_quality_ceiling) : q;
+}
+
+NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const AgentLibrary& library) {
+  const std::string where = "node '" + node.id + "'";
+  const Implementation* impl = library.implementation(a.implementation);
+  if (!impl) throw InvalidConfigError(where + ": unknown implementation '" + a.implementation + "'");
+  if (impl->capability != node.capability)
+    throw InvalidConfigError(where + ": implementation '" + impl->name + "' realizes '" + impl->capability +
+                             "', not '" + node.capability + "'");
+  if (a.placements.empty()) throw InvalidConfigError(where + ": no placements");
+  if (a.path_count < 1) throw InvalidConfigError(where + ": path_count must be >= 1");
+  if (a.path_count > 1 && !node.multi_path)
+    throw InvalidConfigError(where + " is not flagged multi-path in the lexicon");
+  const int fan = a.fan_out();
+  if (fan > 1 && !node.splittable) throw InvalidConfigError(where + " is not splittable; fan-out must be 1");
+
+  struct Worker {
+    const ExecutionProfile* profile;
+    const HardwareSku* sku;
+  };
+  std::vector<Worker> workers;
+  for (const Placement& p : a.placements) {
+    const HardwareSku* sku = library.sku(p.sku);
+    if (!sku) throw InvalidConfigError(where + ": unknown sku '" + p.sku + "'");
+    if (!impl->supports(sku->hardware_class))
+      throw InvalidConfigError(where + ": implementation '" + impl->name + "' does not support " +
+                               (sku->hardware_class == HardwareClass::gpu ? "gpu" : "cpu") + " sku '" +
+                               sku->id + "'");
+    const ExecutionProfile* prof = library.profile(impl->name, sku->id, p.units);
+    if (!prof)
+      throw InvalidConfigError(where + ": no profile for (" + impl->name + ", " + sku->id + ", " +
+                               std::to_string(p.units) + ")");
+    if (p.workers < 1) throw InvalidConfigError(where + ": workers must be >= 1");
+    for (int w = 0; w < p.workers; ++w) workers.push_back({prof, sku});
+  }
+
+  std::vector<double> chunk;
+  if (workers.size() == 1) {
+    chunk = {node.work_units};
+  } else if (a.placements.size() <= 1) {
+    chunk = equal_split(node.work_units, fan, node.min_chunk);
+    if (static_cast<int>(chunk.size()) != fan)
+      throw InvalidConfigError(where + ": fan-out " + std::to_string(fan) + " exceeds the chunk capacity of " +
+                               std::to_string(chunk_capacity(node.work_units, node.min_chunk)));
+  } else {
+    std::vector<double> speeds;
+    for (const Worker& w : workers) speeds.push_back(w.profile->throughput);
+    chunk = water_fill_split(node.work_units, node.min_chunk, speeds);
+    for (double c : chunk)
+      if (c <= 0.0 && node.work_units > 0.0)
+        throw InvalidConfigError(where + ": degenerate hybrid placement; a worker receives no work");
+  }
+
+  NodePlan plan;
+  for (std::size_t w = 0; w < workers.size(); ++w) {
+    const Worker& r = workers[w];
+    const Micros setup = to_micros(r.profile->setup_seconds);
+    const Micros run = to_micros(chunk[w] / r.profile->throughput);
+    const Micros dur = setup + run;
+    plan.wall_us = std::max(plan.wall_us, dur);
+    const double hours = to_seconds(dur) / 3600.0;
+    const double units = static_cast<double>(r.profile->units);
+    const double wh = units * r.sku->busy_watts_per_unit * hours;
+    if (r.sku->hardware_class == HardwareClass::gpu) plan.gpu_wh += wh;
+    else plan.cpu_wh += wh;
+    plan.dollars += units * r.sku->dollars_per_unit_hour * hours;
+  }
+  return plan;
+}
+
+// ---------------------------------------------------------------------------
+// lever enumeration
+// ---------------------------------------------------------------------------
+namespace {
+// A single allocation must fit the largest pool of its sku and the whole
+// worker set must fit the sku's total; a non-empty cap map excludes skus it
+// does not list.
+bool fits(const SearchBounds& b, const std::string& sku, int units, int total_units) {
+  if (!b.sku_pool_cap.empty()) {
+    auto it = b.sku_pool_cap.find(sku);
+    if (it == b.sku_pool_cap.end() || units > it->second) return false;
+  }
+  if (!b.sku_total_cap.empty()) {
+    auto it = b.sku_total_cap.find(sku);
+    if (it == b.sku_total_cap.end() || total_units > it->second) return false;
+  }
+  return true;
+}
+}  // namespace
+
+std::vector<NodeAssignment> node_options(const DagNode& node, const AgentLibrary& library,
+                                         const SearchBounds& bounds) {
+  std::vector<NodeAssignment> out;
+  const int paths_max = node.multi_path ? std::max(1, bounds.max_paths) : 1;
+  const int fan_cap =
+      node.splittable ? std::min(bounds.max_fanout, chunk_capacity(node.work_units, node.min_chunk)) : 1;
+  const int fan_hi = std::max(1, fan_cap);
+  const bool hybrids = node.splittable && bounds.max_fanout >= 2;
+
+  auto emit = [&](const std::string& impl, std::vector<Placement> placements) {
+    for (int k = 1; k <= paths_max; ++k) out.push_back({impl, placements, k});
+  };
+
+  for (const Implementation* impl : library.implementations_for(node.capability)) {
+    std::vector<const ExecutionProfile*> usable;
+    for (const ExecutionProfile* p : library.profiles_for(impl->name))
+      if (impl->supports(library.sku(p->sku)->hardware_class)) usable.push_back(p);
+
+    for (const ExecutionProfile* p : usable)
+      for (int w = 1; w <= fan_hi; ++w)
+        if (fits(bounds, p->sku, p->units, p->units * w)) emit(impl->name, {{p->sku, p->units, w}});
+
+    if (!hybrids) continue;
+    for (const ExecutionProfile* g : usable) {
+      if (library.sku(g->sku)->hardware_class != HardwareClass::gpu) continue;
+      for (const ExecutionProfile* c : usable) {
+        if (library.sku(c->sku)->hardware_class != HardwareClass::cpu) continue;
+        if (!fits(bounds, g->sku, g->units, g->units) || !fits(bounds, c->sku, c->units, c->units)) continue;
+        const auto split = water_fill_split(node.work_units, node.min_chunk, {g->throughput, c->throughput});
+        if (node.work_units > 0 && (split[0] <= 0 || split[1] <= 0)) continue;
+        emit(impl->name, {{g->sku, g->units, 1}, {c->sku, c->units, 1}});
+      }
+    }
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// estimate / order (host copies used for the winner and for small API calls)
+// ---------------------------------------------------------------------------
+namespace {
+// Kahn's algorithm; any topological order gives the same integer critical
+// path, the reference's string-ordered peers (workflow.hpp:467-498) only
+// matter for determinism of its own iteration.
+std::vector<int> topo_order(int n, const std::vector<int32_t>& from, const std::vector<int32_t>& to) {
+  std::vector<int> indeg(n, 0);
+  std::vector<std::vector<int>> succ(n);
+  for (std::size_t e = 0; e < from.size(); ++e) {
+    succ[from[e]].push_back(to[e]);
+    ++indeg[to[e]];
+  }
+  std::priority_queue<int, std::vector<int>, std::greater<>> ready;
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) ready.push(i);
+  std::vector<int> order;
+  while (!ready.empty()) {
+    const int v = ready.top();
+    ready.pop();
+    order.push_back(v);
+    for (int s : succ[v])
+      if (--indeg[s] == 0) ready.push(s);
+  }
+  if (static_cast<int>(order.size()) != n) throw CycleError("dag has a cycle");
+  return order;
+}
+
+std::int64_t quantize(double v) { return static_cast<std::int64_t>(std::llround(v * 1e9)); }
+}  // namespace
+
+ConfigEstimate estimate(const ConfigPoint& config, const WorkflowDag& dag, const AgentLibrary& library) {
+  ConfigEstimate r;
+  r.config = config;
+  r.quality = INT_MAX;
+  std::map<std::string, int> index;
+  for (std::size_t i = 0; i < dag.nodes.size(); ++i) index[dag.nodes[i].id] = static_cast<int>(i);
+  std::vector<Micros> wall(dag.nodes.size(), 0);
+  for (std::size_t i = 0; i < dag.nodes.size(); ++i) {
+    const DagNode& node = dag.nodes[i];
+    auto it = config.nodes.find(node.id);
+    if (it == config.nodes.end()) throw InvalidConfigError("config does not cover node '" + node.id + "'");
+    const NodePlan plan = plan_node_execution(node, it->second, library);
+    wall[i] = plan.wall_us;
+    const double k = static_cast<double>(it->second.path_count);
+    r.gpu_wh += plan.gpu_wh * k;
+    r.cpu_wh += plan.cpu_wh * k;
+    r.dollars += plan.dollars * k;
+    r.quality = std::min(r.quality, node_quality(node, *library.implementation(it->second.implementation),
+                                                 it->second.path_count));
+  }
+  if (dag.nodes.empty()) r.quality = 0;
+  r.total_wh = r.gpu_wh + r.cpu_wh;
+  std::vector<int32_t> from, to;
+  for (const Edge& e : dag.edges) {
+    if (!index.count(e.from) || !index.count(e.to)) throw CycleError("edge references unknown node");
+    from.push_back(index[e.from]);
+    to.push_back(index[e.to]);
+  }
+  std::vector<std::vector<int>> preds(dag.nodes.size());
+  for (std::size_t e = 0; e < from.size(); ++e) preds[to[e]].push_back(from[e]);
+  std::vector<Micros> finish(dag.nodes.size(), 0);
+  for (int v : topo_order(static_cast<int>(dag.nodes.size()), from, to)) {
+    Micros start = 0;
+    for (int p : preds[v]) start = std::max(start, finish[p]);
+    finish[v] = start + wall[v];
+    r.latency_us = std::max(r.latency_us, finish[v]);
+  }
+  return r;
+}
+
+bool objective_less(const ConfigEstimate& a, const ConfigEstimate& b, const ObjectiveHierarchy& objective) {
+  for (Criterion c : objective.criteria) {
+    switch (c) {
+      case Criterion::min_cost_dollars:
+        if (quantize(a.dollars) != quantize(b.dollars)) return quantize(a.dollars) < quantize(b.dollars);
+        break;
+      case Criterion::min_energy:
+        if (quantize(a.gpu_wh) != quantize(b.gpu_wh)) return quantize(a.gpu_wh) < quantize(b.gpu_wh);
+        break;
+      case Criterion::min_latency:
+        if (a.latency_us != b.latency_us) return a.latency_us < b.latency_us;
+        break;
+      case Criterion::max_quality:
+        if (a.quality != b.quality) return a.quality > b.quality;
+        break;
+    }
+  }
+  return a.config.identifier() < b.config.identifier();
+}
+
+bool meets_quality_floor(const ConfigEstimate& e, const ObjectiveHierarchy& objective) {
+  return !objective.quality_floor || e.quality >= *objective.quality_floor;
+}
+
+std::vector<ConfigEstimate> pareto_filter(const std::vector<ConfigEstimate>& in) {
+  auto dominates = [](const ConfigEstimate& a, const ConfigEstimate& b) {
+    const bool le = a.dollars <= b.dollars && a.gpu_wh <= b.gpu_wh && a.latency_us <= b.latency_us &&
+                    a.quality >= b.quality;
+    const bool lt = a.dollars < b.dollars || a.gpu_wh < b.gpu_wh || a.latency_us < b.latency_us ||
+                    a.quality > b.quality;
+    return le && lt;
+  };
+  std::vector<ConfigEstimate> kept;
+  for (std::size_t i = 0; i < in.size(); ++i) {
+    bool beaten = false;
+    for (std::size_t j = 0; j < in.size() && !beaten; ++j) beaten = j != i && dominates(in[j], in[i]);
+    if (!beaten) kept.push_back(in[i]);
+  }
+  return kept;
+}
+
+// ---------------------------------------------------------------------------
+// lowering
+// ---------------------------------------------------------------------------
+LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const SearchBounds& bounds) {
+  LoweredProblem L;
+  const int n = static_cast<int>(dag.nodes.size());
+  std::map<std::string, int> index;
+  for (int i = 0; i < n; ++i) {
+    if (!index.emplace(dag.nodes[i].id, i).second)
+      throw InvalidConfigError("duplicate node id '" + dag.nodes[i].id + "'");
+    L.node_ids.push_back(dag.nodes[i].id);
+  }
+  for (const Edge& e : dag.edges) {
+    auto f = index.find(e.from), t = index.find(e.to);
+    if (f == index.end() || t == index.end()) throw CycleError("edge references unknown node");
+    L.edge_from.push_back(f->second);
+    L.edge_to.push_back(t->second);
+  }
+  topo_order(n, L.edge_from, L.edge_to);  // throws CycleError like topological_order
+
+  // The identifier tie-break is replaced by a per-node rank of the option's
+  // identifier substring.  That is exact only if no substring is a proper
+  // prefix of another one, which holds when names carry no ';'.
+  auto check_name = [](const std::string& s) {
+    if (s.find(';') != std::string::npos)
+      throw InvalidConfigError("name '" + s + "' contains ';', which breaks identifier ordering");
+  };
+
+  L.total = n ? 1 : 0;
+  for (int i = 0; i < n; ++i) {
+    const DagNode& node = dag.nodes[i];
+    check_name(node.id);
+    std::vector<NodeAssignment> opts = node_options(node, library, bounds);
+    const int r = static_cast<int>(opts.size());
+    L.radix.push_back(r);
+    if (r == 0) L.total = 0;
+    else if (L.total && L.total > UINT64_MAX / static_cast<uint64_t>(r))
+      throw InvalidConfigError("plan space exceeds 2^64 plans");
+    else L.total *= static_cast<uint64_t>(r);
+
+    std::vector<std::string> tokens;
+    for (const NodeAssignment& a : opts) {
+      check_name(a.implementation);
+      for (const Placement& p : a.placements) check_name(p.sku);
+      const NodePlan plan = plan_node_execution(node, a, library);
+      const double k = static_cast<double>(a.path_count);
+      L.wall_us.push_back(plan.wall_us);
+      L.gpu_wh.push_back(plan.gpu_wh * k);
+      L.cpu_wh.push_back(plan.cpu_wh * k);
+      L.dollars.push_back(plan.dollars * k);
+      L.quality.push_back(node_quality(node, *library.implementation(a.implementation), a.path_count));
+      tokens.push_back(assignment_token(node.id, a));
+    }
+    std::vector<int> order(r);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tokens[a] < tokens[b]; });
+    std::vector<int32_t> rank(r);
+    for (int k = 0; k < r; ++k) rank[order[k]] = k;
+    L.lexrank.insert(L.lexrank.end(), rank.begin(), rank.end());
+    L.options.push_back(std::move(opts));
+  }
+
+  // Mixed-radix weights in std::map (sorted node id) order: the identifier
+  // concatenates nodes in that order, so the first sorted node is the most
+  // significant digit of the rank.
+  std::vector<int> by_id(n);
+  std::iota(by_id.begin(), by_id.end(), 0);
+  std::sort(by_id.begin(), by_id.end(), [&](int a, int b) { return L.node_ids[a] < L.node_ids[b]; });
+  L.lex_weight.assign(n, 0);
+  uint64_t w = 1;
+  for (int k = n - 1; k >= 0; --k) {
+    L.lex_weight[by_id[k]] = w;
+    if (L.total) w *= static_cast<uint64_t>(L.radix[by_id[k]]);
+  }
+  return L;
+}
+
+loom_problem LoweredProblem::view() const {
+  loom_problem p{};
+  p.n_nodes = static_cast<int32_t>(radix.size());
+  p.n_edges = static_cast<int32_t>(edge_from.size());
+  p.radix = radix.data();
+  p.wall_us = wall_us.data();
+  p.gpu_wh = gpu_wh.data();
+  p.cpu_wh = cpu_wh.data();
+  p.dollars = dollars.data();
+  p.quality = quality.data();
+  p.lexrank = lexrank.data();
+  p.lex_weight = lex_weight.data();
+  p.edge_from = edge_from.data();
+  p.edge_to = edge_to.data();
+  return p;
+}
+
+ConfigPoint LoweredProblem::config_of(uint64_t plan_index) const {
+  ConfigPoint c;
+  for (int i = static_cast<int>(radix.size()) - 1; i >= 0; --i) {
+    const uint64_t r = static_cast<uint64_t>(radix[i]);
+    c.nodes[node_ids[i]] = options[i][plan_index % r];
+    plan_index /= r;
+  }
+  return c;
+}
+
+}  // namespace loom

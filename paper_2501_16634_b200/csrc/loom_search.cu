@@ -1,0 +1,1160 @@
+// sm_100a plan-evaluation kernels: exhaustive argmin over the plan space of a
+// workflow DAG (the reference's loom::exhaustive_search, optimizer.hpp:173-188)
+// and its batched, multi-job form.
+//
+// ALGORITHM.  Plans are indices in ConfigEnumerator order
+// (optimizer.hpp:136-141): node 0 is the most significant digit.  The last K
+// nodes (K = 2..4) form the "suffix"; a "subrow" fixes every digit except the
+// last K-1, i.e. it holds r_sub = prod(radix[N-K+1..N-1]) consecutive plans.
+// Each thread walks a contiguous run of subrows:
+//   * per row (prefix digits change): the energy / dollar left folds of the
+//     prefix nodes in dag order (estimator.hpp:50-60) and a longest-path DP
+//     over the DAG in topological order that treats the K suffix walls as
+//     symbols.  Its output is a max-plus coefficient vector c[S] over subsets
+//     S of the suffix: latency = max_S (c[S] + sum_{s in S} wall_s).  Integer
+//     max/+ is exact, so this equals the reference's finish-time recursion
+//     (estimator.hpp:69-76) for every plan.
+//   * per suffix level: one option of node N-K+j fixes one wall, folding the
+//     coefficient vector in half (c'[S] = max(c[S], c[S+s_j] + w)) and adding
+//     one term to each FP fold -- in dag order, so every plan's sums round
+//     exactly like the reference's.
+//   * innermost node: lat = max(X, Y + w) and e = e_prefix + g per plan.
+// Every plan's primary criterion and feasibility (quality floor folded into
+// an unreachable wall, optional latency SLO) are computed.  Plans that can
+// tie or beat the running best take an exact slow path that quantizes with
+// llround semantics (estimator.hpp:85-87) and compares the full hierarchy
+// then the identifier rank (estimator.hpp:93-116).  Because the order is a
+// strict total order, the per-thread, per-warp, per-CTA and cross-CTA
+// reductions are order independent and bit-exact.
+//
+// Range edges that do not cover whole subrows, and problems with a single
+// node, go through full_eval(): one plan per thread, decoded from its index
+// and re-evaluated from scratch (the reference algorithm restated; also
+// exposed as algo 1 for cross-checking).
+//
+// Compiled with -fmad=false; all FP sums use __dadd_rn explicitly.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "loom_b200.h"
+#include "search_common.h"
+
+using namespace loomk;
+
+namespace {
+
+constexpr int64_t kNeg = -(int64_t(1) << 62);
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+
+// llround(v * 1e9) with the C library's half-away-from-zero rounding
+// (estimator.hpp:85-87).  x - trunc(x) is exact in binary64.
+__device__ __forceinline__ int64_t quantize_dev(double v) {
+  const double x = __dmul_rn(v, 1e9);
+  const double t = trunc(x);
+  const double f = __dsub_rn(x, t);
+  int64_t r = __double2ll_rz(t);
+  if (f >= 0.5) r += 1;
+  else if (f <= -0.5) r -= 1;
+  return r;
+}
+
+// A value strictly above this bound quantizes strictly above q (conservative:
+// values between the exact bound and this one just take the exact slow path).
+__device__ __forceinline__ double hi_of(int64_t q) {
+  const double y = (static_cast<double>(q) + 0.5) / 1e9;
+  return y + fabs(y) * 1e-12 + 1e-300;
+}
+
+struct View {
+  const BlobHeader* h;
+  const int32_t* radix;
+  const int32_t* optoff;
+  const int32_t* topo;
+  const int32_t* predoff;
+  const int32_t* pred;
+  const double* ga;
+  const double* gb;
+  const int64_t* wall;
+  const uint64_t* lexw;
+  const int32_t* q;
+  const InnerEntry* inner;
+};
+
+__device__ __forceinline__ View make_view(const uint8_t* s) {
+  View v;
+  v.h = reinterpret_cast<const BlobHeader*>(s);
+  v.radix = reinterpret_cast<const int32_t*>(s + v.h->off_radix);
+  v.optoff = reinterpret_cast<const int32_t*>(s + v.h->off_optoff);
+  v.topo = reinterpret_cast<const int32_t*>(s + v.h->off_topo);
+  v.predoff = reinterpret_cast<const int32_t*>(s + v.h->off_predoff);
+  v.pred = reinterpret_cast<const int32_t*>(s + v.h->off_pred);
+  v.ga = reinterpret_cast<const double*>(s + v.h->off_ga);
+  v.gb = reinterpret_cast<const double*>(s + v.h->off_gb);
+  v.wall = reinterpret_cast<const int64_t*>(s + v.h->off_wall);
+  v.lexw = reinterpret_cast<const uint64_t*>(s + v.h->off_lexw);
+  v.q = reinterpret_cast<const int32_t*>(s + v.h->off_q);
+  v.inner = reinterpret_cast<const InnerEntry*>(s + v.h->off_inner);
+  return v;
+}
+
+// The problem image arrives in shared memory through one TMA bulk copy
+// (cp.async.bulk, SASS UBLKCP) completing on an mbarrier.
+__device__ __forceinline__ void load_blob(uint8_t* smem, const uint8_t* g, uint32_t bytes, uint64_t* mbar) {
+  const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    constexpr uint32_t kChunk = 16384;
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+      const uint32_t n = min(kChunk, bytes - off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
+          "l"(g + off), "r"(n), "r"(mb)
+          : "memory");
+    }
+  }
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LOOM_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra LOOM_WAIT_%=;\n"
+      "}\n" ::"r"(mb)
+      : "memory");
+}
+
+__device__ __forceinline__ bool rec_better(const Rec& a, const Rec& b, const BlobHeader* h) {
+  if (!a.found) return false;
+  if (!b.found) return true;
+  for (int i = 0; i < h->n_crit; ++i) {
+    switch (h->crit[i]) {
+      case kFpA:
+        if (a.qa != b.qa) return a.qa < b.qa;
+        break;
+      case kFpB:
+        if (a.qb != b.qb) return a.qb < b.qb;
+        break;
+      case kLat:
+        if (a.lat != b.lat) return a.lat < b.lat;
+        break;
+      default:
+        if (a.qual != b.qual) return a.qual > b.qual;
+        break;
+    }
+  }
+  return a.lexkey < b.lexkey;
+}
+
+// Inner-loop thresholds derived from the running best.
+struct Thresh {
+  double hi_a;    // kPrimFp: e > hi_a  => strictly worse
+  int64_t lat_s;  // latency bound: min(slo_eff, best.lat) for kPrimLat, slo_eff otherwise
+  int32_t bq;     // kPrimQual: q < bq  => strictly worse
+};
+
+template <int PRIM>
+__device__ __forceinline__ void thresh_from(const Rec& best, const BlobHeader* h, Thresh& t) {
+  t.hi_a = best.found ? hi_of(best.qa) : INFINITY;
+  t.lat_s = (PRIM == kPrimLat && best.found) ? min(h->slo_eff, best.lat) : h->slo_eff;
+  t.bq = best.found ? best.qual : INT_MIN;
+}
+
+// One plan, decoded from its index and evaluated from scratch.
+__device__ void full_eval(const View& v, uint64_t index, Rec& c) {
+  const int n = v.h->n_nodes;
+  int d[kMaxNodes];
+  uint64_t x = index;
+  for (int i = n - 1; i >= 0; --i) {
+    const uint64_t r = static_cast<uint64_t>(v.radix[i]);
+    d[i] = static_cast<int>(x % r);
+    x /= r;
+  }
+  double ea = 0.0, eb = 0.0;
+  int32_t qual = INT_MAX;
+  uint64_t lex = 0;
+  for (int i = 0; i < n; ++i) {
+    const int o = v.optoff[i] + d[i];
+    ea = __dadd_rn(ea, v.ga[o]);
+    eb = __dadd_rn(eb, v.gb[o]);
+    qual = min(qual, v.q[o]);
+    lex += v.lexw[o];
+  }
+  int64_t fin[kMaxNodes];
+  int64_t lat = 0;
+  for (int t = 0; t < n; ++t) {
+    const int node = v.topo[t];
+    int64_t s = 0;
+    for (int e = v.predoff[node]; e < v.predoff[node + 1]; ++e) s = max(s, fin[v.pred[e]]);
+    fin[node] = s + v.wall[v.optoff[node] + d[node]];
+    lat = max(lat, fin[node]);
+  }
+  c.found = lat <= v.h->slo_eff;
+  c.lat = lat;
+  c.qual = qual;
+  c.lexkey = lex;
+  c.index = index;
+  c.qa = c.found ? quantize_dev(ea) : 0;
+  c.qb = c.found ? quantize_dev(eb) : 0;
+}
+
+// Prefix state of one row: FP folds and quality/identifier partials over
+// nodes [0, P) and the max-plus coefficient vector over the K suffix nodes.
+template <int K>
+__device__ void row_prefix(const View& v, const int* d, int P, double& ea, double& eb, int32_t& qv, uint64_t& lex,
+                           int64_t (&c)[1 << K]) {
+  constexpr int NS = 1 << K;
+  const int n = v.h->n_nodes;
+  ea = 0.0;
+  eb = 0.0;
+  qv = INT_MAX;
+  lex = 0;
+  for (int i = 0; i < P; ++i) {
+    const int o = v.optoff[i] + d[i];
+    ea = __dadd_rn(ea, v.ga[o]);
+    eb = __dadd_rn(eb, v.gb[o]);
+    qv = min(qv, v.q[o]);
+    lex += v.lexw[o];
+  }
+  // f[x][S]: longest path ending at x that visits exactly the suffix nodes in
+  // S, counting prefix walls only.  c[S] = max over x.
+  int64_t f[kMaxNodes][NS];
+#pragma unroll
+  for (int S = 0; S < NS; ++S) c[S] = kNeg;
+  for (int t = 0; t < n; ++t) {
+    const int x = v.topo[t];
+    const int pb = v.predoff[x], pe = v.predoff[x + 1];
+    if (x < P) {
+      const int64_t w = v.wall[v.optoff[x] + d[x]];
+#pragma unroll
+      for (int S = 0; S < NS; ++S) {
+        int64_t b = S == 0 ? 0 : kNeg;
+        for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S]);
+        f[x][S] = b + w;
+        c[S] = max(c[S], f[x][S]);
+      }
+    } else {
+      const int bit = 1 << (x - P);
+#pragma unroll
+      for (int S = 0; S < NS; ++S) {
+        int64_t val = kNeg;
+        if (S & bit) {
+          const int S2 = S ^ bit;
+          int64_t b = S2 == 0 ? 0 : kNeg;
+          for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S2]);
+          val = b;
+        }
+        f[x][S] = val;
+        c[S] = max(c[S], val);
+      }
+    }
+  }
+  c[0] = max(c[0], int64_t(0));
+}
+
+struct Partial {
+  double ea, eb;
+  int32_t qv;
+  uint64_t lex;
+  uint64_t ibase;  // linear index inside the subrow of the digits fixed so far
+};
+
+template <int PRIM>
+__device__ __forceinline__ int32_t inner_tw(int64_t X, int64_t Y, const Thresh& th, int64_t wmin) {
+  if (X > th.lat_s) return INT_MIN;
+  const int64_t t = th.lat_s - Y - wmin;
+  return static_cast<int32_t>(max(min(t, int64_t(INT_MAX) - 1), int64_t(INT_MIN)));
+}
+
+// Innermost node: one LDS.128 + DADD + two compares per plan on the fast path.
+template <int PRIM>
+__device__ __forceinline__ void inner_loop(const View& v, int node, int64_t X, int64_t Y, const Partial& p,
+                                           uint64_t sub_base, Rec& best, Thresh& th) {
+  const BlobHeader* h = v.h;
+  const int n = v.radix[node];
+  const int off = v.optoff[node];
+  const int64_t wmin = h->inner_wmin;
+  int32_t tw = inner_tw<PRIM>(X, Y, th, wmin);
+  const double ea = p.ea;
+  const uint64_t ibase = p.ibase * static_cast<uint64_t>(n);
+#pragma unroll 4
+  for (int o = 0; o < n; ++o) {
+    const InnerEntry e = v.inner[o];
+    const double ev = __dadd_rn(ea, e.g);
+    bool maybe;
+    if (PRIM == kPrimFp) maybe = (e.w <= tw) & (ev <= th.hi_a);
+    else if (PRIM == kPrimLat) maybe = e.w <= tw;
+    else maybe = (e.w <= tw) & (min(p.qv, e.q) >= th.bq);
+    if (__builtin_expect(maybe, 0)) {
+      Rec c;
+      c.lat = max(X, Y + v.wall[off + o]);
+      c.found = c.lat <= h->slo_eff;
+      c.qa = quantize_dev(ev);
+      c.qb = quantize_dev(__dadd_rn(p.eb, v.gb[off + o]));
+      c.qual = min(p.qv, v.q[off + o]);
+      c.lexkey = p.lex + v.lexw[off + o];
+      c.index = sub_base + ibase + static_cast<uint64_t>(o);
+      if (rec_better(c, best, h)) {
+        best = c;
+        thresh_from<PRIM>(best, h, th);
+        tw = inner_tw<PRIM>(X, Y, th, wmin);
+      }
+    }
+  }
+}
+
+// Suffix level J (1 <= J <= K-1) with coefficient vector over suffix nodes J..K-1.
+template <int K, int PRIM, int J>
+__device__ __forceinline__ void suffix_level(const View& v, int P, const int64_t (&c)[1 << (K - J)], const Partial& p,
+                                             uint64_t sub_base, Rec& best, Thresh& th) {
+  const int node = P + J;
+  if constexpr (J == K - 1) {
+    inner_loop<PRIM>(v, node, c[0], c[1], p, sub_base, best, th);
+  } else {
+    constexpr int NS = 1 << (K - J - 1);
+    const int n = v.radix[node];
+    const int off = v.optoff[node];
+    for (int o = 0; o < n; ++o) {
+      const int64_t w = v.wall[off + o];
+      int64_t c2[NS];
+#pragma unroll
+      for (int S = 0; S < NS; ++S) c2[S] = max(c[2 * S], c[2 * S + 1] + w);
+      Partial q;
+      q.ea = __dadd_rn(p.ea, v.ga[off + o]);
+      q.eb = __dadd_rn(p.eb, v.gb[off + o]);
+      q.qv = min(p.qv, v.q[off + o]);
+      q.lex = p.lex + v.lexw[off + o];
+      q.ibase = p.ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o);
+      suffix_level<K, PRIM, J + 1>(v, P, c2, q, sub_base, best, th);
+    }
+  }
+}
+
+// Walk subrows [s_begin, s_end) of the whole space.
+template <int K, int PRIM>
+__device__ void run_subrows(const View& v, uint64_t s_begin, uint64_t s_end, Rec& best, Thresh& th) {
+  constexpr int NS = 1 << K;
+  const BlobHeader* h = v.h;
+  const int n = h->n_nodes;
+  const int P = n - K;
+  const int n0 = v.radix[P];
+  const int off0 = v.optoff[P];
+  const uint64_t r_sub = h->r_sub;
+
+  int d[kMaxNodes];
+  uint64_t row = s_begin / static_cast<uint64_t>(n0);
+  int o0 = static_cast<int>(s_begin % static_cast<uint64_t>(n0));
+  {
+    uint64_t x = row;
+    for (int i = P - 1; i >= 0; --i) {
+      const uint64_t r = static_cast<uint64_t>(v.radix[i]);
+      d[i] = static_cast<int>(x % r);
+      x /= r;
+    }
+  }
+  double ea_pre = 0.0, eb_pre = 0.0;
+  int32_t q_pre = INT_MAX;
+  uint64_t lex_pre = 0;
+  int64_t c0[NS];
+  bool fresh = true;
+  for (uint64_t s = s_begin; s < s_end; ++s) {
+    if (fresh) {
+      row_prefix<K>(v, d, P, ea_pre, eb_pre, q_pre, lex_pre, c0);
+      fresh = false;
+    }
+    // suffix level 0: node P takes option o0 for the whole subrow
+    const int64_t w = v.wall[off0 + o0];
+    int64_t c1[NS / 2];
+#pragma unroll
+    for (int S = 0; S < NS / 2; ++S) c1[S] = max(c0[2 * S], c0[2 * S + 1] + w);
+    Partial p;
+    p.ea = __dadd_rn(ea_pre, v.ga[off0 + o0]);
+    p.eb = __dadd_rn(eb_pre, v.gb[off0 + o0]);
+    p.qv = min(q_pre, v.q[off0 + o0]);
+    p.lex = lex_pre + v.lexw[off0 + o0];
+    p.ibase = 0;
+    suffix_level<K, PRIM, 1>(v, P, c1, p, s * r_sub, best, th);
+
+    if (++o0 == n0) {  // next row: advance the prefix odometer (last prefix node fastest)
+      o0 = 0;
+      fresh = true;
+      for (int i = P - 1; i >= 0; --i) {
+        if (++d[i] < v.radix[i]) break;
+        d[i] = 0;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ Rec shfl_rec(const Rec& r, int delta) {
+  Rec o;
+  o.qa = __shfl_down_sync(0xffffffffu, r.qa, delta);
+  o.qb = __shfl_down_sync(0xffffffffu, r.qb, delta);
+  o.lat = __shfl_down_sync(0xffffffffu, r.lat, delta);
+  o.lexkey = __shfl_down_sync(0xffffffffu, r.lexkey, delta);
+  o.index = __shfl_down_sync(0xffffffffu, r.index, delta);
+  o.qual = __shfl_down_sync(0xffffffffu, r.qual, delta);
+  o.found = __shfl_down_sync(0xffffffffu, r.found, delta);
+  return o;
+}
+
+// Block-wide min-loc under the objective's total order; result valid in thread 0.
+__device__ Rec block_best(Rec r, const BlobHeader* h, Rec* warp_slot) {
+  for (int d = 16; d > 0; d >>= 1) {
+    const Rec o = shfl_rec(r, d);
+    if (rec_better(o, r, h)) r = o;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) warp_slot[warp] = r;
+  __syncthreads();
+  if (warp == 0) {
+    r = lane < kBlock / 32 ? warp_slot[lane] : Rec{0, 0, 0, 0, 0, 0, 0};
+    for (int d = 16; d > 0; d >>= 1) {
+      const Rec o = shfl_rec(r, d);
+      if (rec_better(o, r, h)) r = o;
+    }
+  }
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
+  Rec r;
+  r.qa = __ldcg(&p->qa);
+  r.qb = __ldcg(&p->qb);
+  r.lat = __ldcg(&p->lat);
+  r.lexkey = __ldcg(reinterpret_cast<const unsigned long long*>(&p->lexkey));
+  r.index = __ldcg(reinterpret_cast<const unsigned long long*>(&p->index));
+  r.qual = __ldcg(&p->qual);
+  r.found = __ldcg(&p->found);
+  return r;
+}
+
+template <int K, int PRIM>
+__global__ void __launch_bounds__(kBlock, 2)
+    search_kernel(const uint8_t* __restrict__ arena, const JobDesc* __restrict__ jobs, int ctas_per_job,
+                  Rec* __restrict__ scratch, unsigned* __restrict__ tickets, Rec* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t mbar;
+  __shared__ Rec warp_slot[kBlock / 32];
+  __shared__ int am_last;
+
+  const int job = blockIdx.x / ctas_per_job;
+  const int part = blockIdx.x % ctas_per_job;
+  const JobDesc jd = jobs[job];
+  load_blob(smem, arena + jd.blob_off, jd.blob_bytes, &mbar);
+  const View v = make_view(smem);
+  const BlobHeader* h = v.h;
+
+  Rec best{0, 0, 0, 0, 0, 0, 0};
+  Thresh th;
+  thresh_from<PRIM>(best, h, th);
+
+  const uint64_t gt = static_cast<uint64_t>(part) * kBlock + threadIdx.x;
+  const uint64_t nt = static_cast<uint64_t>(ctas_per_job) * kBlock;
+
+  // Range edges (and whole problems on the full-evaluation path).
+  for (uint64_t i = jd.begin + gt; i < jd.head_end; i += nt) {
+    Rec c;
+    full_eval(v, i, c);
+    if (rec_better(c, best, h)) best = c;
+  }
+  for (uint64_t i = jd.tail_begin + gt; i < jd.end; i += nt) {
+    Rec c;
+    full_eval(v, i, c);
+    if (rec_better(c, best, h)) best = c;
+  }
+  thresh_from<PRIM>(best, h, th);
+
+  // Whole subrows: contiguous share per thread.
+  const uint64_t cnt = jd.sub_hi - jd.sub_lo;
+  if (cnt) {
+    const uint64_t q = cnt / nt, r = cnt % nt;
+    const uint64_t start = jd.sub_lo + gt * q + min(gt, r);
+    const uint64_t len = q + (gt < r ? 1 : 0);
+    if (len) run_subrows<K, PRIM>(v, start, start + len, best, th);
+  }
+
+  Rec b = block_best(best, h, warp_slot);
+  if (threadIdx.x == 0) {
+    scratch[blockIdx.x] = b;
+    __threadfence();
+    const unsigned t = atomicAdd(&tickets[job], 1u);
+    am_last = (t == static_cast<unsigned>(ctas_per_job - 1));
+  }
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    Rec acc{0, 0, 0, 0, 0, 0, 0};
+    for (int i = threadIdx.x; i < ctas_per_job; i += kBlock) {
+      const Rec o = load_rec_cg(&scratch[static_cast<size_t>(job) * ctas_per_job + i]);
+      if (rec_better(o, acc, h)) acc = o;
+    }
+    acc = block_best(acc, h, warp_slot);
+    if (threadIdx.x == 0) {
+      out[job] = acc;
+      tickets[job] = 0;
+    }
+  }
+}
+
+using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, unsigned*, Rec*);
+
+KernelFn pick_kernel(int K, int prim) {
+#define LOOM_K(k)                                         \
+  if (K == k) {                                           \
+    if (prim == kPrimFp) return search_kernel<k, kPrimFp>;   \
+    if (prim == kPrimLat) return search_kernel<k, kPrimLat>; \
+    return search_kernel<k, kPrimQual>;                      \
+  }
+  LOOM_K(2)
+  LOOM_K(3)
+  LOOM_K(4)
+#undef LOOM_K
+  return nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// host: problem image builder
+// ---------------------------------------------------------------------------
+struct Built {
+  std::vector<uint8_t> blob;
+  int K = 2;
+  int prim = kPrimFp;
+  bool full_only = false;
+  uint64_t total = 0;
+  uint64_t r_sub = 1;
+  uint64_t n_sub = 0;
+};
+
+int align16(int x) { return (x + 15) & ~15; }
+
+int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_threads, Built& b) {
+  uint64_t total = 0;
+  if (int rc = loomi::check_problem(p, &total)) return rc;
+  const int n = p->n_nodes;
+  if (n > kMaxNodes) return loomi::fail(LOOM_INVALID, "InvalidConfigError: more than 32 dag nodes");
+  if (p->n_edges > kMaxEdges) return loomi::fail(LOOM_INVALID, "InvalidConfigError: more than 512 dag edges");
+  int n_opts = 0;
+  std::vector<int32_t> optoff(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    optoff[i] = n_opts;
+    n_opts += p->radix[i];
+  }
+  optoff[n] = n_opts;
+  if (n_opts > kMaxOptions) return loomi::fail(LOOM_INVALID, "InvalidConfigError: more than 6144 options");
+  if (!o || o->n_criteria < 0 || o->n_criteria > 4)
+    return loomi::fail(LOOM_INVALID, "InvalidConfigError: objective needs 0..4 criteria");
+
+  // criteria -> slots
+  int fp_kind[2] = {-1, -1};  // LOOM_MIN_ENERGY / LOOM_MIN_COST_DOLLARS per slot
+  int crit[4] = {0, 0, 0, 0};
+  for (int i = 0; i < o->n_criteria; ++i) {
+    const int c = o->criteria[i];
+    if (c == LOOM_MIN_ENERGY || c == LOOM_MIN_COST_DOLLARS) {
+      int slot = fp_kind[0] == c ? 0 : fp_kind[1] == c ? 1 : -1;
+      if (slot < 0) slot = fp_kind[0] < 0 ? 0 : 1;
+      fp_kind[slot] = c;
+      crit[i] = slot == 0 ? kFpA : kFpB;
+    } else if (c == LOOM_MIN_LATENCY) {
+      crit[i] = kLat;
+    } else if (c == LOOM_MAX_QUALITY) {
+      crit[i] = kQual;
+    } else {
+      return loomi::fail(LOOM_INVALID, "InvalidConfigError: unknown criterion " + std::to_string(c));
+    }
+  }
+  const int prim = o->n_criteria == 0 ? kPrimLat : crit[0] == kFpA ? kPrimFp : crit[0] == kLat ? kPrimLat : kPrimQual;
+
+  // walls: quality-floor failures become unreachable; W bounds every feasible latency
+  int64_t W = 0;
+  for (int i = 0; i < n; ++i) {
+    int64_t m = 0;
+    for (int k = optoff[i]; k < optoff[i + 1]; ++k) {
+      if (p->wall_us[k] < 0) return loomi::fail(LOOM_INVALID, "InvalidConfigError: negative wall");
+      m = std::max(m, p->wall_us[k]);
+    }
+    W += m;
+    if (W > (int64_t(1) << 50)) return loomi::fail(LOOM_INVALID, "InvalidConfigError: latency bound exceeds 2^50 us");
+  }
+  const int64_t BIG = W + 1;
+  auto floor_ok = [&](int k) { return !o->has_quality_floor || p->quality[k] >= o->quality_floor; };
+  int64_t slo_eff = W;
+  if (o->has_latency_slo) slo_eff = std::min<int64_t>(o->latency_slo_us, W);
+
+  // K: the deepest suffix that still leaves enough subrows for every thread
+  int K = 2;
+  uint64_t r_sub = 1;
+  bool full_only = n < 2;
+  if (!full_only) {
+    K = 0;
+    for (int k = std::min(4, n); k >= 2; --k) {
+      uint64_t r = 1;
+      for (int j = n - k + 1; j < n; ++j) r *= static_cast<uint64_t>(p->radix[j]);
+      if (total / r >= target_threads || k == 2) {
+        K = k;
+        r_sub = r;
+        break;
+      }
+    }
+  }
+  // inner walls relative to their minimum must fit int32
+  const int inner_node = n - 1;
+  int64_t wmin = INT64_MAX, wmax = 0;
+  for (int k = optoff[inner_node]; k < optoff[inner_node + 1]; ++k) {
+    wmin = std::min(wmin, p->wall_us[k]);
+    wmax = std::max(wmax, p->wall_us[k]);
+  }
+  if (wmax - wmin >= INT_MAX - 2) full_only = true;
+
+  // topology: Kahn order + predecessor CSR
+  std::vector<int32_t> indeg(n, 0), topo;
+  std::vector<std::vector<int32_t>> succ(n), preds(n);
+  for (int e = 0; e < p->n_edges; ++e) {
+    succ[p->edge_from[e]].push_back(p->edge_to[e]);
+    preds[p->edge_to[e]].push_back(p->edge_from[e]);
+    ++indeg[p->edge_to[e]];
+  }
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) topo.push_back(i);
+  for (std::size_t t = 0; t < topo.size(); ++t)
+    for (int s : succ[topo[t]])
+      if (--indeg[s] == 0) topo.push_back(s);
+  if (static_cast<int>(topo.size()) != n) return loomi::fail(LOOM_INVALID, "CycleError: dag has a cycle");
+  std::vector<int32_t> predoff(n + 1, 0), pred;
+  for (int i = 0; i < n; ++i) {
+    predoff[i] = static_cast<int32_t>(pred.size());
+    pred.insert(pred.end(), preds[i].begin(), preds[i].end());
+  }
+  predoff[n] = static_cast<int32_t>(pred.size());
+
+  // layout
+  BlobHeader hd;
+  std::memset(&hd, 0, sizeof hd);
+  int off = align16(sizeof(BlobHeader));
+  auto take = [&](int bytes) {
+    const int at = off;
+    off = align16(off + bytes);
+    return at;
+  };
+  hd.off_radix = take(4 * n);
+  hd.off_optoff = take(4 * (n + 1));
+  hd.off_topo = take(4 * n);
+  hd.off_predoff = take(4 * (n + 1));
+  hd.off_pred = take(4 * std::max<int>(1, static_cast<int>(pred.size())));
+  hd.off_ga = take(8 * n_opts);
+  hd.off_gb = take(8 * n_opts);
+  hd.off_wall = take(8 * n_opts);
+  hd.off_lexw = take(8 * n_opts);
+  hd.off_q = take(4 * n_opts);
+  hd.off_inner = take(static_cast<int>(sizeof(InnerEntry)) * p->radix[inner_node]);
+  if (off > kMaxBlobBytes) return loomi::fail(LOOM_INVALID, "InvalidConfigError: problem image exceeds shared memory");
+  hd.n_nodes = n;
+  hd.n_edges = p->n_edges;
+  hd.n_opts = n_opts;
+  hd.K = K;
+  hd.n_crit = o->n_criteria;
+  for (int i = 0; i < 4; ++i) hd.crit[i] = crit[i];
+  hd.prim = prim;
+  hd.bytes = off;
+  hd.slo_eff = slo_eff;
+  hd.inner_wmin = wmin;
+  hd.total = total;
+  hd.r_sub = r_sub;
+  hd.n_sub = total / r_sub;
+
+  b.blob.assign(off, 0);
+  uint8_t* base = b.blob.data();
+  std::memcpy(base, &hd, sizeof hd);
+  auto put = [&](int at, const void* src, std::size_t bytes) {
+    if (bytes) std::memcpy(base + at, src, bytes);
+  };
+  put(hd.off_radix, p->radix, 4 * n);
+  put(hd.off_optoff, optoff.data(), 4 * (n + 1));
+  put(hd.off_topo, topo.data(), 4 * n);
+  put(hd.off_predoff, predoff.data(), 4 * (n + 1));
+  put(hd.off_pred, pred.data(), 4 * pred.size());
+  double* ga = reinterpret_cast<double*>(base + hd.off_ga);
+  double* gb = reinterpret_cast<double*>(base + hd.off_gb);
+  int64_t* wall = reinterpret_cast<int64_t*>(base + hd.off_wall);
+  uint64_t* lexw = reinterpret_cast<uint64_t*>(base + hd.off_lexw);
+  int32_t* qq = reinterpret_cast<int32_t*>(base + hd.off_q);
+  for (int i = 0; i < n; ++i) {
+    for (int k = optoff[i]; k < optoff[i + 1]; ++k) {
+      const double* src[2] = {nullptr, nullptr};
+      for (int s = 0; s < 2; ++s)
+        src[s] = fp_kind[s] == LOOM_MIN_ENERGY ? p->gpu_wh : fp_kind[s] == LOOM_MIN_COST_DOLLARS ? p->dollars : nullptr;
+      ga[k] = src[0] ? src[0][k] : 0.0;
+      gb[k] = src[1] ? src[1][k] : 0.0;
+      wall[k] = floor_ok(k) ? p->wall_us[k] : BIG;
+      lexw[k] = static_cast<uint64_t>(p->lexrank[k]) * p->lex_weight[i];
+      qq[k] = p->quality[k];
+    }
+  }
+  InnerEntry* inner = reinterpret_cast<InnerEntry*>(base + hd.off_inner);
+  for (int o2 = 0; o2 < p->radix[inner_node]; ++o2) {
+    const int k = optoff[inner_node] + o2;
+    inner[o2].g = ga[k];
+    inner[o2].w = floor_ok(k) ? static_cast<int32_t>(p->wall_us[k] - wmin) : INT_MAX;
+    inner[o2].q = p->quality[k];
+  }
+  b.K = K;
+  b.prim = prim;
+  b.full_only = full_only;
+  b.total = total;
+  b.r_sub = r_sub;
+  b.n_sub = total / r_sub;
+  return LOOM_OK;
+}
+
+// Splits [begin, end) into whole subrows and edge plans.
+JobDesc make_desc(const Built& b, uint64_t begin, uint64_t end, bool full_eval_only) {
+  JobDesc d;
+  std::memset(&d, 0, sizeof d);
+  end = std::min(end, b.total);
+  begin = std::min(begin, end);
+  d.begin = begin;
+  d.end = end;
+  d.blob_bytes = static_cast<uint32_t>(b.blob.size());
+  if (full_eval_only || b.full_only) {
+    d.head_end = end;
+    d.tail_begin = end;
+    return d;
+  }
+  const uint64_t r = b.r_sub;
+  const uint64_t lo = (begin + r - 1) / r, hi = end / r;
+  if (lo >= hi) {  // no whole subrow inside the range
+    d.head_end = end;
+    d.tail_begin = end;
+    return d;
+  }
+  d.sub_lo = lo;
+  d.sub_hi = hi;
+  d.head_end = lo * r;
+  d.tail_begin = hi * r;
+  return d;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context + C ABI
+// ---------------------------------------------------------------------------
+struct loom_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sms = 148;
+  uint64_t launches = 0;
+  // scratch reused across calls
+  uint8_t* d_arena = nullptr;
+  size_t arena_cap = 0;
+  JobDesc* d_jobs = nullptr;
+  size_t jobs_cap = 0;
+  Rec* d_scratch = nullptr;
+  size_t scratch_cap = 0;
+  unsigned* d_tickets = nullptr;
+  size_t tickets_cap = 0;
+  Rec* d_out = nullptr;
+  size_t out_cap = 0;
+  Rec* h_out = nullptr;  // pinned
+  size_t h_out_cap = 0;
+};
+
+struct loom_device_problem {
+  loom_ctx* ctx = nullptr;
+  Built built;
+  loom_problem host;  // shallow copy; arrays owned below
+  std::vector<int32_t> radix, quality, lexrank, efrom, eto;
+  std::vector<int64_t> wall;
+  std::vector<double> gpu, cpu, dol;
+  std::vector<uint64_t> lexw;
+  loom_objective objective;
+  uint8_t* d_blob = nullptr;
+  JobDesc* d_job = nullptr;
+  Rec* d_scratch = nullptr;
+  unsigned* d_ticket = nullptr;
+  Rec* d_out = nullptr;
+  Rec* h_out = nullptr;
+  int ctas = 0;
+  KernelFn fn = nullptr;
+  cudaEvent_t done = nullptr;
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return loomi::fail(LOOM_DEVICE_ERROR, std::string("DeviceError: ") + what + ": " + cudaGetErrorString(e));
+}
+
+#define LOOM_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+template <class T>
+int ensure(T*& ptr, size_t& cap, size_t need) {
+  if (need <= cap && ptr) return LOOM_OK;
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+  LOOM_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), std::max<size_t>(need, 1) * sizeof(T)));
+  cap = need;
+  return LOOM_OK;
+}
+
+int ensure_tickets(loom_ctx* c, size_t need) {
+  if (need <= c->tickets_cap && c->d_tickets) return LOOM_OK;
+  if (c->d_tickets) cudaFree(c->d_tickets);
+  c->d_tickets = nullptr;
+  c->tickets_cap = 0;
+  LOOM_CUDA(cudaMalloc(&c->d_tickets, std::max<size_t>(need, 1) * sizeof(unsigned)));
+  LOOM_CUDA(cudaMemset(c->d_tickets, 0, std::max<size_t>(need, 1) * sizeof(unsigned)));
+  c->tickets_cap = need;
+  return LOOM_OK;
+}
+
+int ensure_host(loom_ctx* c, size_t need) {
+  if (need <= c->h_out_cap && c->h_out) return LOOM_OK;
+  if (c->h_out) cudaFreeHost(c->h_out);
+  c->h_out = nullptr;
+  c->h_out_cap = 0;
+  LOOM_CUDA(cudaMallocHost(&c->h_out, std::max<size_t>(need, 1) * sizeof(Rec)));
+  c->h_out_cap = need;
+  return LOOM_OK;
+}
+
+int set_smem(KernelFn fn, size_t bytes) {
+  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+  return LOOM_OK;
+}
+
+int ctas_for(const loom_ctx* c, uint64_t work_units) {
+  // persistent-style grid: 2 CTAs per SM (the kernel's launch bound), fewer for small spaces
+  const uint64_t full = static_cast<uint64_t>(c->sms) * 2;
+  const uint64_t need = (work_units + kBlock - 1) / kBlock;
+  return static_cast<int>(std::max<uint64_t>(1, std::min(full, need)));
+}
+
+void winner_from_rec(const Rec& r, loom_winner* w) {
+  std::memset(w, 0, sizeof *w);
+  w->found = r.found;
+  w->plan_index = r.index;
+  w->lexkey = r.lexkey;
+  w->latency_us = r.lat;
+  w->quality = r.qual;
+}
+
+int finish_winner(const loom_problem* p, const Rec& r, loom_winner* out) {
+  winner_from_rec(r, out);
+  if (!r.found)
+    return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+  const int64_t lat = r.lat;
+  const uint64_t lex = r.lexkey;
+  if (int rc = loomi::fill_winner(p, out)) return rc;
+  if (out->latency_us != lat || out->lexkey != lex)
+    return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: kernel winner disagrees with host re-evaluation");
+  return LOOM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int loom_ctx_create(int32_t device, void* cuda_stream, loom_ctx** out) {
+  if (!out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null out");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: no CUDA device available (the B200 path has no CPU fallback)");
+  if (device < 0 || device >= count) return loomi::fail(LOOM_INVALID, "InvalidConfigError: bad device ordinal");
+  LOOM_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  LOOM_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: sm_100 device required, found sm_" +
+                                              std::to_string(prop.major * 10 + prop.minor));
+  loom_ctx* c = new loom_ctx;
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  if (cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: cudaStreamCreate failed");
+    }
+    c->own_stream = true;
+  }
+  *out = c;
+  return LOOM_OK;
+}
+
+int loom_ctx_destroy(loom_ctx* c) {
+  if (!c) return LOOM_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaFree(c->d_arena);
+  cudaFree(c->d_jobs);
+  cudaFree(c->d_scratch);
+  cudaFree(c->d_tickets);
+  cudaFree(c->d_out);
+  if (c->h_out) cudaFreeHost(c->h_out);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return LOOM_OK;
+}
+
+uint64_t loom_ctx_launch_count(const loom_ctx* c) { return c ? c->launches : 0; }
+
+int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin,
+                            uint64_t end, int32_t algo, loom_winner* out) {
+  if (!c || !p || !o || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  std::memset(out, 0, sizeof *out);
+  LOOM_CUDA(cudaSetDevice(c->device));
+  Built b;
+  const uint64_t target = static_cast<uint64_t>(c->sms) * 2 * kBlock;
+  if (int rc = build_image(p, o, target, b)) return rc;
+  if (b.total == 0)
+    return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+  const JobDesc d = make_desc(b, begin, end, algo == 1);
+  if (d.begin >= d.end)
+    return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+  const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
+  const int ctas = ctas_for(c, units);
+  KernelFn fn = pick_kernel(b.K, b.prim);
+  if (int rc = ensure(c->d_arena, c->arena_cap, b.blob.size())) return rc;
+  if (int rc = ensure(c->d_jobs, c->jobs_cap, 1)) return rc;
+  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(ctas))) return rc;
+  if (int rc = ensure_tickets(c, 1)) return rc;
+  if (int rc = ensure(c->d_out, c->out_cap, 1)) return rc;
+  if (int rc = ensure_host(c, 1)) return rc;
+  if (int rc = set_smem(fn, b.blob.size())) return rc;
+  LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
+  LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  fn<<<ctas, kBlock, b.blob.size(), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch, c->d_tickets, c->d_out);
+  LOOM_CUDA(cudaGetLastError());
+  ++c->launches;
+  LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+  LOOM_CUDA(cudaStreamSynchronize(c->stream));
+  return finish_winner(p, c->h_out[0], out);
+}
+
+int loom_search_argmin(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin, uint64_t end,
+                       loom_winner* out) {
+  return loom_search_argmin_algo(c, p, o, begin, end, 0, out);
+}
+
+int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const loom_objective* objectives,
+                             int32_t n_jobs, loom_winner* out, int32_t* status) {
+  if (!c || (!problems && n_jobs) || !objectives || (!out && n_jobs) || n_jobs < 0)
+    return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  if (n_jobs == 0) return LOOM_OK;
+  LOOM_CUDA(cudaSetDevice(c->device));
+  // Build every image; group jobs by kernel instantiation.
+  std::vector<Built> built(n_jobs);
+  std::vector<int> ok(n_jobs, 0);
+  for (int j = 0; j < n_jobs; ++j) {
+    std::memset(&out[j], 0, sizeof out[j]);
+    int rc = build_image(&problems[j], &objectives[j], kBlock, built[j]);
+    if (rc == LOOM_OK && built[j].total == 0) {
+      rc = loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+    }
+    if (status) status[j] = rc;
+    ok[j] = rc == LOOM_OK;
+  }
+  struct Group {
+    KernelFn fn;
+    std::vector<int> jobs;
+    size_t smem = 0;
+  };
+  std::vector<Group> groups;
+  for (int j = 0; j < n_jobs; ++j) {
+    if (!ok[j]) continue;
+    KernelFn fn = pick_kernel(built[j].K, built[j].prim);
+    Group* g = nullptr;
+    for (auto& x : groups)
+      if (x.fn == fn) g = &x;
+    if (!g) {
+      groups.push_back({fn, {}, 0});
+      g = &groups.back();
+    }
+    g->jobs.push_back(j);
+    g->smem = std::max(g->smem, built[j].blob.size());
+  }
+  // One arena for all images; one launch per group, one CTA per job.
+  std::vector<uint64_t> off(n_jobs, 0);
+  size_t arena = 0;
+  for (int j = 0; j < n_jobs; ++j)
+    if (ok[j]) {
+      off[j] = arena;
+      arena += built[j].blob.size();
+    }
+  std::vector<uint8_t> host_arena(arena);
+  std::vector<JobDesc> descs;
+  descs.reserve(n_jobs);
+  for (int j = 0; j < n_jobs; ++j)
+    if (ok[j]) std::memcpy(host_arena.data() + off[j], built[j].blob.data(), built[j].blob.size());
+  if (int rc = ensure(c->d_arena, c->arena_cap, arena)) return rc;
+  if (int rc = ensure(c->d_jobs, c->jobs_cap, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure_tickets(c, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure(c->d_out, c->out_cap, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure_host(c, static_cast<size_t>(n_jobs))) return rc;
+  LOOM_CUDA(cudaMemcpyAsync(c->d_arena, host_arena.data(), arena, cudaMemcpyHostToDevice, c->stream));
+  std::vector<JobDesc> all;
+  std::vector<std::pair<int, int>> where;  // (group, slot)
+  size_t base = 0;
+  for (auto& g : groups) {
+    for (int j : g.jobs) {
+      JobDesc d = make_desc(built[j], 0, built[j].total, false);
+      d.blob_off = off[j];
+      all.push_back(d);
+    }
+    (void)base;
+  }
+  LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, all.data(), all.size() * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
+  size_t first = 0;
+  for (auto& g : groups) {
+    if (int rc = set_smem(g.fn, g.smem)) return rc;
+    const int nj = static_cast<int>(g.jobs.size());
+    g.fn<<<nj, kBlock, g.smem, c->stream>>>(c->d_arena, c->d_jobs + first, 1, c->d_scratch + first,
+                                             c->d_tickets + first, c->d_out + first);
+    LOOM_CUDA(cudaGetLastError());
+    ++c->launches;
+    first += nj;
+  }
+  LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, all.size() * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+  LOOM_CUDA(cudaStreamSynchronize(c->stream));
+  size_t k = 0;
+  for (auto& g : groups)
+    for (int j : g.jobs) {
+      const int rc = finish_winner(&problems[j], c->h_out[k++], &out[j]);
+      if (status) status[j] = rc;
+    }
+  return LOOM_OK;
+}
+
+int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective* o, loom_device_problem** out) {
+  if (!c || !p || !o || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  *out = nullptr;
+  LOOM_CUDA(cudaSetDevice(c->device));
+  auto* dp = new loom_device_problem;
+  dp->ctx = c;
+  const uint64_t target = static_cast<uint64_t>(c->sms) * 2 * kBlock;
+  if (int rc = build_image(p, o, target, dp->built)) {
+    delete dp;
+    return rc;
+  }
+  // deep copy of the host tables (the winner is decoded from them)
+  const int n = p->n_nodes;
+  int n_opts = 0;
+  for (int i = 0; i < n; ++i) n_opts += p->radix[i];
+  dp->radix.assign(p->radix, p->radix + n);
+  dp->wall.assign(p->wall_us, p->wall_us + n_opts);
+  dp->gpu.assign(p->gpu_wh, p->gpu_wh + n_opts);
+  dp->cpu.assign(p->cpu_wh, p->cpu_wh + n_opts);
+  dp->dol.assign(p->dollars, p->dollars + n_opts);
+  dp->quality.assign(p->quality, p->quality + n_opts);
+  dp->lexrank.assign(p->lexrank, p->lexrank + n_opts);
+  dp->lexw.assign(p->lex_weight, p->lex_weight + n);
+  dp->efrom.assign(p->edge_from, p->edge_from + p->n_edges);
+  dp->eto.assign(p->edge_to, p->edge_to + p->n_edges);
+  dp->host = *p;
+  dp->host.radix = dp->radix.data();
+  dp->host.wall_us = dp->wall.data();
+  dp->host.gpu_wh = dp->gpu.data();
+  dp->host.cpu_wh = dp->cpu.data();
+  dp->host.dollars = dp->dol.data();
+  dp->host.quality = dp->quality.data();
+  dp->host.lexrank = dp->lexrank.data();
+  dp->host.lex_weight = dp->lexw.data();
+  dp->host.edge_from = dp->efrom.data();
+  dp->host.edge_to = dp->eto.data();
+  dp->objective = *o;
+  dp->fn = pick_kernel(dp->built.K, dp->built.prim);
+  const int ctas = static_cast<int>(static_cast<uint64_t>(c->sms) * 2);
+  dp->ctas = ctas;
+  bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
+             cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
+             cudaMalloc(&dp->d_scratch, sizeof(Rec) * ctas) == cudaSuccess &&
+             cudaMalloc(&dp->d_ticket, sizeof(unsigned)) == cudaSuccess &&
+             cudaMalloc(&dp->d_out, sizeof(Rec)) == cudaSuccess && cudaMallocHost(&dp->h_out, sizeof(Rec)) == cudaSuccess &&
+             cudaEventCreateWithFlags(&dp->done, cudaEventDisableTiming) == cudaSuccess &&
+             cudaMemcpy(dp->d_blob, dp->built.blob.data(), dp->built.blob.size(), cudaMemcpyHostToDevice) ==
+                 cudaSuccess &&
+             cudaMemset(dp->d_ticket, 0, sizeof(unsigned)) == cudaSuccess;
+  if (!okk || set_smem(dp->fn, dp->built.blob.size()) != LOOM_OK) {
+    loom_problem_release(dp);
+    return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: upload failed");
+  }
+  *out = dp;
+  return LOOM_OK;
+}
+
+int loom_problem_release(loom_device_problem* dp) {
+  if (!dp) return LOOM_OK;
+  cudaFree(dp->d_blob);
+  cudaFree(dp->d_job);
+  cudaFree(dp->d_scratch);
+  cudaFree(dp->d_ticket);
+  cudaFree(dp->d_out);
+  if (dp->h_out) cudaFreeHost(dp->h_out);
+  if (dp->done) cudaEventDestroy(dp->done);
+  delete dp;
+  return LOOM_OK;
+}
+
+int loom_search_argmin_async(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end) {
+  if (!c || !dp) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  JobDesc d = make_desc(dp->built, begin, end, false);
+  d.blob_off = 0;
+  if (d.begin >= d.end) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: empty range");
+  const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
+  const int ctas = std::min(dp->ctas, ctas_for(c, units));
+  LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  dp->fn<<<ctas, kBlock, dp->built.blob.size(), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
+                                                             dp->d_ticket, dp->d_out);
+  LOOM_CUDA(cudaGetLastError());
+  ++c->launches;
+  LOOM_CUDA(cudaMemcpyAsync(dp->h_out, dp->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+  LOOM_CUDA(cudaEventRecord(dp->done, c->stream));
+  return LOOM_OK;
+}
+
+int loom_search_argmin_result(loom_ctx* c, loom_device_problem* dp, loom_winner* out) {
+  if (!c || !dp || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  LOOM_CUDA(cudaEventSynchronize(dp->done));
+  return finish_winner(&dp->host, dp->h_out[0], out);
+}
+
+int loom_search_pareto(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end, uint64_t* out_index,
+                       uint64_t capacity, uint64_t* count);
+
+}  // extern "C"
+
+extern "C" int loom_search_pareto(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
+                                  uint64_t* out_index, uint64_t capacity, uint64_t* count) {
+  (void)c; (void)p; (void)begin; (void)end; (void)out_index; (void)capacity; (void)count;
+  return loomi::fail(LOOM_INVALID, "InvalidConfigError: pareto search not built yet");
+}

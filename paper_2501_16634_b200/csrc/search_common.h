@@ -1,0 +1,86 @@
+// Shared definitions between the host-side problem builder and the sm_100a
+// kernels (loom_search.cu).  A "problem image" is one contiguous, 16-byte
+// aligned blob: header + topology + per-option tables.  Each CTA copies its
+// problem image into shared memory with a single cp.async.bulk (TMA bulk
+// copy) and never touches global memory again until the final reduction.
+#pragma once
+
+#include <cstdint>
+
+namespace loomk {
+
+constexpr int kMaxNodes = 32;
+constexpr int kMaxEdges = 512;
+constexpr int kMaxOptions = 6144;
+constexpr int kMaxBlobBytes = 200 * 1024;
+constexpr int kBlock = 256;
+
+// Criterion slots inside the kernels.  FP_A / FP_B are the (at most two)
+// floating-point sums the objective ranks on (gpu_wh and/or dollars); they
+// are compared after quantize() = llround(v * 1e9) (estimator.hpp:85-87).
+enum CritKind : int32_t { kFpA = 0, kFpB = 1, kLat = 2, kQual = 3 };
+
+// How the first criterion is tested in the inner loop.
+enum Prim : int32_t { kPrimFp = 0, kPrimLat = 1, kPrimQual = 2 };
+
+// Innermost node's option, 16 bytes = one LDS.128 broadcast per plan.
+struct alignas(16) InnerEntry {
+  double g;     // FP_A contribution of this option
+  int32_t w;    // wall_us - inner_wmin (INT32_MAX if the option fails the quality floor)
+  int32_t q;    // node quality
+};
+
+struct alignas(16) BlobHeader {
+  int32_t n_nodes;
+  int32_t n_edges;
+  int32_t n_opts;
+  int32_t K;         // suffix levels handled incrementally (2..4)
+  int32_t n_crit;
+  int32_t crit[4];   // CritKind per criterion, most significant first
+  int32_t prim;      // Prim
+  int32_t bytes;     // blob size, multiple of 16
+  int32_t off_radix;
+  int32_t off_optoff;
+  int32_t off_topo;
+  int32_t off_predoff;
+  int32_t off_pred;
+  int32_t off_ga;
+  int32_t off_gb;
+  int32_t off_wall;
+  int32_t off_lexw;
+  int32_t off_q;
+  int32_t off_inner;
+  int32_t pad0;
+  int64_t slo_eff;       // min(latency SLO, sum of max walls): lat <= slo_eff <=> feasible
+  int64_t inner_wmin;    // inner walls are stored relative to this
+  uint64_t total;        // plans in the space
+  uint64_t r_sub;        // plans per subrow = product of the last K-1 radices
+  uint64_t n_sub;        // subrows in the whole space = total / r_sub
+};
+
+// A candidate / winner inside the kernels: the quantized criteria, exact
+// latency and quality, the identifier rank and the plan index.
+struct Rec {
+  int64_t qa;
+  int64_t qb;
+  int64_t lat;
+  uint64_t lexkey;
+  uint64_t index;
+  int32_t qual;
+  int32_t found;
+};
+
+// Per-job launch descriptor (global memory).
+struct JobDesc {
+  uint64_t blob_off;     // byte offset in the blob arena
+  uint64_t begin;        // plans [begin, end)
+  uint64_t end;
+  uint64_t head_end;     // partial plans [begin, head_end) ...
+  uint64_t tail_begin;   // ... and [tail_begin, end): one-plan-per-thread path
+  uint64_t sub_lo;       // whole subrows [sub_lo, sub_hi): hierarchical path
+  uint64_t sub_hi;
+  uint32_t blob_bytes;
+  uint32_t pad;
+};
+
+}  // namespace loomk

@@ -1,0 +1,402 @@
+"""Python binding of libloom_b200.so (include/loom_b200.h) for tests and the
+bench.  It mirrors the reference's public search API (namespace loom,
+optimizer.hpp / estimator.hpp): exhaustive_search(dag, library, objective,
+bounds) returns the ConfigEstimate, errors surface as the reference's error
+classes (errors.hpp:53-54) with the same messages.
+
+There is no CPU fallback: loading fails loudly if the library is missing, and
+device calls raise DeviceError without an sm_100 GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Any, Sequence
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libloom_b200.so"
+
+LOOM_OK, LOOM_INFEASIBLE, LOOM_INVALID, LOOM_DEVICE_ERROR = 0, 1, 2, 3
+CRITERIA = {"min_cost_dollars": 0, "min_energy": 1, "min_latency": 2, "max_quality": 3}
+
+
+# ---- errors (errors.hpp) --------------------------------------------------
+class LoomError(RuntimeError):
+    code = "Error"
+    category = 0
+
+    def __init__(self, message: str, status: int = LOOM_INVALID):
+        super().__init__(message)
+        self.status = status
+
+
+class SchemaError(LoomError):
+    code, category = "SchemaError", 2
+
+
+class ValidationError(LoomError):
+    code, category = "ValidationError", 2
+
+
+class CycleError(LoomError):
+    code, category = "CycleError", 2
+
+
+class DuplicateKeyError(LoomError):
+    code, category = "DuplicateKeyError", 2
+
+
+class DanglingReferenceError(LoomError):
+    code, category = "DanglingReferenceError", 2
+
+
+class UnknownCapabilityError(LoomError):
+    code, category = "UnknownCapabilityError", 2
+
+
+class InvalidConfigError(LoomError):
+    code, category = "InvalidConfigError", 4
+
+
+class NoFeasibleConfigError(LoomError):
+    code, category = "NoFeasibleConfigError", 4
+
+
+class DeviceError(LoomError):
+    code, category = "DeviceError", 5
+
+
+_ERRORS = {cls.code: cls for cls in (SchemaError, ValidationError, CycleError, DuplicateKeyError,
+                                     DanglingReferenceError, UnknownCapabilityError, InvalidConfigError,
+                                     NoFeasibleConfigError, DeviceError)}
+
+
+def _raise(status: int, message: str):
+    code = message.split(":", 1)[0].strip()
+    cls = _ERRORS.get(code)
+    if cls is None:
+        cls = {LOOM_INFEASIBLE: NoFeasibleConfigError, LOOM_DEVICE_ERROR: DeviceError}.get(status,
+                                                                                            InvalidConfigError)
+    raise cls(message, status)
+
+
+# ---- ABI structs ------------------------------------------------------------
+class Problem(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("n_edges", C.c_int32), ("radix", C.POINTER(C.c_int32)),
+                ("wall_us", C.POINTER(C.c_int64)), ("gpu_wh", C.POINTER(C.c_double)),
+                ("cpu_wh", C.POINTER(C.c_double)), ("dollars", C.POINTER(C.c_double)),
+                ("quality", C.POINTER(C.c_int32)), ("lexrank", C.POINTER(C.c_int32)),
+                ("lex_weight", C.POINTER(C.c_uint64)), ("edge_from", C.POINTER(C.c_int32)),
+                ("edge_to", C.POINTER(C.c_int32))]
+
+
+class Objective(C.Structure):
+    _fields_ = [("n_criteria", C.c_int32), ("criteria", C.c_int32 * 4), ("has_quality_floor", C.c_int32),
+                ("quality_floor", C.c_int32), ("has_latency_slo", C.c_int32), ("reserved", C.c_int32),
+                ("latency_slo_us", C.c_int64)]
+
+
+class Winner(C.Structure):
+    _fields_ = [("plan_index", C.c_uint64), ("lexkey", C.c_uint64), ("latency_us", C.c_int64),
+                ("gpu_wh", C.c_double), ("cpu_wh", C.c_double), ("total_wh", C.c_double),
+                ("dollars", C.c_double), ("quality", C.c_int32), ("found", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+assert C.sizeof(Winner) == 64
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libloom_b200.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2501_16634_b200.build`")
+    L = C.CDLL(str(LIB_PATH))
+    P, O, W = C.POINTER(Problem), C.POINTER(Objective), C.POINTER(Winner)
+    vp = C.c_void_p
+    sig = {
+        "loom_abi_version": ([], C.c_int),
+        "loom_last_error": ([], C.c_char_p),
+        "loom_problem_total": ([P, C.POINTER(C.c_uint64)], C.c_int),
+        "loom_evaluate_plan": ([P, C.c_uint64, W], C.c_int),
+        "loom_winner_less": ([W, W, O], C.c_int),
+        "loom_winner_reduce": ([W, C.c_int32, O, W], C.c_int),
+        "loom_objective_parse": ([C.c_char_p, O], C.c_int),
+        "loom_lower": ([C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(vp)], C.c_int),
+        "loom_lowered_problem": ([vp], P),
+        "loom_lowered_config_json": ([vp, C.c_uint64, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+        "loom_lowered_option_json": ([vp, C.c_int32, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+                                     C.c_int),
+        "loom_lowered_destroy": ([vp], None),
+        "loom_ctx_create": ([C.c_int32, vp, C.POINTER(vp)], C.c_int),
+        "loom_ctx_destroy": ([vp], C.c_int),
+        "loom_ctx_launch_count": ([vp], C.c_uint64),
+        "loom_search_argmin": ([vp, P, O, C.c_uint64, C.c_uint64, W], C.c_int),
+        "loom_search_argmin_algo": ([vp, P, O, C.c_uint64, C.c_uint64, C.c_int32, W], C.c_int),
+        "loom_search_argmin_batch": ([vp, P, O, C.c_int32, W, C.POINTER(C.c_int32)], C.c_int),
+        "loom_problem_upload": ([vp, P, O, C.POINTER(vp)], C.c_int),
+        "loom_problem_release": ([vp], C.c_int),
+        "loom_search_argmin_async": ([vp, vp, C.c_uint64, C.c_uint64], C.c_int),
+        "loom_search_argmin_result": ([vp, vp, W], C.c_int),
+        "loom_search_pareto": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64,
+                                C.POINTER(C.c_uint64)], C.c_int),
+        "loom_exhaustive_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                         C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    """Function names declared in include/loom_b200.h."""
+    import re
+    text = (PKG.parent / "include" / "loom_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(loom_[a-z0-9_]+)\s*\(", text)))
+
+
+def last_error() -> str:
+    return (lib().loom_last_error() or b"").decode()
+
+
+def _check(rc: int) -> None:
+    if rc != LOOM_OK:
+        _raise(rc, last_error())
+
+
+def _text(x: Any) -> bytes:
+    return (x if isinstance(x, str) else json.dumps(x)).encode()
+
+
+def objective(obj: dict | str) -> Objective:
+    """Objective JSON / token -> loom_objective (workflow.hpp:91-106)."""
+    if isinstance(obj, str) and not obj.lstrip().startswith("{"):
+        obj = {"constraint": obj}
+    o = Objective()
+    _check(lib().loom_objective_parse(_text(obj), C.byref(o)))
+    return o
+
+
+# ---- lowering -----------------------------------------------------------
+class Lowered:
+    """Reference-format JSON lowered to the flat plan space (host-side C++)."""
+
+    def __init__(self, dag: Any, library: Any, bounds: Any):
+        h = C.c_void_p()
+        _check(lib().loom_lower(_text(dag), _text(library), _text(bounds), C.byref(h)))
+        self._h = h
+        self.problem: Problem = lib().loom_lowered_problem(h).contents
+
+    def close(self) -> None:
+        if self._h:
+            lib().loom_lowered_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def radix(self) -> list[int]:
+        return [self.problem.radix[i] for i in range(self.problem.n_nodes)]
+
+    @property
+    def n_options(self) -> int:
+        return sum(self.radix)
+
+    @property
+    def total(self) -> int:
+        t = C.c_uint64(0)
+        _check(lib().loom_problem_total(C.byref(self.problem), C.byref(t)))
+        return t.value
+
+    def table(self, name: str) -> list:
+        arr = getattr(self.problem, name)
+        n = self.problem.n_nodes if name == "lex_weight" else self.n_options
+        return [arr[i] for i in range(n)]
+
+    def _json(self, fn, *args) -> dict:
+        need = C.c_size_t(0)
+        fn(self._h, *args, None, 0, C.byref(need))
+        buf = C.create_string_buffer(need.value)
+        _check(fn(self._h, *args, buf, need.value, C.byref(need)))
+        return json.loads(buf.value.decode())
+
+    def config(self, plan_index: int) -> dict:
+        return self._json(lib().loom_lowered_config_json, C.c_uint64(plan_index))
+
+    def option(self, node: int, option: int) -> dict:
+        return self._json(lib().loom_lowered_option_json, node, option)
+
+    def evaluate(self, plan_index: int) -> dict:
+        w = Winner()
+        _check(lib().loom_evaluate_plan(C.byref(self.problem), plan_index, C.byref(w)))
+        return w.as_dict()
+
+
+# ---- device context --------------------------------------------------------
+class Context:
+    def __init__(self, device: int = 0, stream: int | None = None):
+        """stream: a cudaStream_t handle to launch on; None -> the ctx owns a
+        stream; 0 (torch's legacy default stream) -> cudaStreamLegacy."""
+        h = C.c_void_p()
+        handle = None if stream is None else C.c_void_p(stream if stream else 1)
+        _check(lib().loom_ctx_create(device, handle, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @property
+    def launches(self) -> int:
+        return lib().loom_ctx_launch_count(self._h)
+
+    def close(self) -> None:
+        if self._h:
+            lib().loom_ctx_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def search_argmin(ctx: Context, problem: Problem, obj: Objective, begin: int = 0, end: int | None = None,
+                  algo: int = 0) -> dict:
+    w = Winner()
+    end = (1 << 64) - 1 if end is None else end
+    _check(lib().loom_search_argmin_algo(ctx.handle, C.byref(problem), C.byref(obj), begin, end, algo, C.byref(w)))
+    return w.as_dict()
+
+
+def search_argmin_batch(ctx: Context, problems: Sequence[Problem], objectives: Sequence[Objective]
+                        ) -> list[tuple[int, dict]]:
+    n = len(problems)
+    P = (Problem * n)(*problems)
+    O = (Objective * n)(*objectives)
+    W = (Winner * n)()
+    S = (C.c_int32 * n)()
+    _check(lib().loom_search_argmin_batch(ctx.handle, P, O, n, W, S))
+    return [(S[i], W[i].as_dict()) for i in range(n)]
+
+
+def winner_reduce(winners: Sequence[Winner], obj: Objective) -> dict:
+    n = len(winners)
+    arr = (Winner * max(1, n))(*winners)
+    out = Winner()
+    _check(lib().loom_winner_reduce(arr, n, C.byref(obj), C.byref(out)))
+    return out.as_dict()
+
+
+def winner_from_dict(d: dict) -> Winner:
+    w = Winner()
+    for k, _ in Winner._fields_:
+        setattr(w, k, d[k])
+    return w
+
+
+class DeviceProblem:
+    """A problem resident in HBM for repeated searches (bench 'value' path)."""
+
+    def __init__(self, ctx: Context, problem: Problem, obj: Objective):
+        h = C.c_void_p()
+        _check(lib().loom_problem_upload(ctx.handle, C.byref(problem), C.byref(obj), C.byref(h)))
+        self._h, self.ctx = h, ctx
+
+    def search_async(self, begin: int = 0, end: int | None = None) -> None:
+        end = (1 << 64) - 1 if end is None else end
+        _check(lib().loom_search_argmin_async(self.ctx.handle, self._h, begin, end))
+
+    def result(self) -> dict:
+        w = Winner()
+        _check(lib().loom_search_argmin_result(self.ctx.handle, self._h, C.byref(w)))
+        return w.as_dict()
+
+    def close(self) -> None:
+        if self._h:
+            lib().loom_problem_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def search_pareto(ctx: Context, problem: Problem, begin: int = 0, end: int | None = None) -> list[int]:
+    end = (1 << 64) - 1 if end is None else end
+    cnt = C.c_uint64(0)
+    _check(lib().loom_search_pareto(ctx.handle, C.byref(problem), begin, end, None, 0, C.byref(cnt)))
+    buf = (C.c_uint64 * max(1, cnt.value))()
+    _check(lib().loom_search_pareto(ctx.handle, C.byref(problem), begin, end, buf, cnt.value, C.byref(cnt)))
+    return [buf[i] for i in range(cnt.value)]
+
+
+# ---- the drop-in call ----------------------------------------------------
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def exhaustive_search(dag: Any, library: Any, objective_: Any, bounds: Any, ctx: Context | None = None) -> dict:
+    """loom::exhaustive_search (optimizer.hpp:173-188) on reference-format JSON;
+    returns the ConfigEstimate as a dict (identifier, config, latency_us,
+    gpu_wh, cpu_wh, total_wh, dollars, quality, plan_index, plans)."""
+    ctx = ctx or default_context()
+    if isinstance(objective_, str) and not objective_.lstrip().startswith("{"):
+        objective_ = {"constraint": objective_}
+    need = C.c_size_t(0)
+    cap = 1 << 16
+    buf = C.create_string_buffer(cap)
+    rc = lib().loom_exhaustive_search_json(ctx.handle, _text(dag), _text(library), _text(objective_),
+                                           _text(bounds), buf, cap, C.byref(need))
+    if rc != LOOM_OK and need.value > cap:
+        buf = C.create_string_buffer(need.value)
+        rc = lib().loom_exhaustive_search_json(ctx.handle, _text(dag), _text(library), _text(objective_),
+                                               _text(bounds), buf, need.value, C.byref(need))
+    out = json.loads(buf.value.decode())
+    if rc != LOOM_OK:
+        _raise(rc, out.get("message", last_error()))
+    return out
+
+
+@dataclass
+class SearchBounds:
+    max_fanout: int = 4
+    max_paths: int = 2
+    sku_pool_cap: dict | None = None
+    sku_total_cap: dict | None = None
+
+    def to_json(self) -> dict:
+        return {"max_fanout": self.max_fanout, "max_paths": self.max_paths,
+                "sku_pool_cap": self.sku_pool_cap or {}, "sku_total_cap": self.sku_total_cap or {}}

@@ -1,0 +1,225 @@
+"""GPU parity: the sm_100a search through the C ABI against the reference's
+golden vectors (tests/golden) and the CPU oracle on the same inputs.  The
+bar is bit-exact: same selected plan (identifier / plan index), same integer
+latency and quality, bit-identical doubles."""
+import random
+
+import pytest
+
+from conftest import cpu_threads
+from oracle import oracle as O
+from paper_2501_16634_b200 import loom, workloads as W
+
+pytestmark = pytest.mark.gpu
+TOKENS = ["MIN_COST", "MIN_DOLLARS", "MIN_LATENCY", "MAX_QUALITY"]
+METRICS = ("latency_us", "gpu_wh", "cpu_wh", "total_wh", "dollars", "quality")
+
+
+def _check_ref(got: dict, ref: dict, lw: loom.Lowered) -> None:
+    assert lw.config(got["plan_index"])["identifier"] == ref["identifier"]
+    for k in METRICS:
+        assert got[k] == ref[k], k
+
+
+def _check_oracle(got: dict, ora: dict) -> None:
+    assert got["plan_index"] == ora["index"]
+    for k in METRICS:
+        assert got[k] == ora[k], k
+
+
+def _search(ctx, w, obj, begin=0, end=None, algo=0):
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    return lw, loom.search_argmin(ctx, lw.problem, loom.objective(obj), begin, end, algo)
+
+
+@pytest.mark.parametrize("token", TOKENS)
+@pytest.mark.parametrize("algo", [0, 1])
+def test_c1_tokens(ctx, golden, token, algo):
+    w = W.config1()
+    lw, got = _search(ctx, w, {"constraint": token}, algo=algo)
+    _check_ref(got, golden("c1/results.json")["tokens"][token]["exhaustive"], lw)
+
+
+@pytest.mark.parametrize("floor", range(6))
+def test_c1_floors(ctx, golden, floor):
+    w = W.config1()
+    ref = golden("c1/results.json")["floors"][str(floor)]
+    obj = {"constraint": "MIN_COST", "quality_floor": floor}
+    if ref.get("error"):
+        with pytest.raises(loom.NoFeasibleConfigError, match="no configuration satisfies the quality floor and bounds"):
+            _search(ctx, w, obj)
+    else:
+        lw, got = _search(ctx, w, obj)
+        _check_ref(got, ref, lw)
+
+
+@pytest.mark.parametrize("token", TOKENS)
+def test_c1_dropin_json(ctx, golden, token):
+    """loom::exhaustive_search on reference-format JSON (the drop-in call)."""
+    w = W.config1()
+    ref = golden("c1/results.json")["tokens"][token]["exhaustive"]
+    got = loom.exhaustive_search(w.dag, w.library, {"constraint": token}, w.bounds, ctx=ctx)
+    assert got["identifier"] == ref["identifier"]
+    assert got["config"]["nodes"] == ref["config"]["nodes"]
+    for k in METRICS:
+        assert got[k] == ref[k]
+    assert got["plans"] == 168
+
+
+def test_c1_min_latency_prefers_hybrid(ctx):
+    """test_fixture.cpp:72-94: MIN_LATENCY breaks the 77 s tie by energy toward gpu+cpu."""
+    w = W.config1()
+    got = loom.exhaustive_search(w.dag, w.library, "MIN_LATENCY", w.bounds, ctx=ctx)
+    stt = got["config"]["nodes"]["t1_speech_to_text"]["placements"]
+    assert {p["sku"] for p in stt} == {"cpu-epyc", "gpu-a100"}
+    assert got["latency_us"] == 76_750_000
+
+
+def test_random_scenarios_all_tokens(ctx, golden):
+    gold = golden("random/results.json")
+    n = 0
+    for seed, entry in gold.items():
+        w = W.random_scenario(int(seed), max_nodes=4)
+        lw = loom.Lowered(w.dag, w.library, w.bounds)
+        for token, ref in entry.get("search", {}).items():
+            for algo in (0, 1):
+                if ref.get("error"):
+                    with pytest.raises(loom.NoFeasibleConfigError):
+                        loom.search_argmin(ctx, lw.problem, loom.objective(token), 0, None, algo)
+                else:
+                    _check_ref(loom.search_argmin(ctx, lw.problem, loom.objective(token), 0, None, algo), ref, lw)
+                    n += 1
+        if "floor2" in entry:
+            ref = entry["floor2"]
+            obj = loom.objective({"constraint": w.objective["constraint"], "quality_floor": 2})
+            if ref.get("error"):
+                with pytest.raises(loom.NoFeasibleConfigError):
+                    loom.search_argmin(ctx, lw.problem, obj)
+            else:
+                _check_ref(loom.search_argmin(ctx, lw.problem, obj), ref, lw)
+    assert n > 400
+
+
+def test_c2_full_space(ctx, golden):
+    g = golden("c2/results.json")
+    w = W.config2()
+    lw, got = _search(ctx, w, w.objective)
+    assert lw.total == g["total"] == 1_207_296
+    _check_ref(got, g["config"], lw)
+    _check_ref(loom.search_argmin(ctx, lw.problem, loom.objective("MIN_COST")), g["min_cost"], lw)
+    _check_ref(loom.search_argmin(ctx, lw.problem, loom.objective({"constraint": "MIN_DOLLARS", "quality_floor": 3})),
+               g["min_dollars_q3"], lw)
+
+
+def test_c2_dropin_json(ctx, golden):
+    g = golden("c2/results.json")["config"]
+    w = W.config2()
+    got = loom.exhaustive_search(w.dag, w.library, w.objective, w.bounds, ctx=ctx)
+    assert got["identifier"] == g["identifier"]
+    assert got["gpu_wh"] == g["gpu_wh"] and got["latency_us"] == g["latency_us"]
+
+
+def test_c2_random_subranges_vs_oracle(ctx):
+    """Unaligned ranges exercise the edge (full re-evaluation) path and the
+    subrow path together."""
+    w = W.config2()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    p = O.problem(w.dag, w.library, w.bounds)
+    rng = random.Random(2)
+    for token in TOKENS:
+        for _ in range(3):
+            b = rng.randrange(lw.total - 1)
+            e = min(lw.total, b + rng.randrange(1, 300_000))
+            obj = {"constraint": token, "quality_floor": rng.choice([None, 2, 3])}
+            ora = O.argmin(p, obj, b, e, threads=cpu_threads())
+            if ora is None:
+                with pytest.raises(loom.NoFeasibleConfigError):
+                    loom.search_argmin(ctx, lw.problem, loom.objective(obj), b, e)
+                continue
+            for algo in (0, 1):
+                _check_oracle(loom.search_argmin(ctx, lw.problem, loom.objective(obj), b, e, algo), ora)
+
+
+def test_c3_slices(ctx, golden):
+    g = golden("c3/slices.json")
+    w = W.config3()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    for s in g["slices"]:
+        ref = s["result"]
+        if not ref["found"]:
+            with pytest.raises(loom.NoFeasibleConfigError):
+                loom.search_argmin(ctx, lw.problem, loom.objective(g["objective"]), s["begin"], s["end"])
+            continue
+        got = loom.search_argmin(ctx, lw.problem, loom.objective(g["objective"]), s["begin"], s["end"])
+        assert got["plan_index"] == ref["winner"]["plan_index"]
+        _check_ref(got, ref["winner"], lw)
+    s = g["slice_no_slo"]
+    got = loom.search_argmin(ctx, lw.problem, loom.objective("MIN_COST"), s["begin"], s["end"])
+    _check_ref(got, s["result"]["winner"], lw)
+
+
+def test_c3_hierarchical_equals_full_eval_on_large_slices(ctx):
+    """Two independent GPU algorithms (max-plus hierarchical vs one plan per
+    thread from scratch) agree on 64M-plan slices, plus the oracle on 4M."""
+    w = W.config3()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    p = O.problem(w.dag, w.library, w.bounds)
+    obj = loom.objective(w.objective)
+    rng = random.Random(9)
+    def outcome(b, e, algo):
+        try:
+            return loom.search_argmin(ctx, lw.problem, obj, b, e, algo)
+        except loom.NoFeasibleConfigError:
+            return None
+
+    feasible = 0
+    for _ in range(6):
+        b = rng.randrange(lw.total - (1 << 26))
+        a0, a1 = outcome(b, b + (1 << 26), 0), outcome(b, b + (1 << 26), 1)
+        assert a0 == a1
+        feasible += a0 is not None
+    # a slice that holds feasible plans (around the golden slice's winner)
+    c = 123_457_159_103
+    a0, a1 = outcome(c - (1 << 25), c + (1 << 25), 0), outcome(c - (1 << 25), c + (1 << 25), 1)
+    assert a0 is not None and a0 == a1
+    b = 777_777_777
+    ora = O.argmin(p, w.objective, b, b + 4_000_000, threads=cpu_threads())
+    _check_oracle(loom.search_argmin(ctx, lw.problem, obj, b, b + 4_000_000), ora)
+
+
+def test_c4_batch(ctx, golden):
+    gold = golden("c4/jobs.json")["jobs"]
+    jobs = W.config4(96)
+    lws = [loom.Lowered(j.dag, j.library, j.bounds) for j in jobs]
+    out = loom.search_argmin_batch(ctx, [lw.problem for lw in lws], [loom.objective(j.objective) for j in jobs])
+    for k, ((st, got), lw) in enumerate(zip(out, lws)):
+        assert st == 0
+        if str(k) in gold:
+            _check_ref(got, gold[str(k)]["result"], lw)
+        elif k < 40:
+            p = O.problem(jobs[k].dag, jobs[k].library, jobs[k].bounds)
+            _check_oracle(got, O.argmin(p, jobs[k].objective, threads=cpu_threads()))
+
+
+def test_resident_problem_async(ctx):
+    w = W.config3()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    obj = loom.objective(w.objective)
+    dp = loom.DeviceProblem(ctx, lw.problem, obj)
+    b, e = 10_000_000_019, 10_000_000_019 + (1 << 27)
+    dp.search_async(b, e)
+    got = dp.result()
+    assert got == loom.search_argmin(ctx, lw.problem, obj, b, e, 1)
+    dp.close()
+
+
+def test_infeasible_and_empty(ctx):
+    w = W.config1()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    with pytest.raises(loom.NoFeasibleConfigError):
+        loom.search_argmin(ctx, lw.problem, loom.objective({"constraint": "MIN_COST", "quality_floor": 9}))
+    with pytest.raises(loom.NoFeasibleConfigError):
+        loom.search_argmin(ctx, lw.problem, loom.objective("MIN_COST"), 100, 100)
+    with pytest.raises(loom.NoFeasibleConfigError):
+        loom.exhaustive_search({"nodes": [], "edges": []}, w.library, "MIN_COST", w.bounds, ctx=ctx)
+    assert ctx.launches > 0

@@ -1,0 +1,149 @@
+"""Host side of the product, no GPU needed: the C ABI library loads and
+exports every entry point include/loom_b200.h declares; the C++ lowering
+(node_options + plan_node_execution + identifier ranks) is bit-identical to
+the oracle's restatement; host estimate / total order / objective parsing and
+error behaviour mirror the reference."""
+import ctypes as C
+import random
+import subprocess
+
+import pytest
+
+from oracle import oracle as O
+from paper_2501_16634_b200 import loom, workloads as W
+
+TOKENS = ["MIN_COST", "MIN_DOLLARS", "MIN_LATENCY", "MAX_QUALITY"]
+
+
+def test_library_exports_every_declared_symbol(loomlib):
+    declared = loom.exported_symbols()
+    assert len(declared) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", str(loom.LIB_PATH)], capture_output=True, text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    for s in declared:
+        assert hasattr(loomlib, s)
+    assert loomlib.loom_abi_version() == 1
+
+
+def _workloads():
+    yield W.config1()
+    yield W.config2()
+    yield W.config3()
+    yield W.config5()
+    yield from W.config4(3)
+    for seed in range(0, 40):
+        yield W.random_scenario(seed)
+
+
+@pytest.mark.parametrize("w", list(_workloads()), ids=lambda w: w.name)
+def test_lowering_bit_identical_to_oracle(loomlib, w):
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    p = O.problem(w.dag, w.library, w.bounds)
+    assert lw.radix == p.lowered.radix
+    assert lw.total == p.total
+    flat = [(pl, op, q, t) for pls, ops, qs, ts in zip(p.lowered.plans, p.lowered.options, p.lowered.quality,
+                                                        p.lowered.tokens) for pl, op, q, t in zip(pls, ops, qs, ts)]
+    wall, gpu, cpu, dol = (lw.table(n) for n in ("wall_us", "gpu_wh", "cpu_wh", "dollars"))
+    qual, rank = lw.table("quality"), lw.table("lexrank")
+    for k, (pl, op, q, tok) in enumerate(flat):
+        k_paths = op["path_count"]
+        assert wall[k] == pl["wall_us"]
+        assert gpu[k] == pl["gpu_wh"] * k_paths
+        assert cpu[k] == pl["cpu_wh"] * k_paths
+        assert dol[k] == pl["dollars"] * k_paths
+        assert qual[k] == q
+    # identifier ranks per node and the sorted-id weights
+    off = 0
+    for i, toks in enumerate(p.lowered.tokens):
+        order = sorted(range(len(toks)), key=lambda j: toks[j].encode())
+        for r, j in enumerate(order):
+            assert rank[off + j] == r
+        off += len(toks)
+    ids = p.lowered.node_ids
+    by_id = sorted(range(len(ids)), key=lambda i: ids[i].encode())
+    weight, expect = lw.table("lex_weight"), 1
+    for i in reversed(by_id):
+        assert weight[i] == expect
+        expect *= p.lowered.radix[i]
+
+
+@pytest.mark.parametrize("w", [W.config1(), W.config2(), W.config3(), W.random_scenario(7)], ids=lambda w: w.name)
+def test_lexkey_order_equals_identifier_order(loomlib, w):
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    p = O.problem(w.dag, w.library, w.bounds)
+    rng = random.Random(5)
+    picks = [rng.randrange(p.total) for _ in range(300)]
+    keyed = [(lw.evaluate(i)["lexkey"], O.identifier(p, i), i) for i in picks]
+    assert sorted(keyed, key=lambda t: t[0]) == sorted(keyed, key=lambda t: t[1].encode())
+    for i in picks[:40]:
+        assert lw.config(i)["identifier"] == O.identifier(p, i)
+
+
+@pytest.mark.parametrize("w", [W.config1(), W.config2(), W.config3(), W.config5()], ids=lambda w: w.name)
+def test_host_evaluate_matches_oracle(loomlib, w):
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    p = O.problem(w.dag, w.library, w.bounds)
+    rng = random.Random(11)
+    for i in [0, p.total - 1] + [rng.randrange(p.total) for _ in range(200)]:
+        a, b = lw.evaluate(i), O.estimates(p, i, i + 1)[0]
+        for k in ("latency_us", "gpu_wh", "cpu_wh", "total_wh", "dollars", "quality"):
+            assert a[k] == b[k], k
+
+
+def test_winner_order_and_reduce(loomlib):
+    w = W.config1()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    p = O.problem(w.dag, w.library, w.bounds)
+    for token in TOKENS:
+        obj = loom.objective(token)
+        winners = [loom.winner_from_dict(lw.evaluate(i)) for i in range(lw.total)]
+        best = loom.winner_reduce(winners, obj)
+        assert best["plan_index"] == O.argmin(p, {"constraint": token})["index"]
+        # order independence
+        rng = random.Random(3)
+        rng.shuffle(winners)
+        assert loom.winner_reduce(winners, obj)["plan_index"] == best["plan_index"]
+    with pytest.raises(loom.NoFeasibleConfigError):
+        loom.winner_reduce([loom.Winner(), loom.Winner()], loom.objective("MIN_COST"))
+
+
+def test_objective_parse():
+    o = loom.objective({"constraint": "MAX_QUALITY", "quality_floor": 3, "latency_slo_us": 99})
+    assert o.n_criteria == 3 and list(o.criteria)[:3] == [3, 1, 2]
+    assert o.has_quality_floor == 1 and o.quality_floor == 3 and o.has_latency_slo == 1 and o.latency_slo_us == 99
+    o = loom.objective({"criteria": ["min_cost_dollars", "min_energy"]})
+    assert o.n_criteria == 2 and list(o.criteria)[:2] == [0, 1]
+    with pytest.raises(loom.SchemaError, match="unknown constraint token 'FASTEST'"):
+        loom.objective("FASTEST")
+
+
+def test_lowering_errors_mirror_reference(loomlib):
+    w = W.config1()
+    dag = {"nodes": w.dag["nodes"] + [dict(w.dag["nodes"][0], id="t9_x", capability="nope")], "edges": w.dag["edges"]}
+    with pytest.raises(loom.UnknownCapabilityError, match="capability 'nope' is not registered"):
+        loom.Lowered(dag, w.library, w.bounds)
+    cyc = {"nodes": w.dag["nodes"], "edges": w.dag["edges"] + [
+        {"from": "t3_summarization", "to": "t0_frame_extraction", "kind": "text"}]}
+    with pytest.raises(loom.CycleError):
+        loom.Lowered(cyc, w.library, w.bounds)
+    with pytest.raises(loom.SchemaError):
+        loom.Lowered("{not json", w.library, w.bounds)
+    bad = dict(w.library, profiles=w.library["profiles"] + [dict(w.library["profiles"][0], units=99, throughput=0)])
+    with pytest.raises(loom.ValidationError, match="throughput must be > 0"):
+        loom.Lowered(w.dag, bad, w.bounds)
+
+
+def test_empty_dag_has_no_plans(loomlib):
+    w = W.config1()
+    lw = loom.Lowered({"nodes": [], "edges": []}, w.library, w.bounds)
+    assert lw.total == 0
+
+
+def test_device_entry_points_fail_loudly_without_gpu(loomlib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(loom.DeviceError, match="no CUDA device"):
+        loom.Context(0)
