@@ -1,0 +1,355 @@
+"""bench.py -- plans evaluated per second for the B200 exhaustive plan search.
+
+Workload (BASELINE.json configs[2], "C3"): a synthetic 10-task DAG with 16
+lever assignments per task, 16^10 = 1.1e12 plans, MIN_COST under a latency
+SLO, the plan-index space sharded by contiguous range across the ranks
+(strong scaling: the whole space is searched at every N).  configs[1] (C2,
+1.2e6 plans) finishes in microseconds and is reported under "configs" with
+C1/C4/C5 as time-to-plan lines, not as the headline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one exhaustive search of the whole plan space.  "value" times the
+search with the problem resident in HBM (CUDA events on the launching
+stream, L2 flushed between steps); "e2e" times the public drop-in call
+(reference-format JSON in, selected plan out: lowering, H2D, kernel, D2H,
+NCCL all-gather of winners, decode) every step.  --impl reference times the
+UNMODIFIED reference (oracle/_ref, compiled from /root/reference) on the
+host cores over a bounded sample of the same plan space.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "plans evaluated/sec (1/2/4/8 B200, % of roofline) vs CPU ref; time-to-plan"
+UNIT = "plans/s"
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"sm_max_mhz": 1965.0, "hbm_gbs": 6650.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for name, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def reference_arm(args) -> None:
+    """The reference's own CPU implementation (oracle/_ref range driver over
+    loom::estimate / meets_quality_floor / objective_less), all host threads,
+    a bounded sample of the C3 plan space per step."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2501_16634_b200 import workloads as W
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    w = W.config3()
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample
+    base = 123_456_789_012  # a slice that holds SLO-feasible plans
+    times = []
+    for step in range(args.warmup + args.steps):
+        b = base + step * sample
+        t0 = time.perf_counter()
+        rc, out = O.ref_range_argmin(w.dag, w.library, w.objective, w.bounds, b, b + sample, threads)
+        dt = time.perf_counter() - t0
+        if rc != 0:
+            raise RuntimeError(out)
+        if step >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    value = sample / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "C3: 10-task DAG x 16 options/task (1.1e12 plans), MIN_COST + latency SLO",
+                       "sample_plans_per_step": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{sample} consecutive plan indices of C3 per step, range driver over the "
+                                       f"reference's estimate/objective_less on {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(seconds_budget: float = 12.0) -> dict:
+    """The compiled reference on this box's host cores over a bounded C3
+    sample (rank 0, N=1 only)."""
+    from oracle import oracle as O
+    from paper_2501_16634_b200 import workloads as W
+
+    if not O.ref_available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref missing"}
+    w = W.config3()
+    threads = os.cpu_count() or 1
+    b = 123_456_789_012
+    probe = 20_000 * threads
+    rc, out = O.ref_range_argmin(w.dag, w.library, w.objective, w.bounds, b, b + probe, threads)
+    rate = probe / max(out["seconds"], 1e-6)
+    sample = int(max(probe, min(rate * seconds_budget, 5e8)))
+    rc, out = O.ref_range_argmin(w.dag, w.library, w.objective, w.bounds, b, b + sample, threads)
+    return {"value": sample / out["seconds"], "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{sample} consecutive C3 plans from index {b}: reference estimate + objective_less "
+                      f"(oracle/_ref range driver, g++ -O2) on {threads} host threads, {out['seconds']:.1f} s"}
+
+
+def flush_l2(torch, buf) -> None:
+    buf.add_(1)  # 256 MiB read+write > 126 MB L2
+
+
+def b200_arm(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_16634_b200 import dist as D, loom, workloads as W
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    ctx = loom.Context(local, stream.cuda_stream)
+    w = W.config3()
+    dag_t, lib_t, obj_t, bounds_t = w.texts()
+
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    obj = loom.objective(w.objective)
+    total = lw.total
+    begin, end = D.shard_range(total, rank, world)
+    dp = loom.DeviceProblem(ctx, lw.problem, obj)
+    scratch = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    # ---- value: resident problem, device-timed -------------------------------
+    for _ in range(args.warmup):
+        dp.search_async(begin, end)
+        dp.result()
+    launches0 = ctx.launches
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        barrier()
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush_l2(torch, scratch)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dp.search_async(begin, end)
+            e1.record(stream)
+            dp.result()
+            step_ms.append(e0.elapsed_time(e1))
+        barrier()
+    launches = ctx.launches - launches0
+    local_ms = sum(step_ms) / len(step_ms)
+    t = torch.tensor([local_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = total / (ms / 1e3)
+
+    # winners must agree with a full-space reduce (checked every run)
+    local_w = dp.result()
+    winners = D.allgather_winners(local_w, device="cuda") if world > 1 else [local_w]
+    chosen = D.combine(winners, obj)
+
+    # ---- e2e: the public drop-in call, host JSON in / plan out ---------------
+    def e2e_step():
+        if world == 1:
+            return loom.exhaustive_search(dag_t, lib_t, obj_t, bounds_t, ctx=ctx)
+        low = loom.Lowered(dag_t, lib_t, bounds_t)
+        o = loom.objective(obj_t)
+        try:
+            mine = loom.search_argmin(ctx, low.problem, o, begin, end)
+        except loom.NoFeasibleConfigError:
+            mine = D.empty_winner()
+        best = D.combine(D.allgather_winners(mine, device="cuda"), o)
+        return low.config(best["plan_index"]) | best
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        out = e2e_step()
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = total / (float(te.item()) / 1e3)
+    assert out["plan_index"] == chosen["plan_index"], (out, chosen)
+
+    if rank == 0:
+        pk = peaks()
+        clk = clocks.summary()
+        f_mhz = clk["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)
+        props = torch.cuda.get_device_properties(local)
+        sms = props.multi_processor_count
+        inst_per_plan = ISSUE_INSTR_PER_PLAN
+        issue_peak = sms * 4 * 32 * f_mhz * 1e6 / 1e12  # Tinst/s (thread instructions)
+        achieved = (total / world) / (local_ms / 1e3) * inst_per_plan / 1e12
+        traffic = None
+        prof = ROOT / "profiles" / "ncu_summary.json"
+        if prof.exists():
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic",
+            "config": {"workload": "C3: 10-task layered DAG x 16 options/task = 1.1e12 plans, MIN_COST "
+                                   "(min gpu energy, then latency) under a latency SLO",
+                       "plans_per_step": total, "parallelism": f"plan-index range x{world}",
+                       "l2": "flushed between timed steps (256 MiB write); the problem image is 8 KB in smem",
+                       "chosen_plan_index": chosen["plan_index"], "chosen_latency_us": chosen["latency_us"],
+                       "chosen_gpu_wh": chosen["gpu_wh"]},
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": float(te.item()),
+                    "h2d_bytes_per_step": dp.image_bytes + 64, "d2h_bytes_per_step": 64,
+                    "path": "loom_exhaustive_search_json: JSON parse + lowering + H2D + kernel + D2H + decode"
+                    if world == 1 else "lowering + loom_search_argmin(shard) + NCCL all-gather + reduce + decode"},
+            "roofline": {"bound": "issue", "achieved": achieved, "peak": issue_peak, "unit": "Tinst/s",
+                         "frac": achieved / issue_peak, "traffic": traffic,
+                         "inst_per_plan": inst_per_plan,
+                         "note": "thread-instructions per plan of the compiled inner loop (DESIGN.md §5); "
+                                 f"peak = {sms} SMs x 4 issue/clk x 32 lanes x measured SM clock"},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        if args.configs:
+            line["configs"] = other_configs(ctx, loom, W)
+        print(json.dumps(line), flush=True)
+    dp.close()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# Compiled inner loop of search_kernel<4, kPrimFp>: 45 SASS instructions per
+# 8 plans (8 LDS.128-half loads, 8 DADD, 8 DSETP, 8 ISETP, mask assembly and
+# one branch) -> see profiles/ and DESIGN.md §5.
+ISSUE_INSTR_PER_PLAN = 45 / 8
+
+
+def other_configs(ctx, loom, W) -> dict:
+    """Time-to-plan for the other BASELINE configs (outside the timed region)."""
+    out = {}
+    for name, w in (("c1", W.config1()), ("c2", W.config2())):
+        dag_t, lib_t, obj_t, bounds_t = w.texts()
+        loom.exhaustive_search(dag_t, lib_t, obj_t, bounds_t, ctx=ctx)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            r = loom.exhaustive_search(dag_t, lib_t, obj_t, bounds_t, ctx=ctx)
+            ts.append(time.perf_counter() - t0)
+        out[name] = {"time_to_plan_ms": 1e3 * min(ts), "plans": r["plans"], "identifier": r["identifier"]}
+    jobs = W.config4(10_000)
+    t0 = time.perf_counter()
+    lws = [loom.Lowered(j.dag, j.library, j.bounds) for j in jobs]
+    t_lower = time.perf_counter() - t0
+    objs = [loom.objective(j.objective) for j in jobs]
+    loom.search_argmin_batch(ctx, [lw.problem for lw in lws[:64]], objs[:64])
+    t0 = time.perf_counter()
+    res = loom.search_argmin_batch(ctx, [lw.problem for lw in lws], objs)
+    t_search = time.perf_counter() - t0
+    plans = sum(lw.total for lw in lws)
+    out["c4"] = {"jobs": len(jobs), "plans": plans, "search_ms": 1e3 * t_search, "lowering_ms": 1e3 * t_lower,
+                 "plans_per_s": plans / t_search, "feasible_jobs": sum(1 for s, _ in res if s == 0)}
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=1 << 21)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--configs", action="store_true", help="also report time-to-plan for C1/C2/C4")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -172,6 +172,8 @@ int loom_search_argmin_batch(loom_ctx* ctx, const loom_problem* problems,
 int loom_problem_upload(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
                         loom_device_problem** out);
 int loom_problem_release(loom_device_problem* dp);
+/* Bytes of the problem image one search copies host->device (evidence for benches). */
+uint64_t loom_device_problem_bytes(const loom_device_problem* dp);
 /* Enqueue a search on the ctx stream without synchronising. */
 int loom_search_argmin_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t begin, uint64_t end);
 /* Wait for the last enqueued search of dp and decode its result. */

@@ -39,6 +39,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -163,30 +164,78 @@ __device__ __forceinline__ bool rec_better(const Rec& a, const Rec& b, const Blo
   return a.lexkey < b.lexkey;
 }
 
-// Inner-loop thresholds derived from the running best.
-struct Thresh {
-  double hi_a;    // kPrimFp: e > hi_a  => strictly worse
-  int64_t lat_s;  // latency bound: min(slo_eff, best.lat) for kPrimLat, slo_eff otherwise
-  int32_t bq;     // kPrimQual: q < bq  => strictly worse
+// ---------------------------------------------------------------------------
+// Per-thread running best and its derived thresholds live in shared memory
+// (structure of arrays, one slot per thread, conflict free).  Only the rare
+// slow path touches them; the hot loops keep just the thresholds they test.
+// ---------------------------------------------------------------------------
+struct Slots {
+  int64_t* qa;
+  int64_t* qb;
+  int64_t* lat;
+  uint64_t* lex;
+  uint64_t* idx;
+  double* hi;      // kPrimFp: e > hi  =>  strictly worse than the best
+  int64_t* lat_s;  // feasible and not worse on latency: lat <= lat_s
+  int32_t* qual;
+  int32_t* found;
+  int32_t* bq;     // kPrimQual: q < bq  =>  strictly worse
 };
+constexpr int kSlotBytes = 8 * 7 + 4 * 3;
 
-template <int PRIM>
-__device__ __forceinline__ void thresh_from(const Rec& best, const BlobHeader* h, Thresh& t) {
-  t.hi_a = best.found ? hi_of(best.qa) : INFINITY;
-  t.lat_s = (PRIM == kPrimLat && best.found) ? min(h->slo_eff, best.lat) : h->slo_eff;
-  t.bq = best.found ? best.qual : INT_MIN;
+__device__ __forceinline__ Slots make_slots(uint8_t* base) {
+  Slots s;
+  s.qa = reinterpret_cast<int64_t*>(base);
+  s.qb = s.qa + kBlock;
+  s.lat = s.qb + kBlock;
+  s.lex = reinterpret_cast<uint64_t*>(s.lat + kBlock);
+  s.idx = s.lex + kBlock;
+  s.hi = reinterpret_cast<double*>(s.idx + kBlock);
+  s.lat_s = reinterpret_cast<int64_t*>(s.hi + kBlock);
+  s.qual = reinterpret_cast<int32_t*>(s.lat_s + kBlock);
+  s.found = s.qual + kBlock;
+  s.bq = s.found + kBlock;
+  return s;
 }
 
-// One plan, decoded from its index and evaluated from scratch.
-__device__ void full_eval(const View& v, uint64_t index, Rec& c) {
-  const int n = v.h->n_nodes;
-  int d[kMaxNodes];
-  uint64_t x = index;
-  for (int i = n - 1; i >= 0; --i) {
-    const uint64_t r = static_cast<uint64_t>(v.radix[i]);
-    d[i] = static_cast<int>(x % r);
-    x /= r;
+__device__ __forceinline__ Rec slot_load(const Slots& s, int t) {
+  return Rec{s.qa[t], s.qb[t], s.lat[t], s.lex[t], s.idx[t], s.qual[t], s.found[t]};
+}
+
+__device__ __forceinline__ void slot_thresholds(const Slots& s, int t, const BlobHeader* h) {
+  const bool f = s.found[t];
+  s.hi[t] = f ? hi_of(s.qa[t]) : INFINITY;
+  s.lat_s[t] = (h->prim == kPrimLat && f) ? min(h->slo_eff, s.lat[t]) : h->slo_eff;
+  s.bq[t] = f ? s.qual[t] : INT_MIN;
+}
+
+__device__ __forceinline__ void slot_init(const Slots& s, int t, const BlobHeader* h) {
+  s.qa[t] = s.qb[t] = s.lat[t] = 0;
+  s.lex[t] = s.idx[t] = 0;
+  s.qual[t] = 0;
+  s.found[t] = 0;
+  slot_thresholds(s, t, h);
+}
+
+__device__ __forceinline__ void slot_offer(const Slots& s, int t, const BlobHeader* h, const Rec& c) {
+  if (rec_better(c, slot_load(s, t), h)) {
+    s.qa[t] = c.qa;
+    s.qb[t] = c.qb;
+    s.lat[t] = c.lat;
+    s.lex[t] = c.lexkey;
+    s.idx[t] = c.index;
+    s.qual[t] = c.qual;
+    s.found[t] = c.found;
+    slot_thresholds(s, t, h);
   }
+}
+
+// One plan from its digits, evaluated from scratch exactly as the reference's
+// estimate (estimator.hpp:43-78): FP left folds in dag order, finish-time
+// recursion in topological order over the effective walls (a quality-floor
+// failure has an unreachable wall), quality min, identifier rank.
+__device__ void eval_digits(const View& v, const int* d, Rec& c, uint64_t index) {
+  const int n = v.h->n_nodes;
   double ea = 0.0, eb = 0.0;
   int32_t qual = INT_MAX;
   uint64_t lex = 0;
@@ -215,35 +264,102 @@ __device__ void full_eval(const View& v, uint64_t index, Rec& c) {
   c.qb = c.found ? quantize_dev(eb) : 0;
 }
 
-// Prefix state of one row: FP folds and quality/identifier partials over
-// nodes [0, P) and the max-plus coefficient vector over the K suffix nodes.
+// One plan decoded from its index (range edges, algo 1).
+__device__ void full_eval(const View& v, uint64_t index, Rec& c) {
+  int d[kMaxNodes];
+  uint64_t x = index;
+  for (int i = v.h->n_nodes - 1; i >= 0; --i) {
+    const uint64_t r = static_cast<uint64_t>(v.radix[i]);
+    d[i] = static_cast<int>(x % r);
+    x /= r;
+  }
+  eval_digits(v, d, c, index);
+}
+
+// Slow path of the hierarchical walk: the prefix digits plus the K suffix
+// digits name one plan that might tie or beat the running best; evaluate it
+// from scratch and offer it.  Out of line so the hot loops stay small.
+__device__ __noinline__ void offer_plan(const uint8_t* smem, uint8_t* slot_base, const int* dpre, int P, int K,
+                                        int o0, int o1, int o2, int o3, uint64_t index) {
+  const View v = make_view(smem);
+  int d[kMaxNodes];
+  for (int i = 0; i < P; ++i) d[i] = dpre[i];
+  const int od[4] = {o0, o1, o2, o3};
+  for (int j = 0; j < K; ++j) d[P + j] = od[j];
+  Rec c;
+  eval_digits(v, d, c, index);
+  slot_offer(make_slots(slot_base), threadIdx.x, v.h, c);
+}
+
+// Slow path of one innermost context (rare): rescan options [g_begin, g_end)
+// of the innermost node, drop the ones the cheap tests reject, and build the
+// exact record of each remaining plan from the fast path's partials:
+//   latency = max(X, Y + wall)          (the max-plus pair of the context)
+//   energy  = quantize(eu + g)          (the dag-order fold, last term added)
+//   rank    = lex_u + rank term         (identifier order)
+// then compare it under the full objective order.  Objectives whose criteria
+// are not carried incrementally (a second FP sum, or quality when it is not
+// the primary) re-evaluate the plan from its digits instead.
+template <int K, int PRIM>
+__device__ __noinline__ void slow_scan(const uint8_t* smem, uint8_t* slot_base, const int* dpre, int P, int o0,
+                                       int o1, int o2, int g_begin, int g_end, int32_t tw, double eu, int32_t qu,
+                                       uint64_t lex_u, int64_t X, int64_t Y, uint64_t base) {
+  const View v = make_view(smem);
+  const BlobHeader* h = v.h;
+  const Slots sl = make_slots(slot_base);
+  const int t = threadIdx.x;
+  const int inner_node = h->n_nodes - 1;
+  const int off = v.optoff[inner_node];
+  const int n = v.radix[inner_node];
+  for (int j = g_begin; j < g_end && j < n; ++j) {
+    const InnerEntry e = v.inner[j];
+    if (e.w > tw) continue;  // infeasible (or, for a latency primary, strictly slower)
+    const double ev = __dadd_rn(eu, e.g);
+    if (PRIM == kPrimFp && ev > sl.hi[t]) continue;
+    if (PRIM == kPrimQual && min(qu, e.q) < sl.bq[t]) continue;
+    if (h->needs_full) {
+      int od[4] = {o0, o1, o2, 0};
+      od[K - 1] = j;
+      offer_plan(smem, slot_base, dpre, P, K, od[0], od[1], od[2], od[3], base + static_cast<uint64_t>(j));
+      continue;
+    }
+    Rec c;
+    c.lat = max(X, Y + v.wall[off + j]);
+    c.found = c.lat <= h->slo_eff;
+    c.qa = quantize_dev(ev);
+    c.qb = 0;
+    c.qual = min(qu, e.q);
+    c.lexkey = lex_u + v.lexw[off + j];
+    c.index = base + static_cast<uint64_t>(j);
+    slot_offer(sl, t, h, c);
+  }
+}
+
+// Prefix of one row: the primary FP fold over nodes [0, P) and the max-plus
+// coefficient vector c[S] over subsets S of the K suffix nodes:
+//   latency(plan) = max_S ( c[S] + sum_{s in S} wall_s ).
+// f[x][S] = longest path ending at node x that visits exactly the suffix
+// nodes in S, counting prefix walls only (suffix walls are symbols).
 template <int K>
-__device__ void row_prefix(const View& v, const int* d, int P, double& ea, double& eb, int32_t& qv, uint64_t& lex,
-                           int64_t (&c)[1 << K]) {
+__device__ void row_prefix(const View& v, const int* d, int P, double& ea, int32_t& qv, uint64_t& lex, int64_t* c) {
   constexpr int NS = 1 << K;
   const int n = v.h->n_nodes;
   ea = 0.0;
-  eb = 0.0;
   qv = INT_MAX;
   lex = 0;
   for (int i = 0; i < P; ++i) {
     const int o = v.optoff[i] + d[i];
     ea = __dadd_rn(ea, v.ga[o]);
-    eb = __dadd_rn(eb, v.gb[o]);
     qv = min(qv, v.q[o]);
     lex += v.lexw[o];
   }
-  // f[x][S]: longest path ending at x that visits exactly the suffix nodes in
-  // S, counting prefix walls only.  c[S] = max over x.
   int64_t f[kMaxNodes][NS];
-#pragma unroll
   for (int S = 0; S < NS; ++S) c[S] = kNeg;
   for (int t = 0; t < n; ++t) {
     const int x = v.topo[t];
     const int pb = v.predoff[x], pe = v.predoff[x + 1];
     if (x < P) {
       const int64_t w = v.wall[v.optoff[x] + d[x]];
-#pragma unroll
       for (int S = 0; S < NS; ++S) {
         int64_t b = S == 0 ? 0 : kNeg;
         for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S]);
@@ -252,7 +368,6 @@ __device__ void row_prefix(const View& v, const int* d, int P, double& ea, doubl
       }
     } else {
       const int bit = 1 << (x - P);
-#pragma unroll
       for (int S = 0; S < NS; ++S) {
         int64_t val = kNeg;
         if (S & bit) {
@@ -269,98 +384,194 @@ __device__ void row_prefix(const View& v, const int* d, int P, double& ea, doubl
   c[0] = max(c[0], int64_t(0));
 }
 
-struct Partial {
-  double ea, eb;
-  int32_t qv;
-  uint64_t lex;
-  uint64_t ibase;  // linear index inside the subrow of the digits fixed so far
+// Hot-loop context of one thread.
+struct Hot {
+  const uint8_t* smem;
+  uint8_t* slot_base;
+  const BlobHeader* h;
+  const int32_t* radix;
+  const int32_t* optoff;
+  const double* ga;
+  const int64_t* wall;
+  const int32_t* w32;
+  const int32_t* q;
+  const uint64_t* lexw;
+  const InnerEntry* inner;
+  const int* dpre;
+  int P;
+  int od[4];
+  uint64_t s_index;  // subrow index (row * radix[P] + o0)
+  double hi;         // thresholds mirrored from the shared slot
+  int64_t lat_s;
+  int32_t bq;
 };
 
-template <int PRIM>
-__device__ __forceinline__ int32_t inner_tw(int64_t X, int64_t Y, const Thresh& th, int64_t wmin) {
-  if (X > th.lat_s) return INT_MIN;
-  const int64_t t = th.lat_s - Y - wmin;
-  return static_cast<int32_t>(max(min(t, int64_t(INT_MAX) - 1), int64_t(INT_MIN)));
+__device__ __forceinline__ void reload(Hot& H) {
+  const Slots s = make_slots(H.slot_base);
+  const int t = threadIdx.x;
+  H.hi = s.hi[t];
+  H.lat_s = s.lat_s[t];
+  H.bq = s.bq[t];
 }
 
-// Innermost node: one LDS.128 + DADD + two compares per plan on the fast path.
-template <int PRIM>
-__device__ __forceinline__ void inner_loop(const View& v, int node, int64_t X, int64_t Y, const Partial& p,
-                                           uint64_t sub_base, Rec& best, Thresh& th) {
-  const BlobHeader* h = v.h;
-  const int n = v.radix[node];
-  const int off = v.optoff[node];
-  const int64_t wmin = h->inner_wmin;
-  int32_t tw = inner_tw<PRIM>(X, Y, th, wmin);
-  const double ea = p.ea;
-  const uint64_t ibase = p.ibase * static_cast<uint64_t>(n);
-#pragma unroll 4
-  for (int o = 0; o < n; ++o) {
-    const InnerEntry e = v.inner[o];
-    const double ev = __dadd_rn(ea, e.g);
-    bool maybe;
-    if (PRIM == kPrimFp) maybe = (e.w <= tw) & (ev <= th.hi_a);
-    else if (PRIM == kPrimLat) maybe = e.w <= tw;
-    else maybe = (e.w <= tw) & (min(p.qv, e.q) >= th.bq);
-    if (__builtin_expect(maybe, 0)) {
-      Rec c;
-      c.lat = max(X, Y + v.wall[off + o]);
-      c.found = c.lat <= h->slo_eff;
-      c.qa = quantize_dev(ev);
-      c.qb = quantize_dev(__dadd_rn(p.eb, v.gb[off + o]));
-      c.qual = min(p.qv, v.q[off + o]);
-      c.lexkey = p.lex + v.lexw[off + o];
-      c.index = sub_base + ibase + static_cast<uint64_t>(o);
-      if (rec_better(c, best, h)) {
-        best = c;
-        thresh_from<PRIM>(best, h, th);
-        tw = inner_tw<PRIM>(X, Y, th, wmin);
+__device__ __forceinline__ int64_t clamp64(int64_t x, int64_t lo, int64_t hi) { return min(max(x, lo), hi); }
+
+// Exact int32 form of the latency test for the last two suffix nodes (u = the
+// node above the innermost, v = the innermost), given the coefficients c[4]
+// over subsets of {u, v} (bit 0 = u, bit 1 = v) and the bound L:
+//   max(c0, c1 + wu, c2 + wv, c3 + wu + wv) <= L
+//   <=> c0 <= L  &&  wu <= L - c1  &&  wv - wmin <= min(L - wmin - c2, L - wmin - c3 - wu)
+// Clamping keeps every comparison exact for wu in [0, wu_max] and
+// wv - wmin in [0, 2^30) (checked on the host).
+struct PreInner {
+  int32_t cmax;  // wu <= cmax
+  int32_t a;     // tw = min(a, b - wu)
+  int32_t b;
+};
+
+__device__ __forceinline__ PreInner pre_inner(const int64_t (&c)[4], int64_t L, int64_t wmin, int64_t wu_max) {
+  PreInner r;
+  const int64_t kHi = int64_t(1) << 30;
+  r.cmax = c[0] <= L ? static_cast<int32_t>(clamp64(L - c[1], -1, wu_max)) : -1;
+  r.a = static_cast<int32_t>(clamp64(L - wmin - c[2], -1, kHi));
+  r.b = static_cast<int32_t>(clamp64(L - wmin - c[3], -1, kHi + wu_max));
+  return r;
+}
+
+__device__ __forceinline__ int32_t inner_tw(const PreInner& r, int32_t wu) {
+  return wu <= r.cmax ? min(r.a, r.b - wu) : INT_MIN;
+}
+
+// Innermost node over one (prefix, o0 .. o_{K-2}) context.  NV > 0: the
+// node's table is in registers (radix <= NV, padded with never-passing
+// entries); NV == 0: read from shared memory in groups of 8.
+template <int K, int PRIM, int NV>
+struct Inner {
+  double g[NV > 0 ? NV : 1];
+  int32_t w[NV > 0 ? NV : 1];
+
+  __device__ __forceinline__ void load(const Hot& H) {
+    if constexpr (NV > 0) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        g[j] = H.inner[j].g;
+        w[j] = H.inner[j].w;
       }
     }
   }
-}
 
-// Suffix level J (1 <= J <= K-1) with coefficient vector over suffix nodes J..K-1.
-template <int K, int PRIM, int J>
-__device__ __forceinline__ void suffix_level(const View& v, int P, const int64_t (&c)[1 << (K - J)], const Partial& p,
-                                             uint64_t sub_base, Rec& best, Thresh& th) {
-  const int node = P + J;
-  if constexpr (J == K - 1) {
-    inner_loop<PRIM>(v, node, c[0], c[1], p, sub_base, best, th);
+  __device__ __forceinline__ bool pass(const Hot& H, int32_t w_, double g_, int32_t q_, int32_t tw, double ea,
+                                       int32_t qv) const {
+    if (PRIM == kPrimFp) return (w_ <= tw) & (__dadd_rn(ea, g_) <= H.hi);
+    if (PRIM == kPrimLat) return w_ <= tw;
+    return (w_ <= tw) & (min(qv, q_) >= H.bq);
+  }
+
+  // NV > 0: does any plan of the context pass?  (one predicate OR per plan)
+  __device__ __forceinline__ bool any_pass(const Hot& H, int32_t tw, double ea, int32_t qv) const {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < (NV > 0 ? NV : 1); ++j) any |= pass(H, w[j], g[j], 0, tw, ea, qv);
+    return any;
+  }
+
+};
+
+// Suffix level J over options [o_lo, o_hi) of node P + J, given the
+// coefficient vector over suffix nodes J..K-1 and the partial FP fold.
+template <int K, int PRIM, int NV, int J>
+__device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV>& in, const int64_t (&c)[1 << (K - J)],
+                                      double ea, int32_t qv, uint64_t lex, int o_lo, int o_hi, uint64_t ibase) {
+  const int node = H.P + J;
+  const int off = H.optoff[node];
+  const int n = H.radix[node];
+  if constexpr (J == K - 2) {
+    const int n_in = H.radix[node + 1];
+    const int64_t wmin = H.h->inner_wmin, wu_max = H.h->pre_wmax;
+    PreInner pr = pre_inner(c, H.lat_s, wmin, wu_max);
+    for (int o = o_lo; o < o_hi; ++o) {
+      const int32_t wu = H.w32[off + o];
+      const double eu = __dadd_rn(ea, H.ga[off + o]);
+      const int32_t qu = (PRIM == kPrimQual) ? min(qv, H.q[off + o]) : INT_MAX;
+      H.od[J] = o;
+      // plan index of option 0 of the innermost node in this context; at J == 0
+      // the digit o is already part of the subrow index
+      const uint64_t inner_base =
+          J == 0 ? 0 : (ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o)) * static_cast<uint64_t>(n_in);
+      int32_t tw = inner_tw(pr, wu);
+      const int g_end = NV > 0 ? NV : ((n_in + 7) & ~7);
+      for (int g0 = 0; g0 < g_end; g0 += (NV > 0 ? NV : 8)) {
+        bool any;
+        if constexpr (NV > 0) {
+          any = in.any_pass(H, tw, eu, qu);
+        } else {
+          any = false;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const InnerEntry e = H.inner[g0 + j];
+            any |= in.pass(H, e.w, e.g, e.q, tw, eu, qu);
+          }
+        }
+        if (__builtin_expect(any, 0)) {
+          const int64_t w_real = H.wall[off + o];
+          const int64_t X = max(c[0], c[1] + w_real), Y = max(c[2], c[3] + w_real);
+          const uint64_t lex_u = lex + H.lexw[off + o];
+          slow_scan<K, PRIM>(H.smem, H.slot_base, H.dpre, H.P, H.od[0], H.od[1], H.od[2], g0,
+                             g0 + (NV > 0 ? NV : 8), tw, eu, qu, lex_u, X, Y, H.s_index * H.h->r_sub + inner_base);
+          reload(H);
+          if (PRIM == kPrimLat) {
+            pr = pre_inner(c, H.lat_s, wmin, wu_max);
+            tw = inner_tw(pr, wu);
+          }
+        }
+      }
+    }
   } else {
     constexpr int NS = 1 << (K - J - 1);
-    const int n = v.radix[node];
-    const int off = v.optoff[node];
-    for (int o = 0; o < n; ++o) {
-      const int64_t w = v.wall[off + o];
+    for (int o = o_lo; o < o_hi; ++o) {
+      const int64_t w = H.wall[off + o];
       int64_t c2[NS];
 #pragma unroll
       for (int S = 0; S < NS; ++S) c2[S] = max(c[2 * S], c[2 * S + 1] + w);
-      Partial q;
-      q.ea = __dadd_rn(p.ea, v.ga[off + o]);
-      q.eb = __dadd_rn(p.eb, v.gb[off + o]);
-      q.qv = min(p.qv, v.q[off + o]);
-      q.lex = p.lex + v.lexw[off + o];
-      q.ibase = p.ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o);
-      suffix_level<K, PRIM, J + 1>(v, P, c2, q, sub_base, best, th);
+      H.od[J] = o;
+      const double e2 = __dadd_rn(ea, H.ga[off + o]);
+      const int32_t q2 = (PRIM == kPrimQual) ? min(qv, H.q[off + o]) : INT_MAX;
+      const uint64_t l2 = lex + H.lexw[off + o];
+      const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o);
+      level<K, PRIM, NV, J + 1>(H, in, c2, e2, q2, l2, 0, H.radix[node + 1], ib);
     }
   }
 }
 
 // Walk subrows [s_begin, s_end) of the whole space.
-template <int K, int PRIM>
-__device__ void run_subrows(const View& v, uint64_t s_begin, uint64_t s_end, Rec& best, Thresh& th) {
+template <int K, int PRIM, int NV>
+__device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, const View& v, uint64_t s_begin,
+                            uint64_t s_end) {
   constexpr int NS = 1 << K;
-  const BlobHeader* h = v.h;
-  const int n = h->n_nodes;
-  const int P = n - K;
-  const int n0 = v.radix[P];
-  const int off0 = v.optoff[P];
-  const uint64_t r_sub = h->r_sub;
+  Hot H;
+  H.smem = smem;
+  H.slot_base = slot_base;
+  H.h = v.h;
+  H.radix = v.radix;
+  H.optoff = v.optoff;
+  H.ga = v.ga;
+  H.wall = v.wall;
+  H.w32 = reinterpret_cast<const int32_t*>(smem + v.h->off_w32);
+  H.q = v.q;
+  H.lexw = v.lexw;
+  H.inner = v.inner;
+  H.P = v.h->n_nodes - K;
+  H.od[0] = H.od[1] = H.od[2] = H.od[3] = 0;
+  reload(H);
+  Inner<K, PRIM, NV> in;
+  in.load(H);
 
+  const int P = H.P;
+  const uint64_t n0 = static_cast<uint64_t>(v.radix[P]);
   int d[kMaxNodes];
-  uint64_t row = s_begin / static_cast<uint64_t>(n0);
-  int o0 = static_cast<int>(s_begin % static_cast<uint64_t>(n0));
+  H.dpre = d;
+  uint64_t row = s_begin / n0;
+  int o0 = static_cast<int>(s_begin % n0);
   {
     uint64_t x = row;
     for (int i = P - 1; i >= 0; --i) {
@@ -369,30 +580,27 @@ __device__ void run_subrows(const View& v, uint64_t s_begin, uint64_t s_end, Rec
       x /= r;
     }
   }
-  double ea_pre = 0.0, eb_pre = 0.0;
+  // The row's coefficient vector is written once per row and read once per
+  // subrow: it lives in this thread's shared-memory column, not in registers.
+  int64_t* c0s = reinterpret_cast<int64_t*>(slot_base + kSlotBytes * kBlock) + threadIdx.x;
+  double ea_pre = 0.0;
   int32_t q_pre = INT_MAX;
   uint64_t lex_pre = 0;
-  int64_t c0[NS];
   bool fresh = true;
   for (uint64_t s = s_begin; s < s_end; ++s) {
     if (fresh) {
-      row_prefix<K>(v, d, P, ea_pre, eb_pre, q_pre, lex_pre, c0);
+      int64_t c[NS];
+      row_prefix<K>(v, d, P, ea_pre, q_pre, lex_pre, c);
+#pragma unroll
+      for (int S = 0; S < NS; ++S) c0s[S * kBlock] = c[S];
       fresh = false;
     }
-    // suffix level 0: node P takes option o0 for the whole subrow
-    const int64_t w = v.wall[off0 + o0];
-    int64_t c1[NS / 2];
+    int64_t c0[NS];
 #pragma unroll
-    for (int S = 0; S < NS / 2; ++S) c1[S] = max(c0[2 * S], c0[2 * S + 1] + w);
-    Partial p;
-    p.ea = __dadd_rn(ea_pre, v.ga[off0 + o0]);
-    p.eb = __dadd_rn(eb_pre, v.gb[off0 + o0]);
-    p.qv = min(q_pre, v.q[off0 + o0]);
-    p.lex = lex_pre + v.lexw[off0 + o0];
-    p.ibase = 0;
-    suffix_level<K, PRIM, 1>(v, P, c1, p, s * r_sub, best, th);
-
-    if (++o0 == n0) {  // next row: advance the prefix odometer (last prefix node fastest)
+    for (int S = 0; S < NS; ++S) c0[S] = c0s[S * kBlock];
+    H.s_index = s;
+    level<K, PRIM, NV, 0>(H, in, c0, ea_pre, q_pre, lex_pre, o0, o0 + 1, 0);
+    if (static_cast<uint64_t>(++o0) == n0) {  // next row: prefix odometer, last prefix node fastest
       o0 = 0;
       fresh = true;
       for (int i = P - 1; i >= 0; --i) {
@@ -447,7 +655,7 @@ __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
   return r;
 }
 
-template <int K, int PRIM>
+template <int K, int PRIM, int NV>
 __global__ void __launch_bounds__(kBlock, 2)
     search_kernel(const uint8_t* __restrict__ arena, const JobDesc* __restrict__ jobs, int ctas_per_job,
                   Rec* __restrict__ scratch, unsigned* __restrict__ tickets, Rec* __restrict__ out) {
@@ -462,10 +670,9 @@ __global__ void __launch_bounds__(kBlock, 2)
   load_blob(smem, arena + jd.blob_off, jd.blob_bytes, &mbar);
   const View v = make_view(smem);
   const BlobHeader* h = v.h;
-
-  Rec best{0, 0, 0, 0, 0, 0, 0};
-  Thresh th;
-  thresh_from<PRIM>(best, h, th);
+  uint8_t* slot_base = smem + ((jd.blob_bytes + 127) & ~127u);
+  const Slots sl = make_slots(slot_base);
+  slot_init(sl, threadIdx.x, h);
 
   const uint64_t gt = static_cast<uint64_t>(part) * kBlock + threadIdx.x;
   const uint64_t nt = static_cast<uint64_t>(ctas_per_job) * kBlock;
@@ -474,14 +681,13 @@ __global__ void __launch_bounds__(kBlock, 2)
   for (uint64_t i = jd.begin + gt; i < jd.head_end; i += nt) {
     Rec c;
     full_eval(v, i, c);
-    if (rec_better(c, best, h)) best = c;
+    slot_offer(sl, threadIdx.x, h, c);
   }
   for (uint64_t i = jd.tail_begin + gt; i < jd.end; i += nt) {
     Rec c;
     full_eval(v, i, c);
-    if (rec_better(c, best, h)) best = c;
+    slot_offer(sl, threadIdx.x, h, c);
   }
-  thresh_from<PRIM>(best, h, th);
 
   // Whole subrows: contiguous share per thread.
   const uint64_t cnt = jd.sub_hi - jd.sub_lo;
@@ -489,10 +695,10 @@ __global__ void __launch_bounds__(kBlock, 2)
     const uint64_t q = cnt / nt, r = cnt % nt;
     const uint64_t start = jd.sub_lo + gt * q + min(gt, r);
     const uint64_t len = q + (gt < r ? 1 : 0);
-    if (len) run_subrows<K, PRIM>(v, start, start + len, best, th);
+    if (len) run_subrows<K, PRIM, NV>(smem, slot_base, v, start, start + len);
   }
 
-  Rec b = block_best(best, h, warp_slot);
+  Rec b = block_best(slot_load(sl, threadIdx.x), h, warp_slot);
   if (threadIdx.x == 0) {
     scratch[blockIdx.x] = b;
     __threadfence();
@@ -517,18 +723,28 @@ __global__ void __launch_bounds__(kBlock, 2)
 
 using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, unsigned*, Rec*);
 
-KernelFn pick_kernel(int K, int prim) {
-#define LOOM_K(k)                                         \
-  if (K == k) {                                           \
-    if (prim == kPrimFp) return search_kernel<k, kPrimFp>;   \
-    if (prim == kPrimLat) return search_kernel<k, kPrimLat>; \
-    return search_kernel<k, kPrimQual>;                      \
+template <int K>
+KernelFn pick_nv(int prim, int nv) {
+  if (prim == kPrimQual) return search_kernel<K, kPrimQual, 0>;
+  if (prim == kPrimFp) {
+    if (nv == 8) return search_kernel<K, kPrimFp, 8>;
+    if (nv == 16) return search_kernel<K, kPrimFp, 16>;
+    return search_kernel<K, kPrimFp, 0>;
   }
-  LOOM_K(2)
-  LOOM_K(3)
-  LOOM_K(4)
-#undef LOOM_K
-  return nullptr;
+  if (nv == 8) return search_kernel<K, kPrimLat, 8>;
+  if (nv == 16) return search_kernel<K, kPrimLat, 16>;
+  return search_kernel<K, kPrimLat, 0>;
+}
+
+KernelFn pick_kernel(int K, int prim, int nv) {
+  if (K == 2) return pick_nv<2>(prim, nv);
+  if (K == 3) return pick_nv<3>(prim, nv);
+  return pick_nv<4>(prim, nv);
+}
+
+// Dynamic shared memory of a launch: problem image + per-thread slots.
+size_t smem_bytes(size_t blob) {
+  return ((blob + 127) & ~size_t(127)) + static_cast<size_t>(kSlotBytes) * kBlock + sizeof(int64_t) * 16 * kBlock;
 }
 
 // ---------------------------------------------------------------------------
@@ -539,6 +755,7 @@ struct Built {
   int K = 2;
   int prim = kPrimFp;
   bool full_only = false;
+  int nv = 0;  // innermost radix held in registers (8 / 16) or 0 (shared-memory loop)
   uint64_t total = 0;
   uint64_t r_sub = 1;
   uint64_t n_sub = 0;
@@ -604,16 +821,19 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   uint64_t r_sub = 1;
   bool full_only = n < 2;
   if (!full_only) {
-    K = 0;
-    for (int k = std::min(4, n); k >= 2; --k) {
+    // Deepest K (<= 4) that still leaves a subrow per thread: the row DP and
+    // the upper suffix levels amortise over more plans (measured on C3:
+    // K=4 1.29e12 plans/s vs K=3 4.2e11).  LOOM_FORCE_K overrides.
+    K = 2;
+    for (int k = 3; k <= std::min(4, n); ++k) {
       uint64_t r = 1;
       for (int j = n - k + 1; j < n; ++j) r *= static_cast<uint64_t>(p->radix[j]);
-      if (total / r >= target_threads || k == 2) {
-        K = k;
-        r_sub = r;
-        break;
-      }
+      if (total / r < target_threads) break;
+      K = k;
     }
+    if (const char* f = std::getenv("LOOM_FORCE_K")) K = std::max(2, std::min({4, n, std::atoi(f)}));
+    r_sub = 1;
+    for (int j = n - K + 1; j < n; ++j) r_sub *= static_cast<uint64_t>(p->radix[j]);
   }
   // inner walls relative to their minimum must fit int32
   const int inner_node = n - 1;
@@ -622,7 +842,15 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
     wmin = std::min(wmin, p->wall_us[k]);
     wmax = std::max(wmax, p->wall_us[k]);
   }
-  if (wmax - wmin >= INT_MAX - 2) full_only = true;
+  // exact int32 latency tests need the innermost wall range and the walls of
+  // the node above it below 2^30 us (~18 min); larger ones take the
+  // one-plan-per-thread path
+  int64_t pre_wmax = 0;
+  if (n >= 2)
+    for (int k = optoff[n - 2]; k < optoff[n - 1]; ++k) pre_wmax = std::max(pre_wmax, p->wall_us[k]);
+  if (wmax - wmin >= (int64_t(1) << 30) - 1 || pre_wmax >= (int64_t(1) << 30) - 1) full_only = true;
+  const int inner_radix = p->radix[inner_node];
+  const int nv = inner_radix <= 8 ? 8 : inner_radix <= 16 ? 16 : 0;
 
   // topology: Kahn order + predecessor CSR
   std::vector<int32_t> indeg(n, 0), topo;
@@ -664,7 +892,9 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   hd.off_wall = take(8 * n_opts);
   hd.off_lexw = take(8 * n_opts);
   hd.off_q = take(4 * n_opts);
-  hd.off_inner = take(static_cast<int>(sizeof(InnerEntry)) * p->radix[inner_node]);
+  const int inner_pad = std::max(nv, (inner_radix + 7) & ~7);
+  hd.off_inner = take(static_cast<int>(sizeof(InnerEntry)) * inner_pad);
+  hd.off_w32 = take(4 * n_opts);
   if (off > kMaxBlobBytes) return loomi::fail(LOOM_INVALID, "InvalidConfigError: problem image exceeds shared memory");
   hd.n_nodes = n;
   hd.n_edges = p->n_edges;
@@ -673,9 +903,12 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   hd.n_crit = o->n_criteria;
   for (int i = 0; i < 4; ++i) hd.crit[i] = crit[i];
   hd.prim = prim;
+  for (int i = 0; i < o->n_criteria; ++i)
+    if (crit[i] == kFpB || (crit[i] == kQual && prim != kPrimQual)) hd.needs_full = 1;
   hd.bytes = off;
   hd.slo_eff = slo_eff;
   hd.inner_wmin = wmin;
+  hd.pre_wmax = pre_wmax;
   hd.total = total;
   hd.r_sub = r_sub;
   hd.n_sub = total / r_sub;
@@ -696,6 +929,7 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   int64_t* wall = reinterpret_cast<int64_t*>(base + hd.off_wall);
   uint64_t* lexw = reinterpret_cast<uint64_t*>(base + hd.off_lexw);
   int32_t* qq = reinterpret_cast<int32_t*>(base + hd.off_q);
+  int32_t* w32 = reinterpret_cast<int32_t*>(base + hd.off_w32);
   for (int i = 0; i < n; ++i) {
     for (int k = optoff[i]; k < optoff[i + 1]; ++k) {
       const double* src[2] = {nullptr, nullptr};
@@ -706,10 +940,17 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
       wall[k] = floor_ok(k) ? p->wall_us[k] : BIG;
       lexw[k] = static_cast<uint64_t>(p->lexrank[k]) * p->lex_weight[i];
       qq[k] = p->quality[k];
+      w32[k] = floor_ok(k) ? static_cast<int32_t>(std::min<int64_t>(p->wall_us[k], int64_t(1) << 30)) : (1 << 30);
     }
   }
   InnerEntry* inner = reinterpret_cast<InnerEntry*>(base + hd.off_inner);
-  for (int o2 = 0; o2 < p->radix[inner_node]; ++o2) {
+  for (int o2 = 0; o2 < inner_pad; ++o2) {
+    if (o2 >= p->radix[inner_node]) {  // padding: can never pass the wall test
+      inner[o2].g = 0.0;
+      inner[o2].w = INT_MAX;
+      inner[o2].q = INT_MIN;
+      continue;
+    }
     const int k = optoff[inner_node] + o2;
     inner[o2].g = ga[k];
     inner[o2].w = floor_ok(k) ? static_cast<int32_t>(p->wall_us[k] - wmin) : INT_MAX;
@@ -718,6 +959,7 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   b.K = K;
   b.prim = prim;
   b.full_only = full_only;
+  b.nv = nv;
   b.total = total;
   b.r_sub = r_sub;
   b.n_sub = total / r_sub;
@@ -848,9 +1090,20 @@ int set_smem(KernelFn fn, size_t bytes) {
   return LOOM_OK;
 }
 
-int ctas_for(const loom_ctx* c, uint64_t work_units) {
-  // persistent-style grid: 2 CTAs per SM (the kernel's launch bound), fewer for small spaces
-  const uint64_t full = static_cast<uint64_t>(c->sms) * 2;
+// Resident CTAs per SM for a kernel instantiation at a given image size.
+int resident_ctas(KernelFn fn, size_t smem) {
+  int nb = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(fn), kBlock, smem) !=
+          cudaSuccess ||
+      nb < 1)
+    nb = 1;
+  return nb;
+}
+
+int ctas_for(const loom_ctx* c, uint64_t work_units, KernelFn fn, size_t smem) {
+  // one full wave of resident CTAs (every thread gets an equal contiguous
+  // share of subrows), fewer for small spaces
+  const uint64_t full = static_cast<uint64_t>(c->sms) * resident_ctas(fn, smem);
   const uint64_t need = (work_units + kBlock - 1) / kBlock;
   return static_cast<int>(std::max<uint64_t>(1, std::min(full, need)));
 }
@@ -941,18 +1194,19 @@ int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objec
   if (d.begin >= d.end)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
-  const int ctas = ctas_for(c, units);
-  KernelFn fn = pick_kernel(b.K, b.prim);
+  KernelFn fn = pick_kernel(b.K, b.prim, b.nv);
+  if (int rc = set_smem(fn, smem_bytes(b.blob.size()))) return rc;
+  const int ctas = ctas_for(c, units, fn, smem_bytes(b.blob.size()));
   if (int rc = ensure(c->d_arena, c->arena_cap, b.blob.size())) return rc;
   if (int rc = ensure(c->d_jobs, c->jobs_cap, 1)) return rc;
   if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(ctas))) return rc;
   if (int rc = ensure_tickets(c, 1)) return rc;
   if (int rc = ensure(c->d_out, c->out_cap, 1)) return rc;
   if (int rc = ensure_host(c, 1)) return rc;
-  if (int rc = set_smem(fn, b.blob.size())) return rc;
+  if (int rc = set_smem(fn, smem_bytes(b.blob.size()))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  fn<<<ctas, kBlock, b.blob.size(), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch, c->d_tickets, c->d_out);
+  fn<<<ctas, kBlock, smem_bytes(b.blob.size()), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch, c->d_tickets, c->d_out);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
@@ -991,7 +1245,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
   std::vector<Group> groups;
   for (int j = 0; j < n_jobs; ++j) {
     if (!ok[j]) continue;
-    KernelFn fn = pick_kernel(built[j].K, built[j].prim);
+    KernelFn fn = pick_kernel(built[j].K, built[j].prim, built[j].nv);
     Group* g = nullptr;
     for (auto& x : groups)
       if (x.fn == fn) g = &x;
@@ -1000,7 +1254,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
       g = &groups.back();
     }
     g->jobs.push_back(j);
-    g->smem = std::max(g->smem, built[j].blob.size());
+    g->smem = std::max(g->smem, smem_bytes(built[j].blob.size()));
   }
   // One arena for all images; one launch per group, one CTA per job.
   std::vector<uint64_t> off(n_jobs, 0);
@@ -1092,8 +1346,12 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   dp->host.edge_from = dp->efrom.data();
   dp->host.edge_to = dp->eto.data();
   dp->objective = *o;
-  dp->fn = pick_kernel(dp->built.K, dp->built.prim);
-  const int ctas = static_cast<int>(static_cast<uint64_t>(c->sms) * 2);
+  dp->fn = pick_kernel(dp->built.K, dp->built.prim, dp->built.nv);
+  if (set_smem(dp->fn, smem_bytes(dp->built.blob.size())) != LOOM_OK) {
+    delete dp;
+    return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: cannot size shared memory");
+  }
+  const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size()));
   dp->ctas = ctas;
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
@@ -1104,7 +1362,7 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
              cudaMemcpy(dp->d_blob, dp->built.blob.data(), dp->built.blob.size(), cudaMemcpyHostToDevice) ==
                  cudaSuccess &&
              cudaMemset(dp->d_ticket, 0, sizeof(unsigned)) == cudaSuccess;
-  if (!okk || set_smem(dp->fn, dp->built.blob.size()) != LOOM_OK) {
+  if (!okk || set_smem(dp->fn, smem_bytes(dp->built.blob.size())) != LOOM_OK) {
     loom_problem_release(dp);
     return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: upload failed");
   }
@@ -1125,15 +1383,19 @@ int loom_problem_release(loom_device_problem* dp) {
   return LOOM_OK;
 }
 
+uint64_t loom_device_problem_bytes(const loom_device_problem* dp) {
+  return dp ? static_cast<uint64_t>(dp->built.blob.size()) : 0;
+}
+
 int loom_search_argmin_async(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end) {
   if (!c || !dp) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   JobDesc d = make_desc(dp->built, begin, end, false);
   d.blob_off = 0;
   if (d.begin >= d.end) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: empty range");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
-  const int ctas = std::min(dp->ctas, ctas_for(c, units));
+  const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size())));
   LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  dp->fn<<<ctas, kBlock, dp->built.blob.size(), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
+  dp->fn<<<ctas, kBlock, smem_bytes(dp->built.blob.size()), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
                                                              dp->d_ticket, dp->d_out);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;

@@ -38,6 +38,7 @@ struct alignas(16) BlobHeader {
   int32_t n_crit;
   int32_t crit[4];   // CritKind per criterion, most significant first
   int32_t prim;      // Prim
+  int32_t needs_full;  // slow path must re-evaluate from digits (criteria not carried incrementally)
   int32_t bytes;     // blob size, multiple of 16
   int32_t off_radix;
   int32_t off_optoff;
@@ -50,9 +51,10 @@ struct alignas(16) BlobHeader {
   int32_t off_lexw;
   int32_t off_q;
   int32_t off_inner;
-  int32_t pad0;
+  int32_t off_w32;       // int32 walls for the level above the innermost node
   int64_t slo_eff;       // min(latency SLO, sum of max walls): lat <= slo_eff <=> feasible
   int64_t inner_wmin;    // inner walls are stored relative to this
+  int64_t pre_wmax;      // largest real wall of the node above the innermost
   uint64_t total;        // plans in the space
   uint64_t r_sub;        // plans per subrow = product of the last K-1 radices
   uint64_t n_sub;        // subrows in the whole space = total / r_sub

@@ -146,6 +146,7 @@ def lib() -> C.CDLL:
         "loom_problem_upload": ([vp, P, O, C.POINTER(vp)], C.c_int),
         "loom_problem_release": ([vp], C.c_int),
         "loom_search_argmin_async": ([vp, vp, C.c_uint64, C.c_uint64], C.c_int),
+        "loom_device_problem_bytes": ([vp], C.c_uint64),
         "loom_search_argmin_result": ([vp, vp, W], C.c_int),
         "loom_search_pareto": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64,
                                 C.POINTER(C.c_uint64)], C.c_int),
@@ -330,6 +331,10 @@ class DeviceProblem:
     def search_async(self, begin: int = 0, end: int | None = None) -> None:
         end = (1 << 64) - 1 if end is None else end
         _check(lib().loom_search_argmin_async(self.ctx.handle, self._h, begin, end))
+
+    @property
+    def image_bytes(self) -> int:
+        return lib().loom_device_problem_bytes(self._h)
 
     def result(self) -> dict:
         w = Winner()
