@@ -335,59 +335,11 @@ __device__ __noinline__ void slow_scan(const uint8_t* smem, uint8_t* slot_base, 
   }
 }
 
-// Prefix of one row: the primary FP fold over nodes [0, P) and the max-plus
-// coefficient vector c[S] over subsets S of the K suffix nodes:
-//   latency(plan) = max_S ( c[S] + sum_{s in S} wall_s ).
-// f[x][S] = longest path ending at node x that visits exactly the suffix
-// nodes in S, counting prefix walls only (suffix walls are symbols).
-template <int K>
-__device__ void row_prefix(const View& v, const int* d, int P, double& ea, int32_t& qv, uint64_t& lex, int64_t* c) {
-  constexpr int NS = 1 << K;
-  const int n = v.h->n_nodes;
-  ea = 0.0;
-  qv = INT_MAX;
-  lex = 0;
-  for (int i = 0; i < P; ++i) {
-    const int o = v.optoff[i] + d[i];
-    ea = __dadd_rn(ea, v.ga[o]);
-    qv = min(qv, v.q[o]);
-    lex += v.lexw[o];
-  }
-  int64_t f[kMaxNodes][NS];
-  for (int S = 0; S < NS; ++S) c[S] = kNeg;
-  for (int t = 0; t < n; ++t) {
-    const int x = v.topo[t];
-    const int pb = v.predoff[x], pe = v.predoff[x + 1];
-    if (x < P) {
-      const int64_t w = v.wall[v.optoff[x] + d[x]];
-      for (int S = 0; S < NS; ++S) {
-        int64_t b = S == 0 ? 0 : kNeg;
-        for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S]);
-        f[x][S] = b + w;
-        c[S] = max(c[S], f[x][S]);
-      }
-    } else {
-      const int bit = 1 << (x - P);
-      for (int S = 0; S < NS; ++S) {
-        int64_t val = kNeg;
-        if (S & bit) {
-          const int S2 = S ^ bit;
-          int64_t b = S2 == 0 ? 0 : kNeg;
-          for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S2]);
-          val = b;
-        }
-        f[x][S] = val;
-        c[S] = max(c[S], val);
-      }
-    }
-  }
-  c[0] = max(c[0], int64_t(0));
-}
-
 // Hot-loop context of one thread.
 struct Hot {
   const uint8_t* smem;
   uint8_t* slot_base;
+  uint8_t* coef_base;
   const BlobHeader* h;
   const int32_t* radix;
   const int32_t* optoff;
@@ -479,15 +431,35 @@ struct Inner {
 
 // Suffix level J over options [o_lo, o_hi) of node P + J, given the
 // coefficient vector over suffix nodes J..K-1 and the partial FP fold.
+// Per-thread coefficient columns in shared memory: the input vector of suffix
+// level J (2^(K-J) int64 entries) sits at column offset sum_{j<J} 2^(K-j),
+// entry S at [S * kBlock + tid] (conflict free).  Keeping them out of the
+// register file leaves the registers to the innermost table and thresholds.
+template <int K>
+__device__ __forceinline__ int64_t* coef_col(uint8_t* coef_base, int J) {
+  int off = 0;
+  for (int j = 0; j < J; ++j) off += 1 << (K - j);
+  return reinterpret_cast<int64_t*>(coef_base) + off * kBlock + threadIdx.x;
+}
+
+template <int K>
+constexpr int coef_entries() {
+  int e = 0;
+  for (int j = 0; j <= K - 2; ++j) e += 1 << (K - j);
+  return e;
+}
+
 template <int K, int PRIM, int NV, int J>
-__device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV>& in, const int64_t (&c)[1 << (K - J)],
-                                      double ea, int32_t qv, uint64_t lex, int o_lo, int o_hi, uint64_t ibase) {
+__device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV>& in, double ea, int32_t qv, uint64_t lex,
+                                      int o_lo, int o_hi, uint64_t ibase) {
   const int node = H.P + J;
   const int off = H.optoff[node];
   const int n = H.radix[node];
+  const int64_t* cin = coef_col<K>(H.coef_base, J);
   if constexpr (J == K - 2) {
     const int n_in = H.radix[node + 1];
     const int64_t wmin = H.h->inner_wmin, wu_max = H.h->pre_wmax;
+    const int64_t c[4] = {cin[0], cin[kBlock], cin[2 * kBlock], cin[3 * kBlock]};
     PreInner pr = pre_inner(c, H.lat_s, wmin, wu_max);
     for (int o = o_lo; o < o_hi; ++o) {
       const int32_t wu = H.w32[off + o];
@@ -514,13 +486,14 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV>& in, cons
         }
         if (__builtin_expect(any, 0)) {
           const int64_t w_real = H.wall[off + o];
-          const int64_t X = max(c[0], c[1] + w_real), Y = max(c[2], c[3] + w_real);
+          const int64_t X = max(cin[0], cin[kBlock] + w_real), Y = max(cin[2 * kBlock], cin[3 * kBlock] + w_real);
           const uint64_t lex_u = lex + H.lexw[off + o];
           slow_scan<K, PRIM>(H.smem, H.slot_base, H.dpre, H.P, H.od[0], H.od[1], H.od[2], g0,
                              g0 + (NV > 0 ? NV : 8), tw, eu, qu, lex_u, X, Y, H.s_index * H.h->r_sub + inner_base);
           reload(H);
           if (PRIM == kPrimLat) {
-            pr = pre_inner(c, H.lat_s, wmin, wu_max);
+            const int64_t cc[4] = {cin[0], cin[kBlock], cin[2 * kBlock], cin[3 * kBlock]};
+            pr = pre_inner(cc, H.lat_s, wmin, wu_max);
             tw = inner_tw(pr, wu);
           }
         }
@@ -528,29 +501,75 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV>& in, cons
     }
   } else {
     constexpr int NS = 1 << (K - J - 1);
+    int64_t* cout = coef_col<K>(H.coef_base, J + 1);
     for (int o = o_lo; o < o_hi; ++o) {
       const int64_t w = H.wall[off + o];
-      int64_t c2[NS];
 #pragma unroll
-      for (int S = 0; S < NS; ++S) c2[S] = max(c[2 * S], c[2 * S + 1] + w);
+      for (int S = 0; S < NS; ++S) cout[S * kBlock] = max(cin[2 * S * kBlock], cin[(2 * S + 1) * kBlock] + w);
       H.od[J] = o;
       const double e2 = __dadd_rn(ea, H.ga[off + o]);
       const int32_t q2 = (PRIM == kPrimQual) ? min(qv, H.q[off + o]) : INT_MAX;
       const uint64_t l2 = lex + H.lexw[off + o];
       const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o);
-      level<K, PRIM, NV, J + 1>(H, in, c2, e2, q2, l2, 0, H.radix[node + 1], ib);
+      level<K, PRIM, NV, J + 1>(H, in, e2, q2, l2, 0, H.radix[node + 1], ib);
     }
   }
 }
 
-// Walk subrows [s_begin, s_end) of the whole space.
+// Warp-cooperative longest-path DP for one DP group: lane S computes state S
+// (a subset of the KD symbolic suffix nodes) for every node in topological
+// order; f lives in per-warp shared memory, so a state of one lane can read
+// the predecessor states of another (S without the node's bit).  Output:
+// cw[S] = max over nodes of f[x][S], the max-plus coefficient vector.
+template <int KD>
+__device__ void warp_dp(const View& v, const int* dtop, int Pd, int64_t* fw, int64_t* cw) {
+  constexpr int NS = 1 << KD;
+  static_assert(NS <= 32, "one state per lane");
+  const int S = threadIdx.x & 31;
+  const bool act = S < NS;
+  const int n = v.h->n_nodes;
+  int64_t cmax = kNeg;
+  for (int t = 0; t < n; ++t) {
+    const int x = v.topo[t];
+    const int pb = v.predoff[x], pe = v.predoff[x + 1];
+    if (act) {
+      int64_t val = kNeg;
+      if (x < Pd) {
+        int64_t b = S == 0 ? 0 : kNeg;
+        for (int e = pb; e < pe; ++e) b = max(b, fw[v.pred[e] * 32 + S]);
+        val = b + v.wall[v.optoff[x] + dtop[x]];
+      } else {
+        const int bit = 1 << (x - Pd);
+        if (S & bit) {
+          const int S2 = S ^ bit;
+          int64_t b = S2 == 0 ? 0 : kNeg;
+          for (int e = pb; e < pe; ++e) b = max(b, fw[v.pred[e] * 32 + S2]);
+          val = b;
+        }
+      }
+      fw[x * 32 + S] = val;
+      cmax = max(cmax, val);
+    }
+    __syncwarp();
+  }
+  if (act) cw[S] = S == 0 ? max(cmax, int64_t(0)) : cmax;
+  __syncwarp();
+}
+
+// Walk subrows [s_begin, s_end) of one DP group.  dtop: the group's digits of
+// nodes [0, P-1); cw: the group's coefficient vector over the K+1 suffix
+// nodes (P >= 1) or the K suffix nodes (P == 0); (ea, q, lex)_top: folds over
+// nodes [0, P-1).  Each row folds the last prefix node's wall into the 2^K
+// vector of suffix level 0.
 template <int K, int PRIM, int NV>
-__device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, const View& v, uint64_t s_begin,
-                            uint64_t s_end) {
+__device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* coef_base, const View& v,
+                            uint64_t s_begin, uint64_t s_end, const int* dtop, const int64_t* cw, double ea_top,
+                            int32_t q_top, uint64_t lex_top) {
   constexpr int NS = 1 << K;
   Hot H;
   H.smem = smem;
   H.slot_base = slot_base;
+  H.coef_base = coef_base;
   H.h = v.h;
   H.radix = v.radix;
   H.optoff = v.optoff;
@@ -570,46 +589,45 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, const View&
   const uint64_t n0 = static_cast<uint64_t>(v.radix[P]);
   int d[kMaxNodes];
   H.dpre = d;
-  uint64_t row = s_begin / n0;
+  for (int i = 0; i + 1 < P; ++i) d[i] = dtop[i];
   int o0 = static_cast<int>(s_begin % n0);
-  {
-    uint64_t x = row;
-    for (int i = P - 1; i >= 0; --i) {
-      const uint64_t r = static_cast<uint64_t>(v.radix[i]);
-      d[i] = static_cast<int>(x % r);
-      x /= r;
-    }
-  }
-  // The row's coefficient vector is written once per row and read once per
-  // subrow: it lives in this thread's shared-memory column, not in registers.
-  int64_t* c0s = reinterpret_cast<int64_t*>(slot_base + kSlotBytes * kBlock) + threadIdx.x;
+  if (P >= 1) d[P - 1] = static_cast<int>((s_begin / n0) % static_cast<uint64_t>(v.radix[P - 1]));
+  int64_t* c0 = coef_col<K>(coef_base, 0);
   double ea_pre = 0.0;
   int32_t q_pre = INT_MAX;
   uint64_t lex_pre = 0;
-  bool fresh = true;
+  bool fresh_row = true;
   for (uint64_t s = s_begin; s < s_end; ++s) {
-    if (fresh) {
-      int64_t c[NS];
-      row_prefix<K>(v, d, P, ea_pre, q_pre, lex_pre, c);
+    if (fresh_row) {
+      if (P == 0) {
 #pragma unroll
-      for (int S = 0; S < NS; ++S) c0s[S * kBlock] = c[S];
-      fresh = false;
-    }
-    int64_t c0[NS];
+        for (int S = 0; S < NS; ++S) c0[S * kBlock] = cw[S];
+        ea_pre = ea_top;
+        q_pre = q_top;
+        lex_pre = lex_top;
+      } else {
+        const int o = v.optoff[P - 1] + d[P - 1];
+        const int64_t w = v.wall[o];
 #pragma unroll
-    for (int S = 0; S < NS; ++S) c0[S] = c0s[S * kBlock];
-    H.s_index = s;
-    level<K, PRIM, NV, 0>(H, in, c0, ea_pre, q_pre, lex_pre, o0, o0 + 1, 0);
-    if (static_cast<uint64_t>(++o0) == n0) {  // next row: prefix odometer, last prefix node fastest
-      o0 = 0;
-      fresh = true;
-      for (int i = P - 1; i >= 0; --i) {
-        if (++d[i] < v.radix[i]) break;
-        d[i] = 0;
+        for (int S = 0; S < NS; ++S) c0[S * kBlock] = max(cw[2 * S], cw[2 * S + 1] + w);
+        ea_pre = __dadd_rn(ea_top, v.ga[o]);
+        q_pre = min(q_top, v.q[o]);
+        lex_pre = lex_top + v.lexw[o];
       }
+      fresh_row = false;
+    }
+    H.s_index = s;
+    level<K, PRIM, NV, 0>(H, in, ea_pre, q_pre, lex_pre, o0, o0 + 1, 0);
+    if (static_cast<uint64_t>(++o0) == n0) {  // next row of the group
+      o0 = 0;
+      fresh_row = true;
+      if (P >= 1) ++d[P - 1];
     }
   }
 }
+
+// Per-warp DP scratch: f[n][32] and c[32] (int64) per warp.
+__host__ __device__ constexpr size_t dp_bytes_per_warp(int n) { return sizeof(int64_t) * 32 * (n + 1); }
 
 __device__ __forceinline__ Rec shfl_rec(const Rec& r, int delta) {
   Rec o;
@@ -689,13 +707,49 @@ __global__ void __launch_bounds__(kBlock, 2)
     slot_offer(sl, threadIdx.x, h, c);
   }
 
-  // Whole subrows: contiguous share per thread.
-  const uint64_t cnt = jd.sub_hi - jd.sub_lo;
-  if (cnt) {
-    const uint64_t q = cnt / nt, r = cnt % nt;
-    const uint64_t start = jd.sub_lo + gt * q + min(gt, r);
-    const uint64_t len = q + (gt < r ? 1 : 0);
-    if (len) run_subrows<K, PRIM, NV>(smem, slot_base, v, start, start + len);
+  // Whole subrows.  Work is dealt to warps in DP groups (all subrows sharing
+  // the digits above the last prefix node, h->group subrows); the 32 lanes
+  // of a warp split each group into contiguous runs, so the row DP and the
+  // row folds happen in lockstep across the warp instead of divergently.
+  if (jd.sub_hi > jd.sub_lo) {
+    const uint64_t G = h->group;
+    const uint64_t g_first = jd.sub_lo / G, g_end = (jd.sub_hi - 1) / G + 1;
+    const uint64_t n_groups = g_end - g_first;
+    const uint64_t warps = static_cast<uint64_t>(ctas_per_job) * (kBlock / 32);
+    const uint64_t w = static_cast<uint64_t>(part) * (kBlock / 32) + (threadIdx.x >> 5);
+    const uint64_t lane = threadIdx.x & 31;
+    const uint64_t gw_lo = g_first + n_groups * w / warps, gw_hi = g_first + n_groups * (w + 1) / warps;
+    uint8_t* coef_base = slot_base + kSlotBytes * kBlock;
+    uint8_t* dp_base = coef_base + sizeof(int64_t) * 28 * kBlock;
+    int64_t* fw = reinterpret_cast<int64_t*>(dp_base + dp_bytes_per_warp(h->n_nodes) * (threadIdx.x >> 5));
+    int64_t* cw = fw + 32 * h->n_nodes;
+    const int P = h->n_nodes - K;
+    for (uint64_t g = gw_lo; g < gw_hi; ++g) {
+      // digits of nodes [0, P-1) shared by the group, and their folds
+      int dtop[kMaxNodes];
+      uint64_t x = g;
+      for (int i = P - 2; i >= 0; --i) {
+        const uint64_t r = static_cast<uint64_t>(v.radix[i]);
+        dtop[i] = static_cast<int>(x % r);
+        x /= r;
+      }
+      double ea_top = 0.0;
+      int32_t q_top = INT_MAX;
+      uint64_t lex_top = 0;
+      for (int i = 0; i + 1 < P; ++i) {
+        const int o = v.optoff[i] + dtop[i];
+        ea_top = __dadd_rn(ea_top, v.ga[o]);
+        q_top = min(q_top, v.q[o]);
+        lex_top += v.lexw[o];
+      }
+      if (P >= 1) warp_dp<K + 1>(v, dtop, P - 1, fw, cw);
+      else warp_dp<K>(v, dtop, 0, fw, cw);
+      const uint64_t lo = max(g * G, jd.sub_lo), hi = min((g + 1) * G, jd.sub_hi);
+      const uint64_t len = hi - lo;
+      const uint64_t a = lo + len * lane / 32, b = lo + len * (lane + 1) / 32;
+      if (a < b) run_subrows<K, PRIM, NV>(smem, slot_base, coef_base, v, a, b, dtop, cw, ea_top, q_top, lex_top);
+      __syncwarp();
+    }
   }
 
   Rec b = block_best(slot_load(sl, threadIdx.x), h, warp_slot);
@@ -743,8 +797,11 @@ KernelFn pick_kernel(int K, int prim, int nv) {
 }
 
 // Dynamic shared memory of a launch: problem image + per-thread slots.
-size_t smem_bytes(size_t blob) {
-  return ((blob + 127) & ~size_t(127)) + static_cast<size_t>(kSlotBytes) * kBlock + sizeof(int64_t) * 16 * kBlock;
+// (coefficient columns sized for K = 4: 16 + 8 + 4 entries per thread)
+// + per-warp DP scratch
+size_t smem_bytes(size_t blob, int n_nodes) {
+  return ((blob + 127) & ~size_t(127)) + static_cast<size_t>(kSlotBytes) * kBlock + sizeof(int64_t) * 28 * kBlock +
+         dp_bytes_per_warp(n_nodes) * (kBlock / 32);
 }
 
 // ---------------------------------------------------------------------------
@@ -912,6 +969,8 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   hd.total = total;
   hd.r_sub = r_sub;
   hd.n_sub = total / r_sub;
+  // DP group: subrows that share every digit above the last prefix node
+  hd.group = full_only ? 1 : (n - K >= 1 ? static_cast<uint64_t>(p->radix[n - K - 1]) * p->radix[n - K] : hd.n_sub);
 
   b.blob.assign(off, 0);
   uint8_t* base = b.blob.data();
@@ -1195,18 +1254,18 @@ int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objec
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
   KernelFn fn = pick_kernel(b.K, b.prim, b.nv);
-  if (int rc = set_smem(fn, smem_bytes(b.blob.size()))) return rc;
-  const int ctas = ctas_for(c, units, fn, smem_bytes(b.blob.size()));
+  if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes))) return rc;
+  const int ctas = ctas_for(c, units, fn, smem_bytes(b.blob.size(), p->n_nodes));
   if (int rc = ensure(c->d_arena, c->arena_cap, b.blob.size())) return rc;
   if (int rc = ensure(c->d_jobs, c->jobs_cap, 1)) return rc;
   if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(ctas))) return rc;
   if (int rc = ensure_tickets(c, 1)) return rc;
   if (int rc = ensure(c->d_out, c->out_cap, 1)) return rc;
   if (int rc = ensure_host(c, 1)) return rc;
-  if (int rc = set_smem(fn, smem_bytes(b.blob.size()))) return rc;
+  if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  fn<<<ctas, kBlock, smem_bytes(b.blob.size()), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch, c->d_tickets, c->d_out);
+  fn<<<ctas, kBlock, smem_bytes(b.blob.size(), p->n_nodes), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch, c->d_tickets, c->d_out);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
@@ -1254,7 +1313,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
       g = &groups.back();
     }
     g->jobs.push_back(j);
-    g->smem = std::max(g->smem, smem_bytes(built[j].blob.size()));
+    g->smem = std::max(g->smem, smem_bytes(built[j].blob.size(), problems[j].n_nodes));
   }
   // One arena for all images; one launch per group, one CTA per job.
   std::vector<uint64_t> off(n_jobs, 0);
@@ -1347,11 +1406,11 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   dp->host.edge_to = dp->eto.data();
   dp->objective = *o;
   dp->fn = pick_kernel(dp->built.K, dp->built.prim, dp->built.nv);
-  if (set_smem(dp->fn, smem_bytes(dp->built.blob.size())) != LOOM_OK) {
+  if (set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)) != LOOM_OK) {
     delete dp;
     return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: cannot size shared memory");
   }
-  const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size()));
+  const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes));
   dp->ctas = ctas;
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
@@ -1362,7 +1421,7 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
              cudaMemcpy(dp->d_blob, dp->built.blob.data(), dp->built.blob.size(), cudaMemcpyHostToDevice) ==
                  cudaSuccess &&
              cudaMemset(dp->d_ticket, 0, sizeof(unsigned)) == cudaSuccess;
-  if (!okk || set_smem(dp->fn, smem_bytes(dp->built.blob.size())) != LOOM_OK) {
+  if (!okk || set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)) != LOOM_OK) {
     loom_problem_release(dp);
     return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: upload failed");
   }
@@ -1393,9 +1452,9 @@ int loom_search_argmin_async(loom_ctx* c, loom_device_problem* dp, uint64_t begi
   d.blob_off = 0;
   if (d.begin >= d.end) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: empty range");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
-  const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size())));
+  const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)));
   LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  dp->fn<<<ctas, kBlock, smem_bytes(dp->built.blob.size()), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
+  dp->fn<<<ctas, kBlock, smem_bytes(dp->built.blob.size(), dp->host.n_nodes), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
                                                              dp->d_ticket, dp->d_out);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;

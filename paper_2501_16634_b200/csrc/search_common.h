@@ -58,6 +58,7 @@ struct alignas(16) BlobHeader {
   uint64_t total;        // plans in the space
   uint64_t r_sub;        // plans per subrow = product of the last K-1 radices
   uint64_t n_sub;        // subrows in the whole space = total / r_sub
+  uint64_t group;        // subrows per DP group (unit of work dealt to a warp)
 };
 
 // A candidate / winner inside the kernels: the quantized criteria, exact
