@@ -104,6 +104,17 @@ typedef struct loom_winner {
   int32_t found;               /* 0: no feasible plan in the searched range       */
 } loom_winner;
 
+/* One plan's Pareto coordinates (pareto_filter's dominance axes,
+ * optimizer.hpp:155-161).  40 bytes, POD. */
+typedef struct loom_point {
+  uint64_t plan_index;
+  double dollars;
+  double gpu_wh;
+  int64_t latency_us;
+  int32_t quality;
+  int32_t reserved;
+} loom_point;
+
 typedef struct loom_ctx loom_ctx;
 typedef struct loom_device_problem loom_device_problem;
 typedef struct loom_lowered loom_lowered;
@@ -185,6 +196,14 @@ int loom_search_argmin_result(loom_ctx* ctx, loom_device_problem* dp, loom_winne
  * call with capacity 0 to get *count. */
 int loom_search_pareto(loom_ctx* ctx, const loom_problem* problem, uint64_t begin, uint64_t end,
                        uint64_t* out_index, uint64_t capacity, uint64_t* count);
+/* Same, returning the frontier's coordinates (for multi-rank merging).  A
+ * call with capacity < count only reports *count; the result of the last
+ * search is cached in the ctx, so the follow-up call does not search again. */
+int loom_search_pareto_points(loom_ctx* ctx, const loom_problem* problem, uint64_t begin, uint64_t end,
+                              loom_point* out, uint64_t capacity, uint64_t* count);
+/* pareto_filter on an arbitrary point set (optimizer.hpp:153-171):
+ * keep[i] = 1 iff no other point dominates point i.  Runs on the device. */
+int loom_pareto_filter_points(loom_ctx* ctx, const loom_point* points, uint64_t n, uint8_t* keep);
 
 /* ---- the drop-in call on reference-format JSON -------------------------- */
 /* exhaustive_search(dag, library, objective, bounds) -> ConfigEstimate JSON:

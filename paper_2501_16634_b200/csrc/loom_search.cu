@@ -805,6 +805,283 @@ size_t smem_bytes(size_t blob, int n_nodes) {
 }
 
 // ---------------------------------------------------------------------------
+// Pareto frontier (pareto_filter, optimizer.hpp:153-171, over estimate(p) for
+// every plan p in ConfigEnumerator order).  Dominance: a <= b on dollars,
+// gpu_wh (raw doubles) and latency, a.quality >= b.quality, one strict.
+//   phase 1  every plan is evaluated (dollars and energy folds in dag order,
+//            max-plus latency, quality min) and tested against a guard set of
+//            real frontier candidates in shared memory; survivors are
+//            appended with warp-ballot compaction.  A plan dominated by a
+//            guard point is dominated (the guard points are plans).
+//   phase 2  exact pairwise filter over the survivors: any dominator of a
+//            survivor is itself a survivor (transitivity), so this is exact.
+// ---------------------------------------------------------------------------
+constexpr int kGuardMax = 2048;
+
+__device__ __forceinline__ bool dominates(double ad, double ae, int64_t al, int32_t aq, double bd, double be,
+                                          int64_t bl, int32_t bq) {
+  return ad <= bd && ae <= be && al <= bl && aq >= bq && (ad < bd || ae < be || al < bl || aq > bq);
+}
+
+struct GuardView {
+  const double* d;
+  const double* e;
+  const int64_t* l;
+  const int32_t* q;
+  int n;
+};
+
+__device__ __forceinline__ bool guarded(const GuardView& g, double d, double e, int64_t l, int32_t q) {
+  for (int k = 0; k < g.n; ++k)
+    if (dominates(g.d[k], g.e[k], g.l[k], g.q[k], d, e, l, q)) return true;
+  return false;
+}
+
+// One plan's point from its digits (estimate restated; slot A = gpu_wh,
+// slot B = dollars in the Pareto image).
+__device__ ParetoPoint eval_point(const View& v, const int* d, uint64_t index) {
+  const int n = v.h->n_nodes;
+  double e = 0.0, dol = 0.0;
+  int32_t q = INT_MAX;
+  for (int i = 0; i < n; ++i) {
+    const int o = v.optoff[i] + d[i];
+    e = __dadd_rn(e, v.ga[o]);
+    dol = __dadd_rn(dol, v.gb[o]);
+    q = min(q, v.q[o]);
+  }
+  int64_t fin[kMaxNodes];
+  int64_t lat = 0;
+  for (int t = 0; t < n; ++t) {
+    const int x = v.topo[t];
+    int64_t s = 0;
+    for (int k = v.predoff[x]; k < v.predoff[x + 1]; ++k) s = max(s, fin[v.pred[k]]);
+    fin[x] = s + v.wall[v.optoff[x] + d[x]];
+    lat = max(lat, fin[x]);
+  }
+  return ParetoPoint{index, dol, e, lat, q, 0};
+}
+
+__device__ __forceinline__ void decode_digits(const View& v, uint64_t index, int* d) {
+  for (int i = v.h->n_nodes - 1; i >= 0; --i) {
+    const uint64_t r = static_cast<uint64_t>(v.radix[i]);
+    d[i] = static_cast<int>(index % r);
+    index /= r;
+  }
+}
+
+// Warp-aggregated append of the lanes whose `keep` is set.
+__device__ __forceinline__ void append_point(bool keep, const ParetoPoint& pt, ParetoPoint* out, uint64_t cap,
+                                             unsigned long long* count) {
+  const unsigned m = __activemask();
+  const unsigned b = __ballot_sync(m, keep);
+  if (!b) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(count, static_cast<unsigned long long>(__popc(b)));
+  base = __shfl_sync(m, base, leader);
+  if (keep) {
+    const uint64_t pos = base + __popc(b & ((1u << lane) - 1));
+    if (pos < cap) out[pos] = pt;
+  }
+}
+
+__device__ __forceinline__ GuardView load_guard(uint8_t* s, const ParetoPoint* g, int n) {
+  GuardView gv;
+  double* d = reinterpret_cast<double*>(s);
+  double* e = d + kGuardMax;
+  int64_t* l = reinterpret_cast<int64_t*>(e + kGuardMax);
+  int32_t* q = reinterpret_cast<int32_t*>(l + kGuardMax);
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    d[k] = g[k].dollars;
+    e[k] = g[k].gpu_wh;
+    l[k] = g[k].latency_us;
+    q[k] = g[k].quality;
+  }
+  __syncthreads();
+  gv.d = d;
+  gv.e = e;
+  gv.l = l;
+  gv.q = q;
+  gv.n = n;
+  return gv;
+}
+
+constexpr size_t kGuardBytes = static_cast<size_t>(kGuardMax) * (8 + 8 + 8 + 4);
+
+// Phase 1 over [begin, end): rows = all digits but the last two fixed.
+__global__ void __launch_bounds__(kBlock)
+    pareto_eval_kernel(const uint8_t* __restrict__ blob_g, uint32_t blob_bytes, uint64_t begin, uint64_t end,
+                       const ParetoPoint* __restrict__ guard, int n_guard, ParetoPoint* __restrict__ out,
+                       uint64_t cap, unsigned long long* __restrict__ count) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t mbar;
+  load_blob(smem, blob_g, blob_bytes, &mbar);
+  const View v = make_view(smem);
+  const GuardView gv = load_guard(smem + ((blob_bytes + 127) & ~127u), guard, n_guard);
+  const int n = v.h->n_nodes;
+  const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nt = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+
+  uint64_t R = 1, row_lo = 0, row_hi = 0;
+  if (n >= 2) {
+    R = static_cast<uint64_t>(v.radix[n - 2]) * v.radix[n - 1];
+    row_lo = (begin + R - 1) / R;
+    row_hi = end / R;
+  }
+  const bool rows = n >= 2 && row_lo < row_hi;
+  const uint64_t head_end = rows ? row_lo * R : end, tail_begin = rows ? row_hi * R : end;
+
+  // range edges: one plan per thread
+  int d[kMaxNodes];
+  for (uint64_t base = begin; base < head_end; base += nt) {
+    const uint64_t i = base + gt;
+    ParetoPoint pt{};
+    bool keep = false;
+    if (i < head_end) {
+      decode_digits(v, i, d);
+      pt = eval_point(v, d, i);
+      keep = !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
+    }
+    append_point(keep, pt, out, cap, count);
+  }
+  for (uint64_t base = tail_begin; base < end; base += nt) {
+    const uint64_t i = base + gt;
+    ParetoPoint pt{};
+    bool keep = false;
+    if (i < end) {
+      decode_digits(v, i, d);
+      pt = eval_point(v, d, i);
+      keep = !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
+    }
+    append_point(keep, pt, out, cap, count);
+  }
+  if (!rows) return;
+
+  // whole rows, contiguous per thread (the row counts differ by at most one)
+  const uint64_t cnt = row_hi - row_lo, qn = cnt / nt, rn = cnt % nt;
+  const uint64_t my_lo = row_lo + gt * qn + min(gt, rn);
+  const uint64_t my_n = qn + (gt < rn ? 1 : 0);
+  const uint64_t max_n = qn + (rn ? 1 : 0);
+  const int u = n - 2, w = n - 1;
+  const int nu = v.radix[u], nw = v.radix[w];
+  const int offu = v.optoff[u], offw = v.optoff[w];
+  if (my_n) decode_digits(v, my_lo * R, d);
+  int64_t f[kMaxNodes][4];
+  for (uint64_t k = 0; k < max_n; ++k) {  // uniform trip count keeps the warp converged for the ballot
+    const bool live = k < my_n;
+    double e0 = 0.0, d0 = 0.0;
+    int32_t q0 = INT_MAX;
+    int64_t c[4] = {0, kNeg, kNeg, kNeg};
+    if (live) {
+      for (int i = 0; i < u; ++i) {
+        const int o = v.optoff[i] + d[i];
+        e0 = __dadd_rn(e0, v.ga[o]);
+        d0 = __dadd_rn(d0, v.gb[o]);
+        q0 = min(q0, v.q[o]);
+      }
+      // longest paths with u (bit 0) and w (bit 1) symbolic
+      c[1] = c[2] = c[3] = kNeg;
+      c[0] = 0;
+      for (int t = 0; t < n; ++t) {
+        const int x = v.topo[t];
+        const int pb = v.predoff[x], pe = v.predoff[x + 1];
+        for (int S = 0; S < 4; ++S) {
+          int64_t val = kNeg;
+          if (x < u) {
+            int64_t b = S == 0 ? 0 : kNeg;
+            for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S]);
+            val = b + v.wall[v.optoff[x] + d[x]];
+          } else {
+            const int bit = x == u ? 1 : 2;
+            if (S & bit) {
+              const int S2 = S ^ bit;
+              int64_t b = S2 == 0 ? 0 : kNeg;
+              for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S2]);
+              val = b;
+            }
+          }
+          f[x][S] = val;
+          c[S] = max(c[S], val);
+        }
+      }
+    }
+    const uint64_t row_base = (my_lo + k) * R;
+    for (int ou = 0; ou < nu; ++ou) {
+      const int64_t wu = v.wall[offu + ou];
+      const int64_t X = max(c[0], c[1] + wu), Y = max(c[2], c[3] + wu);
+      const double eu = __dadd_rn(e0, v.ga[offu + ou]);
+      const double du = __dadd_rn(d0, v.gb[offu + ou]);
+      const int32_t qu = min(q0, v.q[offu + ou]);
+      for (int ow = 0; ow < nw; ++ow) {
+        ParetoPoint pt;
+        pt.index = row_base + static_cast<uint64_t>(ou) * nw + ow;
+        pt.latency_us = max(X, Y + v.wall[offw + ow]);
+        pt.gpu_wh = __dadd_rn(eu, v.ga[offw + ow]);
+        pt.dollars = __dadd_rn(du, v.gb[offw + ow]);
+        pt.quality = min(qu, v.q[offw + ow]);
+        pt.pad = 0;
+        const bool keep = live && !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
+        append_point(keep, pt, out, cap, count);
+      }
+    }
+    if (live)  // next row: odometer over the prefix digits
+      for (int i = u - 1; i >= 0; --i) {
+        if (++d[i] < v.radix[i]) break;
+        d[i] = 0;
+      }
+  }
+}
+
+// Points of an explicit list of plan indices (the guard sample).
+__global__ void __launch_bounds__(kBlock)
+    pareto_points_kernel(const uint8_t* __restrict__ blob_g, uint32_t blob_bytes, const uint64_t* __restrict__ idx,
+                         uint64_t n, ParetoPoint* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t mbar;
+  load_blob(smem, blob_g, blob_bytes, &mbar);
+  const View v = make_view(smem);
+  int d[kMaxNodes];
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    decode_digits(v, idx[i], d);
+    out[i] = eval_point(v, d, idx[i]);
+  }
+}
+
+// Phase 2: keep[i] = no j != i dominates point i (tiles staged in smem).
+__global__ void __launch_bounds__(kBlock)
+    pareto_filter_kernel(const ParetoPoint* __restrict__ pts, uint64_t n, uint8_t* __restrict__ keep) {
+  constexpr int T = 512;
+  __shared__ double sd[T], se[T];
+  __shared__ int64_t sl[T];
+  __shared__ int32_t sq[T];
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  ParetoPoint me{};
+  if (i < n) me = pts[i];
+  bool dom = i >= n;
+  for (uint64_t t0 = 0; t0 < n; t0 += T) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < T && t0 + k < n; k += blockDim.x) {
+      const ParetoPoint p = pts[t0 + k];
+      sd[k] = p.dollars;
+      se[k] = p.gpu_wh;
+      sl[k] = p.latency_us;
+      sq[k] = p.quality;
+    }
+    __syncthreads();
+    const int lim = static_cast<int>(n - t0 < static_cast<uint64_t>(T) ? n - t0 : static_cast<uint64_t>(T));
+    if (!dom)
+      for (int k = 0; k < lim; ++k)
+        if (dominates(sd[k], se[k], sl[k], sq[k], me.dollars, me.gpu_wh, me.latency_us, me.quality)) {
+          dom = true;
+          break;
+        }
+  }
+  if (i < n) keep[i] = !dom;
+}
+
+// ---------------------------------------------------------------------------
 // host: problem image builder
 // ---------------------------------------------------------------------------
 struct Built {
@@ -1077,6 +1354,10 @@ struct loom_ctx {
   size_t out_cap = 0;
   Rec* h_out = nullptr;  // pinned
   size_t h_out_cap = 0;
+  // last Pareto frontier (size-query-then-fill without a second search)
+  std::vector<loom_point> pareto_cache;
+  uint64_t pareto_key = 0;
+  bool pareto_valid = false;
 };
 
 struct loom_device_problem {
@@ -1474,8 +1755,206 @@ int loom_search_pareto(loom_ctx* c, const loom_problem* p, uint64_t begin, uint6
 
 }  // extern "C"
 
+// ---------------------------------------------------------------------------
+// Pareto host driver
+// ---------------------------------------------------------------------------
+namespace {
+
+static_assert(sizeof(ParetoPoint) == sizeof(loom_point), "ParetoPoint must match loom_point");
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) { return cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T)); }
+};
+
+uint64_t fnv(uint64_t h, const void* data, size_t n) {
+  const uint8_t* b = static_cast<const uint8_t*>(data);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+uint64_t problem_hash(const loom_problem* p, uint64_t begin, uint64_t end) {
+  uint64_t h = 1469598103934665603ull;
+  int n_opts = 0;
+  for (int i = 0; i < p->n_nodes; ++i) n_opts += p->radix[i];
+  h = fnv(h, &p->n_nodes, 4);
+  h = fnv(h, p->radix, 4 * p->n_nodes);
+  h = fnv(h, p->wall_us, 8 * n_opts);
+  h = fnv(h, p->gpu_wh, 8 * n_opts);
+  h = fnv(h, p->dollars, 8 * n_opts);
+  h = fnv(h, p->quality, 4 * n_opts);
+  h = fnv(h, p->edge_from, 4 * p->n_edges);
+  h = fnv(h, p->edge_to, 4 * p->n_edges);
+  h = fnv(h, &begin, 8);
+  return fnv(h, &end, 8);
+}
+
+// Exact frontier of device points [0, n) -> host vector.
+int filter_device(loom_ctx* c, const ParetoPoint* d_pts, uint64_t n, std::vector<ParetoPoint>& out) {
+  out.clear();
+  if (n == 0) return LOOM_OK;
+  DevBuf<uint8_t> keep;
+  LOOM_CUDA(keep.alloc(n));
+  const uint64_t blocks = (n + kBlock - 1) / kBlock;
+  pareto_filter_kernel<<<static_cast<unsigned>(blocks), kBlock, 0, c->stream>>>(d_pts, n, keep.p);
+  LOOM_CUDA(cudaGetLastError());
+  ++c->launches;
+  std::vector<uint8_t> hk(n);
+  std::vector<ParetoPoint> hp(n);
+  LOOM_CUDA(cudaMemcpyAsync(hk.data(), keep.p, n, cudaMemcpyDeviceToHost, c->stream));
+  LOOM_CUDA(cudaMemcpyAsync(hp.data(), d_pts, n * sizeof(ParetoPoint), cudaMemcpyDeviceToHost, c->stream));
+  LOOM_CUDA(cudaStreamSynchronize(c->stream));
+  for (uint64_t i = 0; i < n; ++i)
+    if (hk[i]) out.push_back(hp[i]);
+  return LOOM_OK;
+}
+
+// At most kGuardMax points of a frontier, spread over its index order.
+std::vector<ParetoPoint> guard_of(std::vector<ParetoPoint> f) {
+  std::sort(f.begin(), f.end(), [](const ParetoPoint& a, const ParetoPoint& b) { return a.index < b.index; });
+  if (f.size() <= static_cast<size_t>(kGuardMax)) return f;
+  std::vector<ParetoPoint> g;
+  for (int k = 0; k < kGuardMax; ++k) g.push_back(f[f.size() * k / kGuardMax]);
+  return g;
+}
+
+int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end, std::vector<ParetoPoint>& front) {
+  front.clear();
+  loom_objective o;
+  std::memset(&o, 0, sizeof o);
+  o.n_criteria = 2;
+  o.criteria[0] = LOOM_MIN_ENERGY;  // slot A = gpu_wh
+  o.criteria[1] = LOOM_MIN_COST_DOLLARS;  // slot B = dollars
+  Built b;
+  if (int rc = build_image(p, &o, 1, b)) return rc;
+  end = std::min(end, b.total);
+  if (begin >= end) return LOOM_OK;
+  const uint64_t n = end - begin;
+  const uint32_t bytes = static_cast<uint32_t>(b.blob.size());
+  const size_t smem = ((bytes + 127) & ~size_t(127)) + kGuardBytes;
+  DevBuf<uint8_t> d_blob;
+  LOOM_CUDA(d_blob.alloc(bytes));
+  LOOM_CUDA(cudaMemcpyAsync(d_blob.p, b.blob.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pareto_eval_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pareto_points_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes + 128)));
+
+  // guard: exact frontier of an evenly strided sample of the range
+  std::vector<ParetoPoint> guard;
+  const uint64_t kSample = 1 << 16;
+  if (n > kSample) {
+    std::vector<uint64_t> idx(kSample);
+    for (uint64_t k = 0; k < kSample; ++k)
+      idx[k] = begin + static_cast<uint64_t>((static_cast<unsigned __int128>(n) * k) / kSample);
+    DevBuf<uint64_t> d_idx;
+    DevBuf<ParetoPoint> d_s;
+    LOOM_CUDA(d_idx.alloc(kSample));
+    LOOM_CUDA(d_s.alloc(kSample));
+    LOOM_CUDA(cudaMemcpyAsync(d_idx.p, idx.data(), kSample * 8, cudaMemcpyHostToDevice, c->stream));
+    pareto_points_kernel<<<static_cast<unsigned>(kSample / kBlock), kBlock, bytes + 128, c->stream>>>(
+        d_blob.p, bytes, d_idx.p, kSample, d_s.p);
+    LOOM_CUDA(cudaGetLastError());
+    ++c->launches;
+    std::vector<ParetoPoint> f0;
+    if (int rc = filter_device(c, d_s.p, kSample, f0)) return rc;
+    guard = guard_of(f0);
+  }
+
+  const uint64_t cap = std::min<uint64_t>(uint64_t(1) << 22, n);
+  DevBuf<ParetoPoint> d_cand, d_guard;
+  DevBuf<unsigned long long> d_count;
+  LOOM_CUDA(d_cand.alloc(cap));
+  LOOM_CUDA(d_guard.alloc(kGuardMax));
+  LOOM_CUDA(d_count.alloc(1));
+  int resident = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, reinterpret_cast<const void*>(pareto_eval_kernel), kBlock,
+                                                smem);
+  const uint64_t units = n / 64 + 1;
+  const unsigned grid =
+      static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(c->sms) * std::max(1, resident),
+                                                                     (units + kBlock - 1) / kBlock)));
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    unsigned long long count = 0;
+    LOOM_CUDA(cudaMemsetAsync(d_count.p, 0, sizeof(unsigned long long), c->stream));
+    if (!guard.empty())
+      LOOM_CUDA(cudaMemcpyAsync(d_guard.p, guard.data(), guard.size() * sizeof(ParetoPoint), cudaMemcpyHostToDevice,
+                                c->stream));
+    pareto_eval_kernel<<<grid, kBlock, smem, c->stream>>>(d_blob.p, bytes, begin, end, d_guard.p,
+                                                          static_cast<int>(guard.size()), d_cand.p, cap, d_count.p);
+    LOOM_CUDA(cudaGetLastError());
+    ++c->launches;
+    LOOM_CUDA(cudaMemcpyAsync(&count, d_count.p, sizeof count, cudaMemcpyDeviceToHost, c->stream));
+    LOOM_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<ParetoPoint> f;
+    if (int rc = filter_device(c, d_cand.p, std::min<uint64_t>(count, cap), f)) return rc;
+    if (count <= cap) {
+      std::sort(f.begin(), f.end(), [](const ParetoPoint& a, const ParetoPoint& b) { return a.index < b.index; });
+      front = std::move(f);
+      return LOOM_OK;
+    }
+    // overflow: the frontier of what was collected (real plans) joins the guard
+    f.insert(f.end(), guard.begin(), guard.end());
+    DevBuf<ParetoPoint> d_g2;
+    LOOM_CUDA(d_g2.alloc(f.size()));
+    LOOM_CUDA(cudaMemcpyAsync(d_g2.p, f.data(), f.size() * sizeof(ParetoPoint), cudaMemcpyHostToDevice, c->stream));
+    std::vector<ParetoPoint> g2;
+    if (int rc = filter_device(c, d_g2.p, f.size(), g2)) return rc;
+    guard = guard_of(g2);
+  }
+  return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: pareto candidate buffer overflowed repeatedly");
+}
+
+}  // namespace
+
+extern "C" int loom_search_pareto_points(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
+                                         loom_point* out, uint64_t capacity, uint64_t* count) {
+  if (!c || !p || !count) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  LOOM_CUDA(cudaSetDevice(c->device));
+  uint64_t total = 0;
+  if (int rc = loomi::check_problem(p, &total)) return rc;
+  const uint64_t key = problem_hash(p, begin, end);
+  if (!c->pareto_valid || c->pareto_key != key) {
+    std::vector<ParetoPoint> f;
+    if (int rc = pareto_run(c, p, begin, end, f)) return rc;
+    c->pareto_cache.assign(reinterpret_cast<const loom_point*>(f.data()),
+                           reinterpret_cast<const loom_point*>(f.data()) + f.size());
+    c->pareto_key = key;
+    c->pareto_valid = true;
+  }
+  *count = c->pareto_cache.size();
+  if (out && capacity >= c->pareto_cache.size())
+    std::copy(c->pareto_cache.begin(), c->pareto_cache.end(), out);
+  return LOOM_OK;
+}
+
 extern "C" int loom_search_pareto(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
                                   uint64_t* out_index, uint64_t capacity, uint64_t* count) {
-  (void)c; (void)p; (void)begin; (void)end; (void)out_index; (void)capacity; (void)count;
-  return loomi::fail(LOOM_INVALID, "InvalidConfigError: pareto search not built yet");
+  uint64_t n = 0;
+  if (int rc = loom_search_pareto_points(c, p, begin, end, nullptr, 0, &n)) return rc;
+  *count = n;
+  if (out_index && capacity >= n)
+    for (uint64_t i = 0; i < n; ++i) out_index[i] = c->pareto_cache[i].plan_index;
+  return LOOM_OK;
+}
+
+extern "C" int loom_pareto_filter_points(loom_ctx* c, const loom_point* pts, uint64_t n, uint8_t* keep) {
+  if (!c || (n && (!pts || !keep))) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  if (n == 0) return LOOM_OK;
+  LOOM_CUDA(cudaSetDevice(c->device));
+  DevBuf<ParetoPoint> d;
+  DevBuf<uint8_t> k;
+  LOOM_CUDA(d.alloc(n));
+  LOOM_CUDA(k.alloc(n));
+  LOOM_CUDA(cudaMemcpyAsync(d.p, pts, n * sizeof(loom_point), cudaMemcpyHostToDevice, c->stream));
+  pareto_filter_kernel<<<static_cast<unsigned>((n + kBlock - 1) / kBlock), kBlock, 0, c->stream>>>(d.p, n, k.p);
+  LOOM_CUDA(cudaGetLastError());
+  ++c->launches;
+  LOOM_CUDA(cudaMemcpyAsync(keep, k.p, n, cudaMemcpyDeviceToHost, c->stream));
+  LOOM_CUDA(cudaStreamSynchronize(c->stream));
+  return LOOM_OK;
 }

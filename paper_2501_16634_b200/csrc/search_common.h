@@ -73,6 +73,16 @@ struct Rec {
   int32_t found;
 };
 
+// One plan's Pareto coordinates (40 bytes; same layout as loom_point).
+struct ParetoPoint {
+  uint64_t index;
+  double dollars;
+  double gpu_wh;
+  int64_t latency_us;
+  int32_t quality;
+  int32_t pad;
+};
+
 // Per-job launch descriptor (global memory).
 struct JobDesc {
   uint64_t blob_off;     // byte offset in the blob arena

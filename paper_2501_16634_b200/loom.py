@@ -110,6 +110,17 @@ class Winner(C.Structure):
 assert C.sizeof(Winner) == 64
 
 
+class Point(C.Structure):
+    _fields_ = [("plan_index", C.c_uint64), ("dollars", C.c_double), ("gpu_wh", C.c_double),
+                ("latency_us", C.c_int64), ("quality", C.c_int32), ("reserved", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+assert C.sizeof(Point) == 40
+
+
 _lib = None
 
 
@@ -150,6 +161,9 @@ def lib() -> C.CDLL:
         "loom_search_argmin_result": ([vp, vp, W], C.c_int),
         "loom_search_pareto": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64,
                                 C.POINTER(C.c_uint64)], C.c_int),
+        "loom_search_pareto_points": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(Point), C.c_uint64,
+                                       C.POINTER(C.c_uint64)], C.c_int),
+        "loom_pareto_filter_points": ([vp, C.POINTER(Point), C.c_uint64, C.POINTER(C.c_uint8)], C.c_int),
         "loom_exhaustive_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
                                          C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     }
@@ -360,6 +374,28 @@ def search_pareto(ctx: Context, problem: Problem, begin: int = 0, end: int | Non
     buf = (C.c_uint64 * max(1, cnt.value))()
     _check(lib().loom_search_pareto(ctx.handle, C.byref(problem), begin, end, buf, cnt.value, C.byref(cnt)))
     return [buf[i] for i in range(cnt.value)]
+
+
+def search_pareto_points(ctx: Context, problem: Problem, begin: int = 0, end: int | None = None) -> list[dict]:
+    """Frontier of plans [begin, end) under pareto_filter's dominance, ascending index."""
+    end = (1 << 64) - 1 if end is None else end
+    cnt = C.c_uint64(0)
+    _check(lib().loom_search_pareto_points(ctx.handle, C.byref(problem), begin, end, None, 0, C.byref(cnt)))
+    buf = (Point * max(1, cnt.value))()
+    _check(lib().loom_search_pareto_points(ctx.handle, C.byref(problem), begin, end, buf, cnt.value, C.byref(cnt)))
+    return [buf[i].as_dict() for i in range(cnt.value)]
+
+
+def pareto_filter_points(ctx: Context, points: Sequence[dict]) -> list[bool]:
+    """pareto_filter (optimizer.hpp:153-171) on arbitrary points, on the device."""
+    n = len(points)
+    arr = (Point * max(1, n))()
+    for i, p in enumerate(points):
+        for k in ("plan_index", "dollars", "gpu_wh", "latency_us", "quality"):
+            setattr(arr[i], k, p[k])
+    keep = (C.c_uint8 * max(1, n))()
+    _check(lib().loom_pareto_filter_points(ctx.handle, arr, n, keep))
+    return [bool(keep[i]) for i in range(n)]
 
 
 # ---- the drop-in call ----------------------------------------------------
