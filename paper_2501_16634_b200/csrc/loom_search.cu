@@ -37,7 +37,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -837,6 +839,18 @@ __device__ __forceinline__ bool guarded(const GuardView& g, double d, double e, 
   return false;
 }
 
+// Same, trying the previous plan's dominator first (consecutive plans of a
+// thread differ in one digit, so the same guard point usually dominates).
+__device__ __forceinline__ bool guarded_hint(const GuardView& g, int& hint, double d, double e, int64_t l, int32_t q) {
+  if (hint < g.n && dominates(g.d[hint], g.e[hint], g.l[hint], g.q[hint], d, e, l, q)) return true;
+  for (int k = 0; k < g.n; ++k)
+    if (dominates(g.d[k], g.e[k], g.l[k], g.q[k], d, e, l, q)) {
+      hint = k;
+      return true;
+    }
+  return false;
+}
+
 // One plan's point from its digits (estimate restated; slot A = gpu_wh,
 // slot B = dollars in the Pareto image).
 __device__ ParetoPoint eval_point(const View& v, const int* d, uint64_t index) {
@@ -968,6 +982,7 @@ __global__ void __launch_bounds__(kBlock)
   const int offu = v.optoff[u], offw = v.optoff[w];
   if (my_n) decode_digits(v, my_lo * R, d);
   int64_t f[kMaxNodes][4];
+  int hint = 0;
   for (uint64_t k = 0; k < max_n; ++k) {  // uniform trip count keeps the warp converged for the ballot
     const bool live = k < my_n;
     double e0 = 0.0, d0 = 0.0;
@@ -1021,7 +1036,7 @@ __global__ void __launch_bounds__(kBlock)
         pt.dollars = __dadd_rn(du, v.gb[offw + ow]);
         pt.quality = min(qu, v.q[offw + ow]);
         pt.pad = 0;
-        const bool keep = live && !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
+        const bool keep = live && !guarded_hint(gv, hint, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
         append_point(keep, pt, out, cap, count);
       }
     }
@@ -1046,6 +1061,26 @@ __global__ void __launch_bounds__(kBlock)
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     decode_digits(v, idx[i], d);
     out[i] = eval_point(v, d, idx[i]);
+  }
+}
+
+// Candidate refinement: keep the candidates no guard point dominates
+// (guard points are real plans, so this never drops a frontier point).
+__global__ void __launch_bounds__(kBlock)
+    pareto_prefilter_kernel(const ParetoPoint* __restrict__ in, uint64_t n, const ParetoPoint* __restrict__ guard,
+                            int n_guard, ParetoPoint* __restrict__ out, unsigned long long* __restrict__ count) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const GuardView gv = load_guard(smem, guard, n_guard);
+  const uint64_t nt = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t base = 0; base < n; base += nt) {
+    const uint64_t i = base + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    ParetoPoint pt{};
+    bool keep = false;
+    if (i < n) {
+      pt = in[i];
+      keep = !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
+    }
+    append_point(keep, pt, out, n, count);
   }
 }
 
@@ -1822,6 +1857,58 @@ std::vector<ParetoPoint> guard_of(std::vector<ParetoPoint> f) {
   return g;
 }
 
+// Exact frontier of device candidates [0, n): while the set is large, the
+// frontier of a strided 64K subsample (plus the current guard) becomes the
+// guard, and the candidates it dominates are dropped; the rest goes through
+// the exact pairwise filter.
+int refine_and_filter(loom_ctx* c, ParetoPoint* d_in, uint64_t n, std::vector<ParetoPoint> guard,
+                      std::vector<ParetoPoint>& front) {
+  const uint64_t kSub = 1 << 16;
+  DevBuf<ParetoPoint> d_a, d_sub, d_g;
+  DevBuf<unsigned long long> d_cnt;
+  LOOM_CUDA(d_a.alloc(n));
+  LOOM_CUDA(d_sub.alloc(kSub));
+  LOOM_CUDA(d_g.alloc(kGuardMax));
+  LOOM_CUDA(d_cnt.alloc(1));
+  ParetoPoint* cur = d_in;
+  ParetoPoint* nxt = d_a.p;
+  const size_t gsmem = kGuardBytes;
+  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pareto_prefilter_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
+  for (int round = 0; round < 8 && n > kSub; ++round) {
+    const uint64_t stride = n / kSub;
+    LOOM_CUDA(cudaMemcpy2DAsync(d_sub.p, sizeof(ParetoPoint), cur, sizeof(ParetoPoint) * stride, sizeof(ParetoPoint),
+                                kSub, cudaMemcpyDeviceToDevice, c->stream));
+    std::vector<ParetoPoint> g;
+    if (int rc = filter_device(c, d_sub.p, kSub, g)) return rc;
+    g.insert(g.end(), guard.begin(), guard.end());
+    LOOM_CUDA(cudaMemcpyAsync(d_sub.p, g.data(), std::min<size_t>(g.size(), kSub) * sizeof(ParetoPoint),
+                              cudaMemcpyHostToDevice, c->stream));
+    std::vector<ParetoPoint> g2;
+    if (int rc = filter_device(c, d_sub.p, std::min<size_t>(g.size(), kSub), g2)) return rc;
+    guard = guard_of(g2);
+    LOOM_CUDA(cudaMemcpyAsync(d_g.p, guard.data(), guard.size() * sizeof(ParetoPoint), cudaMemcpyHostToDevice,
+                              c->stream));
+    LOOM_CUDA(cudaMemsetAsync(d_cnt.p, 0, sizeof(unsigned long long), c->stream));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + kBlock - 1) / kBlock, uint64_t(c->sms) * 8));
+    pareto_prefilter_kernel<<<grid, kBlock, gsmem, c->stream>>>(cur, n, d_g.p, static_cast<int>(guard.size()), nxt,
+                                                                d_cnt.p);
+    LOOM_CUDA(cudaGetLastError());
+    ++c->launches;
+    unsigned long long m = 0;
+    LOOM_CUDA(cudaMemcpyAsync(&m, d_cnt.p, sizeof m, cudaMemcpyDeviceToHost, c->stream));
+    LOOM_CUDA(cudaStreamSynchronize(c->stream));
+    if (std::getenv("LOOM_DEBUG"))
+      std::fprintf(stderr, "[loom pareto] refine %d: %llu -> %llu (guard %zu)\n", round,
+                   static_cast<unsigned long long>(n), m, guard.size());
+    const bool progress = m < n - n / 8;
+    n = m;
+    std::swap(cur, nxt);
+    if (!progress) break;
+  }
+  return filter_device(c, cur, n, front);
+}
+
 int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end, std::vector<ParetoPoint>& front) {
   front.clear();
   loom_objective o;
@@ -1879,6 +1966,7 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
       static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(c->sms) * std::max(1, resident),
                                                                      (units + kBlock - 1) / kBlock)));
   for (int attempt = 0; attempt < 6; ++attempt) {
+    const auto t0 = std::chrono::steady_clock::now();
     unsigned long long count = 0;
     LOOM_CUDA(cudaMemsetAsync(d_count.p, 0, sizeof(unsigned long long), c->stream));
     if (!guard.empty())
@@ -1890,13 +1978,20 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
     ++c->launches;
     LOOM_CUDA(cudaMemcpyAsync(&count, d_count.p, sizeof count, cudaMemcpyDeviceToHost, c->stream));
     LOOM_CUDA(cudaStreamSynchronize(c->stream));
-    std::vector<ParetoPoint> f;
-    if (int rc = filter_device(c, d_cand.p, std::min<uint64_t>(count, cap), f)) return rc;
+    const auto t_eval = std::chrono::steady_clock::now();
     if (count <= cap) {
+      std::vector<ParetoPoint> f;
+      if (int rc = refine_and_filter(c, d_cand.p, count, guard, f)) return rc;
+      if (std::getenv("LOOM_DEBUG"))
+        std::fprintf(stderr, "[loom pareto] guard=%zu candidates=%llu frontier=%zu eval=%.3fs refine+filter=%.3fs\n",
+                     guard.size(), count, f.size(), std::chrono::duration<double>(t_eval - t0).count(),
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t_eval).count());
       std::sort(f.begin(), f.end(), [](const ParetoPoint& a, const ParetoPoint& b) { return a.index < b.index; });
       front = std::move(f);
       return LOOM_OK;
     }
+    std::vector<ParetoPoint> f;
+    if (int rc = filter_device(c, d_cand.p, cap, f)) return rc;
     // overflow: the frontier of what was collected (real plans) joins the guard
     f.insert(f.end(), guard.begin(), guard.end());
     DevBuf<ParetoPoint> d_g2;
