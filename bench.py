@@ -302,14 +302,16 @@ def b200_arm(args) -> None:
         dist.destroy_process_group()
 
 
-# Compiled inner loop of search_kernel<4, kPrimFp>: 45 SASS instructions per
-# 8 plans (8 LDS.128-half loads, 8 DADD, 8 DSETP, 8 ISETP, mask assembly and
-# one branch) -> see profiles/ and DESIGN.md §5.
-ISSUE_INSTR_PER_PLAN = 45 / 8
+# Compiled fast path of the innermost context of search_kernel<4, kPrimFp, 16>
+# (tools/sass_hot.py 4 0 16): 68 SASS instructions per 16 plans -- 17 DADD,
+# 16 DSETP, 17 ISETP, 8 PLOP3, loads/loop control.  DESIGN.md §5.
+ISSUE_INSTR_PER_PLAN = 68 / 16
 
 
 def other_configs(ctx, loom, W) -> dict:
-    """Time-to-plan for the other BASELINE configs (outside the timed region)."""
+    """Time-to-plan for the other BASELINE configs (outside the timed region):
+    C1/C2 through the JSON drop-in call; C4 = batched lowering + one batched
+    search of 10,000 jobs; C5 = the full Pareto frontier."""
     out = {}
     for name, w in (("c1", W.config1()), ("c2", W.config2())):
         dag_t, lib_t, obj_t, bounds_t = w.texts()
@@ -319,19 +321,31 @@ def other_configs(ctx, loom, W) -> dict:
             t0 = time.perf_counter()
             r = loom.exhaustive_search(dag_t, lib_t, obj_t, bounds_t, ctx=ctx)
             ts.append(time.perf_counter() - t0)
-        out[name] = {"time_to_plan_ms": 1e3 * min(ts), "plans": r["plans"], "identifier": r["identifier"]}
+        out[name] = {"time_to_plan_ms": 1e3 * min(ts), "plans": r["plans"], "identifier": r["identifier"],
+                     "latency_us": r["latency_us"], "gpu_wh": r["gpu_wh"]}
     jobs = W.config4(10_000)
-    t0 = time.perf_counter()
-    lws = [loom.Lowered(j.dag, j.library, j.bounds) for j in jobs]
-    t_lower = time.perf_counter() - t0
+    dags = [json.dumps(j.dag) for j in jobs]
+    lib_t, bounds_t = json.dumps(jobs[0].library), json.dumps(jobs[0].bounds)
     objs = [loom.objective(j.objective) for j in jobs]
-    loom.search_argmin_batch(ctx, [lw.problem for lw in lws[:64]], objs[:64])
+    lws = loom.lower_batch(dags[:64], lib_t, bounds_t)
+    loom.search_argmin_batch(ctx, [lw.problem for lw in lws], objs[:64])
     t0 = time.perf_counter()
+    lws = loom.lower_batch(dags, lib_t, bounds_t)
+    t1 = time.perf_counter()
     res = loom.search_argmin_batch(ctx, [lw.problem for lw in lws], objs)
-    t_search = time.perf_counter() - t0
+    t2 = time.perf_counter()
     plans = sum(lw.total for lw in lws)
-    out["c4"] = {"jobs": len(jobs), "plans": plans, "search_ms": 1e3 * t_search, "lowering_ms": 1e3 * t_lower,
-                 "plans_per_s": plans / t_search, "feasible_jobs": sum(1 for s, _ in res if s == 0)}
+    out["c4"] = {"jobs": len(jobs), "plans": plans, "lowering_ms": 1e3 * (t1 - t0), "search_ms": 1e3 * (t2 - t1),
+                 "time_to_plan_ms": 1e3 * (t2 - t0), "search_plans_per_s": plans / (t2 - t1),
+                 "feasible_jobs": sum(1 for s, _ in res if s == 0)}
+    w5 = W.config5()
+    lw5 = loom.Lowered(w5.dag, w5.library, w5.bounds)
+    loom.search_pareto_points(ctx, lw5.problem, 0, lw5.total - 1)
+    t0 = time.perf_counter()
+    front = loom.search_pareto_points(ctx, lw5.problem, 0, lw5.total)
+    t5 = time.perf_counter() - t0
+    out["c5"] = {"plans": lw5.total, "frontier_points": len(front), "time_to_frontier_ms": 1e3 * t5,
+                 "plans_per_s": lw5.total / t5}
     return out
 
 

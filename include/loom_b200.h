@@ -143,6 +143,11 @@ int loom_objective_parse(const char* objective_json, loom_objective* out);
  * {"max_fanout":4,"max_paths":2,"sku_pool_cap":{..},"sku_total_cap":{..}}. */
 int loom_lower(const char* dag_json, const char* library_json, const char* bounds_json,
                loom_lowered** out);
+/* Many DAGs against one library bundle and bounds (config 4: the library is
+ * parsed once and the DAGs are lowered on `threads` host threads; 0 = all).
+ * out[i] receives a handle or NULL; status[i] the per-DAG status. */
+int loom_lower_batch(const char* library_json, const char* bounds_json, const char* const* dag_jsons,
+                     int32_t n, int32_t threads, loom_lowered** out, int32_t* status);
 const loom_problem* loom_lowered_problem(const loom_lowered* lowered);
 /* ConfigPoint JSON (config.hpp:88-95) + "identifier" for a plan index. */
 int loom_lowered_config_json(const loom_lowered* lowered, uint64_t plan_index, char* buf,

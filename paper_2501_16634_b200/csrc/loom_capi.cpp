@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -350,6 +351,45 @@ int loom_lower(const char* dag_json, const char* library_json, const char* bound
     return loomi::fail(status_of(e), e.what());
   } catch (const std::exception& e) {
     return loomi::fail(LOOM_INVALID, std::string("InvalidConfigError: ") + e.what());
+  }
+}
+
+int loom_lower_batch(const char* library_json, const char* bounds_json, const char* const* dag_jsons, int32_t n,
+                     int32_t threads, loom_lowered** out, int32_t* status) {
+  if (!library_json || !bounds_json || (n > 0 && (!dag_jsons || !out || !status)) || n < 0)
+    return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  try {
+    const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json);
+    const loom::SearchBounds bounds = loom::SearchBounds::from_json_text(bounds_json);
+    int t = threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    t = std::max(1, std::min(t, n));
+    std::vector<std::string> errors(n);
+    std::vector<std::thread> pool;
+    for (int w = 0; w < t; ++w)
+      pool.emplace_back([&, w] {
+        for (int i = w; i < n; i += t) {
+          out[i] = nullptr;
+          try {
+            auto lw = std::make_unique<loom_lowered>();
+            lw->L = loom::lower(loom::WorkflowDag::from_json_text(dag_jsons[i] ? dag_jsons[i] : ""), lib, bounds);
+            lw->view = lw->L.view();
+            out[i] = lw.release();
+            status[i] = LOOM_OK;
+          } catch (const loom::Error& e) {
+            status[i] = status_of(e);
+            errors[i] = e.what();
+          } catch (const std::exception& e) {
+            status[i] = LOOM_INVALID;
+            errors[i] = std::string("InvalidConfigError: ") + e.what();
+          }
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (int i = 0; i < n; ++i)
+      if (status[i] != LOOM_OK) loomi::set_error(errors[i]);
+    return LOOM_OK;
+  } catch (const loom::Error& e) {
+    return loomi::fail(status_of(e), e.what());
   }
 }
 

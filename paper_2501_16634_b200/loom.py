@@ -144,6 +144,8 @@ def lib() -> C.CDLL:
         "loom_objective_parse": ([C.c_char_p, O], C.c_int),
         "loom_lower": ([C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(vp)], C.c_int),
         "loom_lowered_problem": ([vp], P),
+        "loom_lower_batch": ([C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p), C.c_int32, C.c_int32, C.POINTER(vp),
+                              C.POINTER(C.c_int32)], C.c_int),
         "loom_lowered_config_json": ([vp, C.c_uint64, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
         "loom_lowered_option_json": ([vp, C.c_int32, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
                                      C.c_int),
@@ -208,9 +210,12 @@ def objective(obj: dict | str) -> Objective:
 class Lowered:
     """Reference-format JSON lowered to the flat plan space (host-side C++)."""
 
-    def __init__(self, dag: Any, library: Any, bounds: Any):
-        h = C.c_void_p()
-        _check(lib().loom_lower(_text(dag), _text(library), _text(bounds), C.byref(h)))
+    def __init__(self, dag: Any, library: Any, bounds: Any, _handle: C.c_void_p | None = None):
+        if _handle is None:
+            h = C.c_void_p()
+            _check(lib().loom_lower(_text(dag), _text(library), _text(bounds), C.byref(h)))
+        else:
+            h = _handle
         self._h = h
         self.problem: Problem = lib().loom_lowered_problem(h).contents
 
@@ -261,6 +266,22 @@ class Lowered:
         w = Winner()
         _check(lib().loom_evaluate_plan(C.byref(self.problem), plan_index, C.byref(w)))
         return w.as_dict()
+
+
+def lower_batch(dags: Sequence[Any], library: Any, bounds: Any, threads: int = 0) -> list[Lowered]:
+    """Lower many DAGs against one library bundle (parsed once, multi-threaded)."""
+    n = len(dags)
+    texts = [_text(d) for d in dags]
+    arr = (C.c_char_p * max(1, n))(*texts)
+    out = (C.c_void_p * max(1, n))()
+    st = (C.c_int32 * max(1, n))()
+    _check(lib().loom_lower_batch(_text(library), _text(bounds), arr, n, threads, out, st))
+    res = []
+    for i in range(n):
+        if st[i] != LOOM_OK:
+            _raise(st[i], f"job {i}: " + last_error())
+        res.append(Lowered(None, None, None, _handle=C.c_void_p(out[i])))
+    return res
 
 
 # ---- device context --------------------------------------------------------
