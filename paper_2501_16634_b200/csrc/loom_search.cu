@@ -342,6 +342,7 @@ struct Hot {
   const uint8_t* smem;
   uint8_t* slot_base;
   uint8_t* coef_base;
+  const int64_t* c0;  // level-0 coefficient vector (thread-local)
   const BlobHeader* h;
   const int32_t* radix;
   const int32_t* optoff;
@@ -399,13 +400,17 @@ __device__ __forceinline__ int32_t inner_tw(const PreInner& r, int32_t wu) {
 // Innermost node over one (prefix, o0 .. o_{K-2}) context.  NV > 0: the
 // node's table is in registers (radix <= NV, padded with never-passing
 // entries); NV == 0: read from shared memory in groups of 8.
-template <int K, int PRIM, int NV>
+template <int K, int PRIM, int NV, bool PT>
 struct Inner {
-  double g[NV > 0 ? NV : 1];
-  int32_t w[NV > 0 ? NV : 1];
+  double g[NV > 0 && !PT ? NV : 1];
+  int32_t w[NV > 0 && !PT ? NV : 1];
+
+  // table entry j: kernel parameter (PT) or register copy
+  __device__ __forceinline__ double G(const InnerParams& ip, int j) const { return PT ? ip.g[j] : g[PT ? 0 : j]; }
+  __device__ __forceinline__ int32_t W(const InnerParams& ip, int j) const { return PT ? ip.w[j] : w[PT ? 0 : j]; }
 
   __device__ __forceinline__ void load(const Hot& H) {
-    if constexpr (NV > 0) {
+    if constexpr (NV > 0 && !PT) {
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
         g[j] = H.inner[j].g;
@@ -422,10 +427,11 @@ struct Inner {
   }
 
   // NV > 0: does any plan of the context pass?  (one predicate OR per plan)
-  __device__ __forceinline__ bool any_pass(const Hot& H, int32_t tw, double ea, int32_t qv) const {
+  __device__ __forceinline__ bool any_pass(const Hot& H, const InnerParams& ip, int32_t tw, double ea,
+                                           int32_t qv) const {
     bool any = false;
 #pragma unroll
-    for (int j = 0; j < (NV > 0 ? NV : 1); ++j) any |= pass(H, w[j], g[j], 0, tw, ea, qv);
+    for (int j = 0; j < (NV > 0 ? NV : 1); ++j) any |= pass(H, W(ip, j), G(ip, j), 0, tw, ea, qv);
     return any;
   }
 
@@ -437,65 +443,94 @@ struct Inner {
 // level J (2^(K-J) int64 entries) sits at column offset sum_{j<J} 2^(K-j),
 // entry S at [S * kBlock + tid] (conflict free).  Keeping them out of the
 // register file leaves the registers to the innermost table and thresholds.
+// Per-thread coefficient columns in shared memory for suffix levels
+// J = 1 .. K-2: the input vector of level J (2^(K-J) int64 entries) sits at
+// column offset sum_{1<=j<J} 2^(K-j), entry S at [S * kBlock + tid] (conflict
+// free).  Level 0's vector (read once per subrow) lives in local memory.
 template <int K>
 __device__ __forceinline__ int64_t* coef_col(uint8_t* coef_base, int J) {
   int off = 0;
-  for (int j = 0; j < J; ++j) off += 1 << (K - j);
+  for (int j = 1; j < J; ++j) off += 1 << (K - j);
   return reinterpret_cast<int64_t*>(coef_base) + off * kBlock + threadIdx.x;
 }
 
-template <int K>
-constexpr int coef_entries() {
-  int e = 0;
-  for (int j = 0; j <= K - 2; ++j) e += 1 << (K - j);
-  return e;
-}
+constexpr int kCoefEntries = 8 + 4;  // K = 4: levels 1 and 2
 
-template <int K, int PRIM, int NV, int J>
-__device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV>& in, double ea, int32_t qv, uint64_t lex,
+template <int K, int PRIM, int NV, bool PT, int J>
+__device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, const InnerParams& ip, double ea,
+                                      int32_t qv, uint64_t lex,
                                       int o_lo, int o_hi, uint64_t ibase) {
   const int node = H.P + J;
   const int off = H.optoff[node];
   const int n = H.radix[node];
-  const int64_t* cin = coef_col<K>(H.coef_base, J);
+  // level 0 reads the thread's local vector (stride 1), deeper levels their
+  // shared-memory column (stride kBlock)
+  constexpr int SI = J == 0 ? 1 : kBlock;
+  const int64_t* cin = J == 0 ? H.c0 : coef_col<K>(H.coef_base, J);
   if constexpr (J == K - 2) {
     const int n_in = H.radix[node + 1];
     const int64_t wmin = H.h->inner_wmin, wu_max = H.h->pre_wmax;
-    const int64_t c[4] = {cin[0], cin[kBlock], cin[2 * kBlock], cin[3 * kBlock]};
+    const int64_t c[4] = {cin[0], cin[SI], cin[2 * SI], cin[3 * SI]};
     PreInner pr = pre_inner(c, H.lat_s, wmin, wu_max);
-    for (int o = o_lo; o < o_hi; ++o) {
-      const int32_t wu = H.w32[off + o];
-      const double eu = __dadd_rn(ea, H.ga[off + o]);
-      const int32_t qu = (PRIM == kPrimQual) ? min(qv, H.q[off + o]) : INT_MAX;
+    // Exact slow path of one context (rare).
+    auto context_slow = [&](int o, double eu, int32_t qu, int32_t tw, int g0) {
       H.od[J] = o;
       // plan index of option 0 of the innermost node in this context; at J == 0
       // the digit o is already part of the subrow index
       const uint64_t inner_base =
           J == 0 ? 0 : (ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o)) * static_cast<uint64_t>(n_in);
-      int32_t tw = inner_tw(pr, wu);
-      const int g_end = NV > 0 ? NV : ((n_in + 7) & ~7);
-      for (int g0 = 0; g0 < g_end; g0 += (NV > 0 ? NV : 8)) {
-        bool any;
-        if constexpr (NV > 0) {
-          any = in.any_pass(H, tw, eu, qu);
-        } else {
-          any = false;
+      const int64_t w_real = H.wall[off + o];
+      const int64_t X = max(cin[0], cin[SI] + w_real), Y = max(cin[2 * SI], cin[3 * SI] + w_real);
+      const uint64_t lex_u = lex + H.lexw[off + o];
+      slow_scan<K, PRIM>(H.smem, H.slot_base, H.dpre, H.P, H.od[0], H.od[1], H.od[2], g0, g0 + (NV > 0 ? NV : 8), tw,
+                         eu, qu, lex_u, X, Y, H.s_index * H.h->r_sub + inner_base);
+      reload(H);
+      if (PRIM == kPrimLat) {
+        const int64_t cc[4] = {cin[0], cin[SI], cin[2 * SI], cin[3 * SI]};
+        pr = pre_inner(cc, H.lat_s, wmin, wu_max);
+      }
+    };
+    if constexpr (NV > 0) {
+      // Two contexts per step share the register-resident innermost table:
+      // twice the independent DADD -> DSETP chains per warp.
+      int o = o_lo;
+      for (; o + 1 < o_hi; o += 2) {
+        const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
+        const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
+        const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
+        bool a0 = false, a1 = false;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          a0 |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw0, eu0, INT_MAX);
+          a1 |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw1, eu1, INT_MAX);
+        }
+        if (__builtin_expect(a0 | a1, 0)) {
+          if (a0) context_slow(o, eu0, INT_MAX, tw0, 0);
+          if (a1) context_slow(o + 1, eu1, INT_MAX, inner_tw(pr, wu1), 0);
+        }
+      }
+      if (o < o_hi) {
+        const int32_t wu = H.w32[off + o];
+        const double eu = __dadd_rn(ea, H.ga[off + o]);
+        const int32_t tw = inner_tw(pr, wu);
+        if (__builtin_expect(in.any_pass(H, ip, tw, eu, INT_MAX), 0)) context_slow(o, eu, INT_MAX, tw, 0);
+      }
+    } else {
+      for (int o = o_lo; o < o_hi; ++o) {
+        const int32_t wu = H.w32[off + o];
+        const double eu = __dadd_rn(ea, H.ga[off + o]);
+        const int32_t qu = (PRIM == kPrimQual) ? min(qv, H.q[off + o]) : INT_MAX;
+        int32_t tw = inner_tw(pr, wu);
+        const int g_end = (n_in + 7) & ~7;
+        for (int g0 = 0; g0 < g_end; g0 += 8) {
+          bool any = false;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const InnerEntry e = H.inner[g0 + j];
             any |= in.pass(H, e.w, e.g, e.q, tw, eu, qu);
           }
-        }
-        if (__builtin_expect(any, 0)) {
-          const int64_t w_real = H.wall[off + o];
-          const int64_t X = max(cin[0], cin[kBlock] + w_real), Y = max(cin[2 * kBlock], cin[3 * kBlock] + w_real);
-          const uint64_t lex_u = lex + H.lexw[off + o];
-          slow_scan<K, PRIM>(H.smem, H.slot_base, H.dpre, H.P, H.od[0], H.od[1], H.od[2], g0,
-                             g0 + (NV > 0 ? NV : 8), tw, eu, qu, lex_u, X, Y, H.s_index * H.h->r_sub + inner_base);
-          reload(H);
-          if (PRIM == kPrimLat) {
-            const int64_t cc[4] = {cin[0], cin[kBlock], cin[2 * kBlock], cin[3 * kBlock]};
-            pr = pre_inner(cc, H.lat_s, wmin, wu_max);
+          if (__builtin_expect(any, 0)) {
+            context_slow(o, eu, qu, tw, g0);
             tw = inner_tw(pr, wu);
           }
         }
@@ -507,13 +542,13 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV>& in, doub
     for (int o = o_lo; o < o_hi; ++o) {
       const int64_t w = H.wall[off + o];
 #pragma unroll
-      for (int S = 0; S < NS; ++S) cout[S * kBlock] = max(cin[2 * S * kBlock], cin[(2 * S + 1) * kBlock] + w);
+      for (int S = 0; S < NS; ++S) cout[S * kBlock] = max(cin[2 * S * SI], cin[(2 * S + 1) * SI] + w);
       H.od[J] = o;
       const double e2 = __dadd_rn(ea, H.ga[off + o]);
       const int32_t q2 = (PRIM == kPrimQual) ? min(qv, H.q[off + o]) : INT_MAX;
       const uint64_t l2 = lex + H.lexw[off + o];
       const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o);
-      level<K, PRIM, NV, J + 1>(H, in, e2, q2, l2, 0, H.radix[node + 1], ib);
+      level<K, PRIM, NV, PT, J + 1>(H, in, ip, e2, q2, l2, 0, H.radix[node + 1], ib);
     }
   }
 }
@@ -563,10 +598,10 @@ __device__ void warp_dp(const View& v, const int* dtop, int Pd, int64_t* fw, int
 // nodes (P >= 1) or the K suffix nodes (P == 0); (ea, q, lex)_top: folds over
 // nodes [0, P-1).  Each row folds the last prefix node's wall into the 2^K
 // vector of suffix level 0.
-template <int K, int PRIM, int NV>
+template <int K, int PRIM, int NV, bool PT>
 __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* coef_base, const View& v,
-                            uint64_t s_begin, uint64_t s_end, const int* dtop, const int64_t* cw, double ea_top,
-                            int32_t q_top, uint64_t lex_top) {
+                            const InnerParams& ip, uint64_t s_begin, uint64_t s_end, const int* dtop, const int64_t* cw,
+                            double ea_top, int32_t q_top, uint64_t lex_top) {
   constexpr int NS = 1 << K;
   Hot H;
   H.smem = smem;
@@ -584,7 +619,7 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
   H.P = v.h->n_nodes - K;
   H.od[0] = H.od[1] = H.od[2] = H.od[3] = 0;
   reload(H);
-  Inner<K, PRIM, NV> in;
+  Inner<K, PRIM, NV, PT> in;
   in.load(H);
 
   const int P = H.P;
@@ -594,7 +629,8 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
   for (int i = 0; i + 1 < P; ++i) d[i] = dtop[i];
   int o0 = static_cast<int>(s_begin % n0);
   if (P >= 1) d[P - 1] = static_cast<int>((s_begin / n0) % static_cast<uint64_t>(v.radix[P - 1]));
-  int64_t* c0 = coef_col<K>(coef_base, 0);
+  int64_t c0[NS];  // written once per row, read once per subrow
+  H.c0 = c0;
   double ea_pre = 0.0;
   int32_t q_pre = INT_MAX;
   uint64_t lex_pre = 0;
@@ -602,16 +638,16 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
   for (uint64_t s = s_begin; s < s_end; ++s) {
     if (fresh_row) {
       if (P == 0) {
-#pragma unroll
-        for (int S = 0; S < NS; ++S) c0[S * kBlock] = cw[S];
+#pragma unroll 1
+        for (int S = 0; S < NS; ++S) c0[S] = cw[S];
         ea_pre = ea_top;
         q_pre = q_top;
         lex_pre = lex_top;
       } else {
         const int o = v.optoff[P - 1] + d[P - 1];
         const int64_t w = v.wall[o];
-#pragma unroll
-        for (int S = 0; S < NS; ++S) c0[S * kBlock] = max(cw[2 * S], cw[2 * S + 1] + w);
+#pragma unroll 1
+        for (int S = 0; S < NS; ++S) c0[S] = max(cw[2 * S], cw[2 * S + 1] + w);
         ea_pre = __dadd_rn(ea_top, v.ga[o]);
         q_pre = min(q_top, v.q[o]);
         lex_pre = lex_top + v.lexw[o];
@@ -619,7 +655,7 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
       fresh_row = false;
     }
     H.s_index = s;
-    level<K, PRIM, NV, 0>(H, in, ea_pre, q_pre, lex_pre, o0, o0 + 1, 0);
+    level<K, PRIM, NV, PT, 0>(H, in, ip, ea_pre, q_pre, lex_pre, o0, o0 + 1, 0);
     if (static_cast<uint64_t>(++o0) == n0) {  // next row of the group
       o0 = 0;
       fresh_row = true;
@@ -675,10 +711,11 @@ __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
   return r;
 }
 
-template <int K, int PRIM, int NV>
-__global__ void __launch_bounds__(kBlock, 2)
+template <int K, int PRIM, int NV, bool PT>
+__global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
     search_kernel(const uint8_t* __restrict__ arena, const JobDesc* __restrict__ jobs, int ctas_per_job,
-                  Rec* __restrict__ scratch, unsigned* __restrict__ tickets, Rec* __restrict__ out) {
+                  Rec* __restrict__ scratch, unsigned* __restrict__ tickets, Rec* __restrict__ out,
+                  const InnerParams ip) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mbar;
   __shared__ Rec warp_slot[kBlock / 32];
@@ -722,7 +759,7 @@ __global__ void __launch_bounds__(kBlock, 2)
     const uint64_t lane = threadIdx.x & 31;
     const uint64_t gw_lo = g_first + n_groups * w / warps, gw_hi = g_first + n_groups * (w + 1) / warps;
     uint8_t* coef_base = slot_base + kSlotBytes * kBlock;
-    uint8_t* dp_base = coef_base + sizeof(int64_t) * 28 * kBlock;
+    uint8_t* dp_base = coef_base + sizeof(int64_t) * kCoefEntries * kBlock;
     int64_t* fw = reinterpret_cast<int64_t*>(dp_base + dp_bytes_per_warp(h->n_nodes) * (threadIdx.x >> 5));
     int64_t* cw = fw + 32 * h->n_nodes;
     const int P = h->n_nodes - K;
@@ -749,7 +786,8 @@ __global__ void __launch_bounds__(kBlock, 2)
       const uint64_t lo = max(g * G, jd.sub_lo), hi = min((g + 1) * G, jd.sub_hi);
       const uint64_t len = hi - lo;
       const uint64_t a = lo + len * lane / 32, b = lo + len * (lane + 1) / 32;
-      if (a < b) run_subrows<K, PRIM, NV>(smem, slot_base, coef_base, v, a, b, dtop, cw, ea_top, q_top, lex_top);
+      if (a < b)
+        run_subrows<K, PRIM, NV, PT>(smem, slot_base, coef_base, v, ip, a, b, dtop, cw, ea_top, q_top, lex_top);
       __syncwarp();
     }
   }
@@ -777,32 +815,34 @@ __global__ void __launch_bounds__(kBlock, 2)
   }
 }
 
-using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, unsigned*, Rec*);
+using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, unsigned*, Rec*, InnerParams);
 
+// pt: the innermost table comes from the kernel parameter (single-problem
+// launches); batch launches read it per job from shared memory.
 template <int K>
-KernelFn pick_nv(int prim, int nv) {
-  if (prim == kPrimQual) return search_kernel<K, kPrimQual, 0>;
+KernelFn pick_nv(int prim, int nv, bool pt) {
+  if (prim == kPrimQual) return search_kernel<K, kPrimQual, 0, false>;
   if (prim == kPrimFp) {
-    if (nv == 8) return search_kernel<K, kPrimFp, 8>;
-    if (nv == 16) return search_kernel<K, kPrimFp, 16>;
-    return search_kernel<K, kPrimFp, 0>;
+    if (nv == 8) return pt ? search_kernel<K, kPrimFp, 8, true> : search_kernel<K, kPrimFp, 8, false>;
+    if (nv == 16) return pt ? search_kernel<K, kPrimFp, 16, true> : search_kernel<K, kPrimFp, 16, false>;
+    return search_kernel<K, kPrimFp, 0, false>;
   }
-  if (nv == 8) return search_kernel<K, kPrimLat, 8>;
-  if (nv == 16) return search_kernel<K, kPrimLat, 16>;
-  return search_kernel<K, kPrimLat, 0>;
+  if (nv == 8) return pt ? search_kernel<K, kPrimLat, 8, true> : search_kernel<K, kPrimLat, 8, false>;
+  if (nv == 16) return pt ? search_kernel<K, kPrimLat, 16, true> : search_kernel<K, kPrimLat, 16, false>;
+  return search_kernel<K, kPrimLat, 0, false>;
 }
 
-KernelFn pick_kernel(int K, int prim, int nv) {
-  if (K == 2) return pick_nv<2>(prim, nv);
-  if (K == 3) return pick_nv<3>(prim, nv);
-  return pick_nv<4>(prim, nv);
+KernelFn pick_kernel(int K, int prim, int nv, bool pt) {
+  if (K == 2) return pick_nv<2>(prim, nv, pt);
+  if (K == 3) return pick_nv<3>(prim, nv, pt);
+  return pick_nv<4>(prim, nv, pt);
 }
 
 // Dynamic shared memory of a launch: problem image + per-thread slots.
-// (coefficient columns sized for K = 4: 16 + 8 + 4 entries per thread)
+// (coefficient columns sized for K = 4: 8 + 4 entries per thread)
 // + per-warp DP scratch
 size_t smem_bytes(size_t blob, int n_nodes) {
-  return ((blob + 127) & ~size_t(127)) + static_cast<size_t>(kSlotBytes) * kBlock + sizeof(int64_t) * 28 * kBlock +
+  return ((blob + 127) & ~size_t(127)) + static_cast<size_t>(kSlotBytes) * kBlock + sizeof(int64_t) * kCoefEntries * kBlock +
          dp_bytes_per_warp(n_nodes) * (kBlock / 32);
 }
 
@@ -1125,6 +1165,7 @@ struct Built {
   int prim = kPrimFp;
   bool full_only = false;
   int nv = 0;  // innermost radix held in registers (8 / 16) or 0 (shared-memory loop)
+  InnerParams ip{};  // innermost table as a kernel parameter (nv > 0)
   uint64_t total = 0;
   uint64_t r_sub = 1;
   uint64_t n_sub = 0;
@@ -1219,7 +1260,8 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
     for (int k = optoff[n - 2]; k < optoff[n - 1]; ++k) pre_wmax = std::max(pre_wmax, p->wall_us[k]);
   if (wmax - wmin >= (int64_t(1) << 30) - 1 || pre_wmax >= (int64_t(1) << 30) - 1) full_only = true;
   const int inner_radix = p->radix[inner_node];
-  const int nv = inner_radix <= 8 ? 8 : inner_radix <= 16 ? 16 : 0;
+  int nv = inner_radix <= 8 ? 8 : inner_radix <= 16 ? 16 : 0;
+  if (const char* f = std::getenv("LOOM_FORCE_NV")) nv = std::atoi(f) == 0 ? 0 : nv;  // experiments
 
   // topology: Kahn order + predecessor CSR
   std::vector<int32_t> indeg(n, 0), topo;
@@ -1331,6 +1373,10 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   b.prim = prim;
   b.full_only = full_only;
   b.nv = nv;
+  for (int j = 0; j < 16; ++j) {
+    b.ip.g[j] = j < inner_pad ? inner[j].g : 0.0;
+    b.ip.w[j] = j < inner_pad ? inner[j].w : INT_MAX;
+  }
   b.total = total;
   b.r_sub = r_sub;
   b.n_sub = total / r_sub;
@@ -1569,7 +1615,7 @@ int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objec
   if (d.begin >= d.end)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
-  KernelFn fn = pick_kernel(b.K, b.prim, b.nv);
+  KernelFn fn = pick_kernel(b.K, b.prim, b.nv, true);
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes))) return rc;
   const int ctas = ctas_for(c, units, fn, smem_bytes(b.blob.size(), p->n_nodes));
   if (int rc = ensure(c->d_arena, c->arena_cap, b.blob.size())) return rc;
@@ -1581,7 +1627,8 @@ int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objec
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  fn<<<ctas, kBlock, smem_bytes(b.blob.size(), p->n_nodes), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch, c->d_tickets, c->d_out);
+  fn<<<ctas, kBlock, smem_bytes(b.blob.size(), p->n_nodes), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch,
+                                                                   c->d_tickets, c->d_out, b.ip);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
@@ -1620,7 +1667,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
   std::vector<Group> groups;
   for (int j = 0; j < n_jobs; ++j) {
     if (!ok[j]) continue;
-    KernelFn fn = pick_kernel(built[j].K, built[j].prim, built[j].nv);
+    KernelFn fn = pick_kernel(built[j].K, built[j].prim, built[j].nv, false);
     Group* g = nullptr;
     for (auto& x : groups)
       if (x.fn == fn) g = &x;
@@ -1652,15 +1699,12 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
   if (int rc = ensure_host(c, static_cast<size_t>(n_jobs))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, host_arena.data(), arena, cudaMemcpyHostToDevice, c->stream));
   std::vector<JobDesc> all;
-  std::vector<std::pair<int, int>> where;  // (group, slot)
-  size_t base = 0;
   for (auto& g : groups) {
     for (int j : g.jobs) {
       JobDesc d = make_desc(built[j], 0, built[j].total, false);
       d.blob_off = off[j];
       all.push_back(d);
     }
-    (void)base;
   }
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, all.data(), all.size() * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
   size_t first = 0;
@@ -1668,7 +1712,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
     if (int rc = set_smem(g.fn, g.smem)) return rc;
     const int nj = static_cast<int>(g.jobs.size());
     g.fn<<<nj, kBlock, g.smem, c->stream>>>(c->d_arena, c->d_jobs + first, 1, c->d_scratch + first,
-                                             c->d_tickets + first, c->d_out + first);
+                                             c->d_tickets + first, c->d_out + first, InnerParams{});
     LOOM_CUDA(cudaGetLastError());
     ++c->launches;
     first += nj;
@@ -1721,7 +1765,7 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   dp->host.edge_from = dp->efrom.data();
   dp->host.edge_to = dp->eto.data();
   dp->objective = *o;
-  dp->fn = pick_kernel(dp->built.K, dp->built.prim, dp->built.nv);
+  dp->fn = pick_kernel(dp->built.K, dp->built.prim, dp->built.nv, true);
   if (set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)) != LOOM_OK) {
     delete dp;
     return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: cannot size shared memory");
@@ -1771,7 +1815,7 @@ int loom_search_argmin_async(loom_ctx* c, loom_device_problem* dp, uint64_t begi
   const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)));
   LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
   dp->fn<<<ctas, kBlock, smem_bytes(dp->built.blob.size(), dp->host.n_nodes), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
-                                                             dp->d_ticket, dp->d_out);
+                                                             dp->d_ticket, dp->d_out, dp->built.ip);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(dp->h_out, dp->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));

@@ -73,6 +73,13 @@ struct Rec {
   int32_t found;
 };
 
+// Innermost table of a single-problem launch, passed as a kernel parameter so
+// the fast path reads it as constant-bank operands instead of registers.
+struct InnerParams {
+  double g[16];
+  int32_t w[16];
+};
+
 // One plan's Pareto coordinates (40 bytes; same layout as loom_point).
 struct ParetoPoint {
   uint64_t index;

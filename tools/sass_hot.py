@@ -8,6 +8,7 @@ import tempfile
 from pathlib import Path
 
 K, P, NV = sys.argv[1:4]
+PT = sys.argv[4] if len(sys.argv) > 4 else "1"
 obj = Path(__file__).resolve().parents[1] / "paper_2501_16634_b200" / "_build" / "loom_search.cu.o"
 with tempfile.TemporaryDirectory() as td:
     subprocess.run(["cuobjdump", "-xelf", "all", str(obj)], cwd=td, capture_output=True)
@@ -15,7 +16,7 @@ with tempfile.TemporaryDirectory() as td:
     sass = subprocess.run(["nvdisasm", "-c", str(cubin)], capture_output=True, text=True).stdout
 for sec in re.split(r"\n\s*\.section\s+\.text\.", sass)[1:]:
     name = sec.split(",")[0]
-    if f"search_kernelILi{K}ELi{P}ELi{NV}E" not in name or "slow" in name:
+    if f"search_kernelILi{K}ELi{P}ELi{NV}ELb{PT}E" not in name or "slow" in name:
         continue
     lines = [l for l in sec.split("\n") if re.search(r"/\*[0-9a-f]{4,5}\*/", l) or l.strip().startswith(".L_x")]
     idx = [i for i, l in enumerate(lines) if "DSETP" in l or ("ISETP.LE.AND" in l)]
