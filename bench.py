@@ -177,9 +177,16 @@ def b200_arm(args) -> None:
     from paper_2501_16634_b200 import dist as D, loom, workloads as W
 
     world, rank, local = dist_env()
+    # one process per GPU; LOOM_DIST_BACKEND=gloo lets ranks share a GPU when
+    # validating the multi-rank path on a single-GPU box
+    backend = os.environ.get("LOOM_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.Stream()
     ctx = loom.Context(local, stream.cuda_stream)
     w = W.config3()
@@ -194,13 +201,22 @@ def b200_arm(args) -> None:
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
+
+    def shard_result():
+        try:
+            return dp.result()
+        except loom.NoFeasibleConfigError:  # nothing feasible in this rank's shard
+            return D.empty_winner()
 
     # ---- value: resident problem, device-timed -------------------------------
     for _ in range(args.warmup):
         dp.search_async(begin, end)
-        dp.result()
+        shard_result()
     launches0 = ctx.launches
     step_ms = []
     with ClockSampler(local) as clocks:
@@ -212,20 +228,21 @@ def b200_arm(args) -> None:
             e0.record(stream)
             dp.search_async(begin, end)
             e1.record(stream)
-            dp.result()
+            shard_result()
             step_ms.append(e0.elapsed_time(e1))
         barrier()
     launches = ctx.launches - launches0
     local_ms = sum(step_ms) / len(step_ms)
-    t = torch.tensor([local_ms], dtype=torch.float64, device="cuda")
+    red_dev = "cuda" if backend == "nccl" else "cpu"
+    t = torch.tensor([local_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = total / (ms / 1e3)
 
     # winners must agree with a full-space reduce (checked every run)
-    local_w = dp.result()
-    winners = D.allgather_winners(local_w, device="cuda") if world > 1 else [local_w]
+    local_w = shard_result()
+    winners = D.allgather_winners(local_w, device=red_dev) if world > 1 else [local_w]
     chosen = D.combine(winners, obj)
 
     # ---- e2e: the public drop-in call, host JSON in / plan out ---------------
@@ -238,7 +255,7 @@ def b200_arm(args) -> None:
             mine = loom.search_argmin(ctx, low.problem, o, begin, end)
         except loom.NoFeasibleConfigError:
             mine = D.empty_winner()
-        best = D.combine(D.allgather_winners(mine, device="cuda"), o)
+        best = D.combine(D.allgather_winners(mine, device=red_dev), o)
         return low.config(best["plan_index"]) | best
 
     for _ in range(max(1, args.warmup)):
@@ -250,7 +267,7 @@ def b200_arm(args) -> None:
         t0 = time.perf_counter()
         out = e2e_step()
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device="cuda")
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = total / (float(te.item()) / 1e3)
