@@ -319,10 +319,11 @@ def b200_arm(args) -> None:
         dist.destroy_process_group()
 
 
-# Compiled fast path of the innermost context of search_kernel<4, kPrimFp, 16>
-# (tools/sass_hot.py 4 0 16): 68 SASS instructions per 16 plans -- 17 DADD,
-# 16 DSETP, 17 ISETP, 8 PLOP3, loads/loop control.  DESIGN.md §5.
-ISSUE_INSTR_PER_PLAN = 68 / 16
+# Compiled fast path of the innermost contexts of search_kernel<4, kPrimFp,
+# 16, true> (tools/sass_hot.py 4 0 16 1): 143 SASS instructions per 32 plans
+# -- 34 DADD, 32 DSETP, 34 ISETP, 17 PLOP3, 12 LDCU, loads/loop control.
+# DESIGN.md §5.
+ISSUE_INSTR_PER_PLAN = 143 / 32
 
 
 def other_configs(ctx, loom, W) -> dict:
