@@ -356,6 +356,14 @@ def other_configs(ctx, loom, W) -> dict:
     out["c4"] = {"jobs": len(jobs), "plans": plans, "lowering_ms": 1e3 * (t1 - t0), "search_ms": 1e3 * (t2 - t1),
                  "time_to_plan_ms": 1e3 * (t2 - t0), "search_plans_per_s": plans / (t2 - t1),
                  "feasible_jobs": sum(1 for s, _ in res if s == 0)}
+    # greedy_search (the reference CLI's default) on the GPU, one CTA
+    w3 = W.config3(slo_us=None)
+    g_args = (json.dumps(w3.dag), json.dumps(w3.library), {"constraint": "MIN_COST"}, json.dumps(w3.bounds))
+    loom.greedy_search(*g_args, ctx=ctx)
+    t0 = time.perf_counter()
+    g = loom.greedy_search(*g_args, ctx=ctx)
+    out["c3_greedy"] = {"time_to_plan_ms": 1e3 * (time.perf_counter() - t0), "latency_us": g["latency_us"],
+                        "gpu_wh": g["gpu_wh"]}
     w5 = W.config5()
     lw5 = loom.Lowered(w5.dag, w5.library, w5.bounds)
     loom.search_pareto_points(ctx, lw5.problem, 0, lw5.total - 1)

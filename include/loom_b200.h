@@ -210,6 +210,28 @@ int loom_search_pareto_points(loom_ctx* ctx, const loom_problem* problem, uint64
  * keep[i] = 1 iff no other point dominates point i.  Runs on the device. */
 int loom_pareto_filter_points(loom_ctx* ctx, const loom_point* points, uint64_t n, uint8_t* keep);
 
+/* ---- greedy_search (optimizer.hpp:227-291) -------------------------------- */
+/* Node-local seed of greedy_search (optimizer.hpp:194-220, 256-268): per node,
+ * among options meeting the quality floor, the first minimum of the criteria
+ * values of the option alone.  LOOM_INFEASIBLE if a node has none
+ * (optimizer.hpp:248-251). */
+int loom_greedy_seed(const loom_problem* problem, const loom_objective* objective, int32_t* digits);
+/* Coordinate descent from `seed` (NULL: loom_greedy_seed), re-optimizing one
+ * node at a time in `sweep_order` (NULL: index-ordered Kahn; the reference
+ * uses topological_order, see loom_lowered_sweep_order) for at most
+ * `max_sweeps` sweeps, stopping after a sweep without improvement.  Each
+ * node step evaluates all of the node's options on the device at once; the
+ * result equals the reference's sequential first-improvement scan because
+ * the objective order is strict. */
+int loom_search_greedy(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
+                       const int32_t* sweep_order, const int32_t* seed, int32_t max_sweeps, loom_winner* out);
+/* The reference's topological_order (workflow.hpp:467-498, peers by node id) as node indices. */
+int loom_lowered_sweep_order(const loom_lowered* lowered, int32_t* out);
+/* greedy_search(dag, library, objective, bounds) on reference-format JSON; same output as
+ * loom_exhaustive_search_json. */
+int loom_greedy_search_json(loom_ctx* ctx, const char* dag_json, const char* library_json, const char* objective_json,
+                            const char* bounds_json, int32_t max_sweeps, char* out_json, size_t cap, size_t* needed);
+
 /* ---- the drop-in call on reference-format JSON -------------------------- */
 /* exhaustive_search(dag, library, objective, bounds) -> ConfigEstimate JSON:
  * {"identifier","config","latency_us","gpu_wh","cpu_wh","total_wh","dollars",

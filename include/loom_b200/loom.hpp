@@ -227,6 +227,13 @@ ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& lib
                                  const ObjectiveHierarchy& objective, const SearchBounds& bounds,
                                  loom_ctx* ctx, std::optional<Micros> latency_slo_us = std::nullopt);
 
+// greedy_search (optimizer.hpp:227-291) on the GPU: node-local seeds on the
+// host, every sweep's per-node argmin on the device (one CTA).
+ConfigEstimate greedy_search(const WorkflowDag& dag, const AgentLibrary& library, const ObjectiveHierarchy& objective,
+                             const SearchBounds& bounds, int max_sweeps = 10);
+ConfigEstimate greedy_search(const WorkflowDag& dag, const AgentLibrary& library, const ObjectiveHierarchy& objective,
+                             const SearchBounds& bounds, int max_sweeps, loom_ctx* ctx);
+
 // ---- lowering: the flat tables the kernels read --------------------------
 struct LoweredProblem {
   std::vector<std::string> node_ids;                 // dag.nodes order
@@ -237,6 +244,7 @@ struct LoweredProblem {
   std::vector<int32_t> quality, lexrank;
   std::vector<uint64_t> lex_weight;
   std::vector<int32_t> edge_from, edge_to;
+  std::vector<int32_t> sweep_order;  // topological_order (workflow.hpp:467-498): id-ordered Kahn
   uint64_t total = 0;  // 0 for an empty space
   loom_problem view() const;
   ConfigPoint config_of(uint64_t plan_index) const;

@@ -273,11 +273,124 @@ ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& lib
   return e;
 }
 
+namespace {
+// greedy_search's seeding / feasibility errors carry node ids (optimizer.hpp:232-251).
+void greedy_prepare(const LoweredProblem& L, const WorkflowDag& dag, const loom_objective& o, std::vector<int32_t>& seed) {
+  if (dag.nodes.empty()) throw NoFeasibleConfigError("cannot search an empty dag");
+  const loom_problem view = L.view();
+  seed.assign(L.radix.size(), 0);
+  const int rc = loom_greedy_seed(&view, &o, seed.data());
+  if (rc == LOOM_INFEASIBLE) {
+    const std::string msg = loom_last_error();
+    const auto at = msg.find("node #");
+    const int idx = at == std::string::npos ? -1 : std::atoi(msg.c_str() + at + 6);
+    const std::string id = idx >= 0 && idx < static_cast<int>(L.node_ids.size()) ? L.node_ids[idx] : "?";
+    throw NoFeasibleConfigError("node '" + id + "' has no lever assignment meeting the quality floor");
+  }
+  if (rc != LOOM_OK) throw std::runtime_error(loom_last_error());
+}
+}  // namespace
+
+ConfigEstimate greedy_search(const WorkflowDag& dag, const AgentLibrary& library, const ObjectiveHierarchy& objective,
+                             const SearchBounds& bounds, int max_sweeps) {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  if (!g_ctx && loom_ctx_create(0, nullptr, &g_ctx) != LOOM_OK) throw std::runtime_error(loom_last_error());
+  return greedy_search(dag, library, objective, bounds, max_sweeps, g_ctx);
+}
+
+ConfigEstimate greedy_search(const WorkflowDag& dag, const AgentLibrary& library, const ObjectiveHierarchy& objective,
+                             const SearchBounds& bounds, int max_sweeps, loom_ctx* ctx) {
+  const LoweredProblem L = lower(dag, library, bounds);
+  const loom_objective obj = to_objective(objective, std::nullopt);
+  std::vector<int32_t> seed;
+  greedy_prepare(L, dag, obj, seed);
+  if (L.total == 0) throw NoFeasibleConfigError("no configuration satisfies the quality floor and bounds");
+  const loom_problem view = L.view();
+  loom_winner w;
+  const int rc = loom_search_greedy(ctx, &view, &obj, L.sweep_order.data(), seed.data(), max_sweeps, &w);
+  if (rc != LOOM_OK) throw std::runtime_error(loom_last_error());
+  return estimate(L.config_of(w.plan_index), dag, library);
+}
+
 }  // namespace loom
 
 extern "C" {
 
 int loom_abi_version(void) { return LOOM_B200_ABI_VERSION; }
+
+int loom_greedy_seed(const loom_problem* p, const loom_objective* o, int32_t* digits) {
+  uint64_t total = 0;
+  if (int rc = loomi::check_problem(p, &total)) return rc;
+  if (!o || !digits) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  int off = 0;
+  for (int i = 0; i < p->n_nodes; ++i) {
+    // detail::node_local_key (optimizer.hpp:194-220): the option's own
+    // contribution to each criterion; std::vector<double> ordering
+    int best = -1;
+    std::vector<double> best_key;
+    for (int k = 0; k < p->radix[i]; ++k) {
+      const int x = off + k;
+      if (o->has_quality_floor && p->quality[x] < o->quality_floor) continue;  // optimizer.hpp:239-247
+      std::vector<double> key;
+      for (int c = 0; c < o->n_criteria; ++c) {
+        switch (o->criteria[c]) {
+          case LOOM_MIN_COST_DOLLARS: key.push_back(p->dollars[x]); break;
+          case LOOM_MIN_ENERGY: key.push_back(p->gpu_wh[x]); break;
+          case LOOM_MIN_LATENCY: key.push_back(static_cast<double>(p->wall_us[x])); break;
+          default: key.push_back(static_cast<double>(-p->quality[x])); break;
+        }
+      }
+      if (best < 0 || key < best_key) {
+        best = k;
+        best_key = std::move(key);
+      }
+    }
+    if (best < 0)
+      return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: node #" + std::to_string(i) +
+                                              " has no lever assignment meeting the quality floor");
+    digits[i] = best;
+    off += p->radix[i];
+  }
+  return LOOM_OK;
+}
+
+int loom_lowered_sweep_order(const loom_lowered* lw, int32_t* out) {
+  if (!lw || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  std::copy(lw->L.sweep_order.begin(), lw->L.sweep_order.end(), out);
+  return LOOM_OK;
+}
+
+int loom_greedy_search_json(loom_ctx* ctx, const char* dag_json, const char* library_json, const char* objective_json,
+                            const char* bounds_json, int32_t max_sweeps, char* out_json, size_t cap, size_t* needed) {
+  int rc = LOOM_OK;
+  std::string result;
+  try {
+    const loom::WorkflowDag dag = loom::WorkflowDag::from_json_text(dag_json ? dag_json : "");
+    const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json ? library_json : "");
+    const loom::SearchBounds bounds = loom::SearchBounds::from_json_text(bounds_json ? bounds_json : "{}");
+    const ParsedObjective obj = parse_objective_json(objective_json ? objective_json : "");
+    const loom::LoweredProblem L = loom::lower(dag, lib, bounds);
+    const loom_objective o = to_objective(obj.hierarchy, obj.slo);
+    std::vector<int32_t> seed;
+    loom::greedy_prepare(L, dag, o, seed);
+    const loom_problem view = L.view();
+    loom_winner w;
+    rc = loom_search_greedy(ctx, &view, &o, L.sweep_order.data(), seed.data(), max_sweeps, &w);
+    if (rc == LOOM_OK) result = estimate_json(loom::estimate(L.config_of(w.plan_index), dag, lib), w.plan_index, L.total);
+    else result = error_json(loom_last_error());
+  } catch (const loom::Error& e) {
+    rc = loomi::fail(status_of(e), e.what());
+    result = error_json(e.what());
+  } catch (const std::exception& e) {
+    rc = loomi::fail(LOOM_INVALID, std::string("InvalidConfigError: ") + e.what());
+    result = error_json(loom_last_error());
+  }
+  const std::string err = loom_last_error();
+  const int crc = copy_out(result, out_json, cap, needed);
+  if (rc == LOOM_OK) return crc;
+  loomi::set_error(err);
+  return rc;
+}
 
 const char* loom_last_error(void) { return loomi::g_error.c_str(); }
 

@@ -600,6 +600,27 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
     L.edge_to.push_back(t->second);
   }
   topo_order(n, L.edge_from, L.edge_to);  // throws CycleError like topological_order
+  {
+    // the reference's topological_order: Kahn with ready peers popped in node-id
+    // order (workflow.hpp:467-498); greedy_search sweeps nodes in this order
+    std::vector<int> indeg(n, 0);
+    std::vector<std::vector<int>> succ(n);
+    for (std::size_t e = 0; e < L.edge_from.size(); ++e) {
+      succ[L.edge_from[e]].push_back(L.edge_to[e]);
+      ++indeg[L.edge_to[e]];
+    }
+    auto by_id = [&](int a, int b) { return L.node_ids[a] > L.node_ids[b]; };
+    std::priority_queue<int, std::vector<int>, decltype(by_id)> ready(by_id);
+    for (int i = 0; i < n; ++i)
+      if (!indeg[i]) ready.push(i);
+    while (!ready.empty()) {
+      const int v = ready.top();
+      ready.pop();
+      L.sweep_order.push_back(v);
+      for (int s2 : succ[v])
+        if (--indeg[s2] == 0) ready.push(s2);
+    }
+  }
 
   // The identifier tie-break is replaced by a per-node rank of the option's
   // identifier substring.  That is exact only if no substring is a proper

@@ -44,6 +44,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -1157,6 +1158,84 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // ---------------------------------------------------------------------------
+// greedy_search (optimizer.hpp:227-291): one CTA runs the whole coordinate
+// descent.  A node step re-optimizes one node with every other digit fixed;
+// the reference scans the node's options sequentially, replacing the best on
+// every strict improvement, which under a strict total order ends at the
+// argmin over {current, all options} -- computed here in one parallel pass
+// (one thread per option, full re-evaluation, block min-loc).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock)
+    greedy_kernel(const uint8_t* __restrict__ blob_g, uint32_t blob_bytes, const int32_t* __restrict__ order,
+                  const int32_t* __restrict__ seed, int max_sweeps, Rec* __restrict__ out, int* __restrict__ sweeps) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t mbar;
+  __shared__ Rec warp_slot[kBlock / 32];
+  __shared__ int cur[kMaxNodes];
+  __shared__ uint64_t stride[kMaxNodes];
+  __shared__ Rec best;
+  __shared__ int improved;
+  load_blob(smem, blob_g, blob_bytes, &mbar);
+  const View v = make_view(smem);
+  const BlobHeader* h = v.h;
+  const int n = h->n_nodes;
+  if (threadIdx.x == 0) {
+    uint64_t s = 1;
+    for (int i = n - 1; i >= 0; --i) {
+      stride[i] = s;
+      s *= static_cast<uint64_t>(v.radix[i]);
+    }
+  }
+  if (threadIdx.x < n) cur[threadIdx.x] = seed[threadIdx.x];
+  __syncthreads();
+  auto index_of = [&](const int* d) {
+    uint64_t x = 0;
+    for (int i = 0; i < n; ++i) x += static_cast<uint64_t>(d[i]) * stride[i];
+    return x;
+  };
+  if (threadIdx.x == 0) {
+    int d[kMaxNodes];
+    for (int i = 0; i < n; ++i) d[i] = cur[i];
+    Rec c;
+    eval_digits(v, d, c, index_of(d));
+    best = c;
+  }
+  __syncthreads();
+  int done = 0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) improved = 0;
+    __syncthreads();
+    for (int t = 0; t < n; ++t) {
+      const int node = order[t];
+      const int r = v.radix[node];
+      Rec mine{0, 0, 0, 0, 0, 0, 0};
+      for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        if (j == cur[node]) continue;  // optimizer.hpp:277
+        int d[kMaxNodes];
+        for (int i = 0; i < n; ++i) d[i] = cur[i];
+        d[node] = j;
+        Rec c;
+        eval_digits(v, d, c, index_of(d));
+        if (rec_better(c, mine, h)) mine = c;
+      }
+      const Rec cand = block_best(mine, h, warp_slot);
+      if (threadIdx.x == 0 && rec_better(cand, best, h)) {
+        best = cand;
+        cur[node] = static_cast<int>((cand.index / stride[node]) % static_cast<uint64_t>(r));
+        improved = 1;
+      }
+      __syncthreads();
+    }
+    done = sweep + 1;
+    if (!improved) break;
+  }
+  if (threadIdx.x == 0) {
+    out[0] = best;
+    sweeps[0] = done;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host: problem image builder
 // ---------------------------------------------------------------------------
 struct Built {
@@ -2096,4 +2175,66 @@ extern "C" int loom_pareto_filter_points(loom_ctx* c, const loom_point* pts, uin
   LOOM_CUDA(cudaMemcpyAsync(keep, k.p, n, cudaMemcpyDeviceToHost, c->stream));
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   return LOOM_OK;
+}
+
+extern "C" int loom_search_greedy(loom_ctx* c, const loom_problem* p, const loom_objective* o,
+                                  const int32_t* sweep_order, const int32_t* seed, int32_t max_sweeps,
+                                  loom_winner* out) {
+  if (!c || !p || !o || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  std::memset(out, 0, sizeof *out);
+  LOOM_CUDA(cudaSetDevice(c->device));
+  uint64_t total = 0;
+  if (int rc = loomi::check_problem(p, &total)) return rc;
+  if (p->n_nodes == 0) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: cannot search an empty dag");
+  const int n = p->n_nodes;
+  std::vector<int32_t> sd(n), ord;
+  if (seed) sd.assign(seed, seed + n);
+  else if (int rc = loom_greedy_seed(p, o, sd.data())) return rc;
+  if (sweep_order) {
+    ord.assign(sweep_order, sweep_order + n);
+  } else {  // index-ordered Kahn
+    std::vector<int> indeg(n, 0);
+    std::vector<std::vector<int>> succ(n);
+    for (int e = 0; e < p->n_edges; ++e) {
+      succ[p->edge_from[e]].push_back(p->edge_to[e]);
+      ++indeg[p->edge_to[e]];
+    }
+    std::priority_queue<int, std::vector<int>, std::greater<>> ready;
+    for (int i = 0; i < n; ++i)
+      if (!indeg[i]) ready.push(i);
+    while (!ready.empty()) {
+      const int x = ready.top();
+      ready.pop();
+      ord.push_back(x);
+      for (int y : succ[x])
+        if (--indeg[y] == 0) ready.push(y);
+    }
+    if (static_cast<int>(ord.size()) != n) return loomi::fail(LOOM_INVALID, "CycleError: dag has a cycle");
+  }
+  for (int i = 0; i < n; ++i)
+    if (sd[i] < 0 || sd[i] >= p->radix[i]) return loomi::fail(LOOM_INVALID, "InvalidConfigError: seed out of range");
+  Built b;
+  if (int rc = build_image(p, o, 1, b)) return rc;
+  const uint32_t bytes = static_cast<uint32_t>(b.blob.size());
+  DevBuf<uint8_t> d_blob;
+  DevBuf<int32_t> d_ord, d_seed, d_sw;
+  DevBuf<Rec> d_out;
+  LOOM_CUDA(d_blob.alloc(bytes));
+  LOOM_CUDA(d_ord.alloc(n));
+  LOOM_CUDA(d_seed.alloc(n));
+  LOOM_CUDA(d_sw.alloc(1));
+  LOOM_CUDA(d_out.alloc(1));
+  LOOM_CUDA(cudaMemcpyAsync(d_blob.p, b.blob.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+  LOOM_CUDA(cudaMemcpyAsync(d_ord.p, ord.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
+  LOOM_CUDA(cudaMemcpyAsync(d_seed.p, sd.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
+  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(greedy_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes + 128)));
+  greedy_kernel<<<1, kBlock, bytes + 128, c->stream>>>(d_blob.p, bytes, d_ord.p, d_seed.p, max_sweeps, d_out.p,
+                                                       d_sw.p);
+  LOOM_CUDA(cudaGetLastError());
+  ++c->launches;
+  Rec r;
+  LOOM_CUDA(cudaMemcpyAsync(&r, d_out.p, sizeof r, cudaMemcpyDeviceToHost, c->stream));
+  LOOM_CUDA(cudaStreamSynchronize(c->stream));
+  return finish_winner(p, r, out);
 }

@@ -166,6 +166,11 @@ def lib() -> C.CDLL:
         "loom_search_pareto_points": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(Point), C.c_uint64,
                                        C.POINTER(C.c_uint64)], C.c_int),
         "loom_pareto_filter_points": ([vp, C.POINTER(Point), C.c_uint64, C.POINTER(C.c_uint8)], C.c_int),
+        "loom_greedy_seed": ([P, O, C.POINTER(C.c_int32)], C.c_int),
+        "loom_search_greedy": ([vp, P, O, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, W], C.c_int),
+        "loom_lowered_sweep_order": ([vp, C.POINTER(C.c_int32)], C.c_int),
+        "loom_greedy_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32, C.c_char_p,
+                                     C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
         "loom_exhaustive_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
                                          C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     }
@@ -261,6 +266,11 @@ class Lowered:
 
     def option(self, node: int, option: int) -> dict:
         return self._json(lib().loom_lowered_option_json, node, option)
+
+    def sweep_order(self) -> list[int]:
+        out = (C.c_int32 * max(1, self.problem.n_nodes))()
+        _check(lib().loom_lowered_sweep_order(self._h, out))
+        return list(out)[: self.problem.n_nodes]
 
     def evaluate(self, plan_index: int) -> dict:
         w = Winner()
@@ -450,6 +460,33 @@ def exhaustive_search(dag: Any, library: Any, objective_: Any, bounds: Any, ctx:
     if rc != LOOM_OK:
         _raise(rc, out.get("message", last_error()))
     return out
+
+
+def greedy_search(dag: Any, library: Any, objective_: Any, bounds: Any, ctx: Context | None = None,
+                  max_sweeps: int = 10) -> dict:
+    """loom::greedy_search (optimizer.hpp:227-291) on reference-format JSON."""
+    ctx = ctx or default_context()
+    if isinstance(objective_, str) and not objective_.lstrip().startswith("{"):
+        objective_ = {"constraint": objective_}
+    need = C.c_size_t(0)
+    cap = 1 << 16
+    buf = C.create_string_buffer(cap)
+    rc = lib().loom_greedy_search_json(ctx.handle, _text(dag), _text(library), _text(objective_), _text(bounds),
+                                       max_sweeps, buf, cap, C.byref(need))
+    out = json.loads(buf.value.decode())
+    if rc != LOOM_OK:
+        _raise(rc, out.get("message", last_error()))
+    return out
+
+
+def search_greedy(ctx: Context, problem: Problem, obj: Objective, sweep_order: Sequence[int] | None = None,
+                  seed: Sequence[int] | None = None, max_sweeps: int = 10) -> dict:
+    n = problem.n_nodes
+    so = (C.c_int32 * n)(*sweep_order) if sweep_order is not None else None
+    sd = (C.c_int32 * n)(*seed) if seed is not None else None
+    w = Winner()
+    _check(lib().loom_search_greedy(ctx.handle, C.byref(problem), C.byref(obj), so, sd, max_sweeps, C.byref(w)))
+    return w.as_dict()
 
 
 @dataclass

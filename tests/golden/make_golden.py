@@ -122,6 +122,29 @@ def make_random(n: int = 80) -> None:
     dump(GOLD / "random" / "results.json", out)
 
 
+def make_greedy(n: int = 80) -> None:
+    """Reference greedy_search on the random scenarios (all tokens, plus a
+    quality floor), C2, C3 (no SLO: the reference has none) and C4 jobs."""
+    out = {"random": {}, "c2": {}, "c3": {}, "c4": {}}
+    for seed in range(n):
+        w = W.random_scenario(seed, max_nodes=5)
+        entry = {"digest": digest(w)}
+        for t in TOKENS:
+            entry[t] = search(w, {"constraint": t}, "greedy")
+        entry["floor2"] = search(w, {"constraint": w.objective["constraint"], "quality_floor": 2}, "greedy")
+        out["random"][str(seed)] = entry
+    w = W.config2()
+    for t in TOKENS:
+        out["c2"][t] = search(w, {"constraint": t}, "greedy")
+    out["c2"]["config"] = search(w, w.objective, "greedy")
+    w = W.config3(slo_us=None)
+    for t in TOKENS:
+        out["c3"][t] = search(w, {"constraint": t}, "greedy")
+    for j, w in enumerate(W.config4(16)):
+        out["c4"][str(j)] = search(w, w.objective, "greedy")
+    dump(GOLD / "greedy" / "results.json", out)
+
+
 def make_c3() -> None:
     w = W.config3()
     threads = os.cpu_count() or 8
@@ -160,7 +183,7 @@ if __name__ == "__main__":
         if a.startswith("--only"):
             only = set(a.split("=", 1)[1].split(","))
     for name, fn in [("c1", make_c1), ("c2", make_c2), ("random", make_random), ("c3", make_c3),
-                     ("c4", make_c4), ("c5", make_c5)]:
+                     ("c4", make_c4), ("c5", make_c5), ("greedy", make_greedy)]:
         if only is None or name in only:
             t = time.time()
             fn()
