@@ -320,10 +320,11 @@ def b200_arm(args) -> None:
 
 
 # Compiled fast path of the innermost contexts of search_kernel<4, kPrimFp,
-# 16, true> (tools/sass_hot.py 4 0 16 1): 143 SASS instructions per 32 plans
-# -- 34 DADD, 32 DSETP, 34 ISETP, 17 PLOP3, 12 LDCU, loads/loop control.
+# 16, true> (tools/sass_hot.py 4 0 16 1): 271 SASS instructions per 64 plans
+# (two unrolled two-context steps) -- 68 DADD, 64 DSETP, 69 ISETP, 32 PLOP3,
+# 12 LDCU, loads / loop control.
 # DESIGN.md §5.
-ISSUE_INSTR_PER_PLAN = 143 / 32
+ISSUE_INSTR_PER_PLAN = 271 / 64
 
 
 def other_configs(ctx, loom, W) -> dict:

@@ -492,29 +492,50 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       }
     };
     if constexpr (NV > 0) {
-      // Two contexts per step share the register-resident innermost table:
-      // twice the independent DADD -> DSETP chains per warp.
-      int o = o_lo;
-      for (; o + 1 < o_hi; o += 2) {
-        const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
-        const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
-        const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
-        bool a0 = false, a1 = false;
+      // Two contexts per step share the innermost table: twice the
+      // independent DADD -> DSETP chains per warp.  The step loop holds no
+      // call, so the table stays in uniform registers across steps: a step
+      // whose contexts may hold a plan that ties or beats the running best
+      // only sets its bit in `hits`, and those contexts are re-tested (with
+      // the then-current thresholds) and scanned exactly after the loop.
+      // Testing with thresholds older than the running best only lets more
+      // contexts through, so no candidate is lost.
+      for (int c_lo = o_lo; c_lo < o_hi; c_lo += 64) {
+        const int c_hi = min(o_hi, c_lo + 64);
+        uint32_t hits = 0, bit = 1;
+        int o = c_lo;
+#pragma unroll 2
+        for (; o + 1 < c_hi; o += 2, bit <<= 1) {
+          const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
+          const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
+          const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
+          bool a = false;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          a0 |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw0, eu0, INT_MAX);
-          a1 |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw1, eu1, INT_MAX);
+          for (int j = 0; j < NV; ++j) {
+            a |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw0, eu0, INT_MAX);
+            a |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw1, eu1, INT_MAX);
+          }
+          // a real (rarely taken) branch keeps the per-plan tests a predicate
+          // OR chain; the empty asm stops if-conversion into per-plan selects
+          if (__builtin_expect(a, 0)) {
+            asm volatile("");
+            hits |= bit;
+          }
         }
-        if (__builtin_expect(a0 | a1, 0)) {
-          if (a0) context_slow(o, eu0, INT_MAX, tw0, 0);
-          if (a1) context_slow(o + 1, eu1, INT_MAX, inner_tw(pr, wu1), 0);
+        if (o < c_hi) {
+          const int32_t wu = H.w32[off + o];
+          const double eu = __dadd_rn(ea, H.ga[off + o]);
+          if (in.any_pass(H, ip, inner_tw(pr, wu), eu, INT_MAX)) hits |= bit;
         }
-      }
-      if (o < o_hi) {
-        const int32_t wu = H.w32[off + o];
-        const double eu = __dadd_rn(ea, H.ga[off + o]);
-        const int32_t tw = inner_tw(pr, wu);
-        if (__builtin_expect(in.any_pass(H, ip, tw, eu, INT_MAX), 0)) context_slow(o, eu, INT_MAX, tw, 0);
+        while (__builtin_expect(hits != 0, 0)) {
+          const int p = __ffs(hits) - 1;
+          hits &= hits - 1;
+          for (int oo = c_lo + 2 * p; oo < min(c_hi, c_lo + 2 * p + 2); ++oo) {
+            const double eu = __dadd_rn(ea, H.ga[off + oo]);
+            const int32_t tw = inner_tw(pr, H.w32[off + oo]);
+            if (in.any_pass(H, ip, tw, eu, INT_MAX)) context_slow(oo, eu, INT_MAX, tw, 0);
+          }
+        }
       }
     } else {
       for (int o = o_lo; o < o_hi; ++o) {
@@ -715,7 +736,7 @@ __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
 template <int K, int PRIM, int NV, bool PT>
 __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
     search_kernel(const uint8_t* __restrict__ arena, const JobDesc* __restrict__ jobs, int ctas_per_job,
-                  Rec* __restrict__ scratch, unsigned* __restrict__ tickets, Rec* __restrict__ out,
+                  Rec* __restrict__ scratch, JobSync* __restrict__ sync, Rec* __restrict__ out,
                   const InnerParams ip) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mbar;
@@ -754,17 +775,21 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
   if (jd.sub_hi > jd.sub_lo) {
     const uint64_t G = h->group;
     const uint64_t g_first = jd.sub_lo / G, g_end = (jd.sub_hi - 1) / G + 1;
-    const uint64_t n_groups = g_end - g_first;
-    const uint64_t warps = static_cast<uint64_t>(ctas_per_job) * (kBlock / 32);
-    const uint64_t w = static_cast<uint64_t>(part) * (kBlock / 32) + (threadIdx.x >> 5);
     const uint64_t lane = threadIdx.x & 31;
-    const uint64_t gw_lo = g_first + n_groups * w / warps, gw_hi = g_first + n_groups * (w + 1) / warps;
     uint8_t* coef_base = slot_base + kSlotBytes * kBlock;
     uint8_t* dp_base = coef_base + sizeof(int64_t) * kCoefEntries * kBlock;
     int64_t* fw = reinterpret_cast<int64_t*>(dp_base + dp_bytes_per_warp(h->n_nodes) * (threadIdx.x >> 5));
     int64_t* cw = fw + 32 * h->n_nodes;
     const int P = h->n_nodes - K;
-    for (uint64_t g = gw_lo; g < gw_hi; ++g) {
+    // Groups are dealt to warps dynamically (one 64-bit atomic per group):
+    // the exact slow path is data dependent, so a static split would leave
+    // warps idle at the end.
+    auto next_group = [&]() -> uint64_t {
+      unsigned long long x = 0;
+      if (lane == 0) x = atomicAdd(&sync[job].next_group, 1ull);
+      return g_first + __shfl_sync(0xffffffffu, x, 0);
+    };
+    for (uint64_t g = next_group(); g < g_end; g = next_group()) {
       // digits of nodes [0, P-1) shared by the group, and their folds
       int dtop[kMaxNodes];
       uint64_t x = g;
@@ -797,7 +822,7 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
   if (threadIdx.x == 0) {
     scratch[blockIdx.x] = b;
     __threadfence();
-    const unsigned t = atomicAdd(&tickets[job], 1u);
+    const unsigned t = atomicAdd(&sync[job].ticket, 1u);
     am_last = (t == static_cast<unsigned>(ctas_per_job - 1));
   }
   __syncthreads();
@@ -811,12 +836,13 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
     acc = block_best(acc, h, warp_slot);
     if (threadIdx.x == 0) {
       out[job] = acc;
-      tickets[job] = 0;
+      sync[job].ticket = 0;
+      sync[job].next_group = 0;
     }
   }
 }
 
-using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, unsigned*, Rec*, InnerParams);
+using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, JobSync*, Rec*, InnerParams);
 
 // pt: the innermost table comes from the kernel parameter (single-problem
 // launches); batch launches read it per job from shared memory.
@@ -1508,7 +1534,7 @@ struct loom_ctx {
   size_t jobs_cap = 0;
   Rec* d_scratch = nullptr;
   size_t scratch_cap = 0;
-  unsigned* d_tickets = nullptr;
+  JobSync* d_tickets = nullptr;
   size_t tickets_cap = 0;
   Rec* d_out = nullptr;
   size_t out_cap = 0;
@@ -1532,7 +1558,7 @@ struct loom_device_problem {
   uint8_t* d_blob = nullptr;
   JobDesc* d_job = nullptr;
   Rec* d_scratch = nullptr;
-  unsigned* d_ticket = nullptr;
+  JobSync* d_ticket = nullptr;
   Rec* d_out = nullptr;
   Rec* h_out = nullptr;
   int ctas = 0;
@@ -1568,8 +1594,8 @@ int ensure_tickets(loom_ctx* c, size_t need) {
   if (c->d_tickets) cudaFree(c->d_tickets);
   c->d_tickets = nullptr;
   c->tickets_cap = 0;
-  LOOM_CUDA(cudaMalloc(&c->d_tickets, std::max<size_t>(need, 1) * sizeof(unsigned)));
-  LOOM_CUDA(cudaMemset(c->d_tickets, 0, std::max<size_t>(need, 1) * sizeof(unsigned)));
+  LOOM_CUDA(cudaMalloc(&c->d_tickets, std::max<size_t>(need, 1) * sizeof(JobSync)));
+  LOOM_CUDA(cudaMemset(c->d_tickets, 0, std::max<size_t>(need, 1) * sizeof(JobSync)));
   c->tickets_cap = need;
   return LOOM_OK;
 }
@@ -1854,12 +1880,12 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
              cudaMalloc(&dp->d_scratch, sizeof(Rec) * ctas) == cudaSuccess &&
-             cudaMalloc(&dp->d_ticket, sizeof(unsigned)) == cudaSuccess &&
+             cudaMalloc(&dp->d_ticket, sizeof(JobSync)) == cudaSuccess &&
              cudaMalloc(&dp->d_out, sizeof(Rec)) == cudaSuccess && cudaMallocHost(&dp->h_out, sizeof(Rec)) == cudaSuccess &&
              cudaEventCreateWithFlags(&dp->done, cudaEventDisableTiming) == cudaSuccess &&
              cudaMemcpy(dp->d_blob, dp->built.blob.data(), dp->built.blob.size(), cudaMemcpyHostToDevice) ==
                  cudaSuccess &&
-             cudaMemset(dp->d_ticket, 0, sizeof(unsigned)) == cudaSuccess;
+             cudaMemset(dp->d_ticket, 0, sizeof(JobSync)) == cudaSuccess;
   if (!okk || set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)) != LOOM_OK) {
     loom_problem_release(dp);
     return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: upload failed");

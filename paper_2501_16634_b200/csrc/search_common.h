@@ -90,6 +90,15 @@ struct ParetoPoint {
   int32_t pad;
 };
 
+// Per-job device counters (global memory, zero between launches): the CTA
+// arrival ticket of the final reduction and the next DP group to deal out.
+// The last CTA to arrive resets both.
+struct alignas(16) JobSync {
+  unsigned ticket;
+  unsigned pad;
+  unsigned long long next_group;
+};
+
 // Per-job launch descriptor (global memory).
 struct JobDesc {
   uint64_t blob_off;     // byte offset in the blob arena
