@@ -2,6 +2,9 @@
 travels with the gpurun snapshot; no JIT cache is involved.
 
     python -m paper_2501_16634_b200.build [--force]
+    python -m paper_2501_16634_b200.build --variant NAME -DMACRO=V ...
+        (experiment builds: _build/variants/NAME/libloom_b200.so, loaded by
+        loom.py when LOOM_B200_LIB points at it)
 """
 from __future__ import annotations
 
@@ -43,28 +46,36 @@ def _stale(out: Path, deps: list[Path]) -> bool:
     return not out.exists() or any(d.stat().st_mtime > out.stat().st_mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: list[str] | None = None) -> Path:
     OBJ.mkdir(exist_ok=True)
+    defines = defines or []
+    cu_obj = OBJ if variant is None else OBJ / "variants" / variant
+    lib = LIB if variant is None else cu_obj / "libloom_b200.so"
+    cu_obj.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.hpp")) + list((ROOT / "include").rglob("*.h*"))
     log: list[str] = []
     objs = []
     for src in CU_SOURCES:
-        o = OBJ / (src + ".o")
-        if force or _stale(o, [CSRC / src, *headers]):
-            _run([NVCC, *CU_FLAGS, "-c", str(CSRC / src), "-o", str(o)], log)
+        o = cu_obj / (src + ".o")
+        if force or variant is not None or _stale(o, [CSRC / src, *headers]):
+            _run([NVCC, *CU_FLAGS, *defines, "-c", str(CSRC / src), "-o", str(o)], log)
         objs.append(o)
     for src in CXX_SOURCES:
         o = OBJ / (src + ".o")
         if force or _stale(o, [CSRC / src, *headers]):
             _run(["g++", *CXX_FLAGS, "-c", str(CSRC / src), "-o", str(o)], log)
         objs.append(o)
-    if force or _stale(LIB, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", str(LIB), *map(str, objs), "-lpthread"], log)
+    if force or _stale(lib, objs):
+        _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lpthread"], log)
     if verbose:
         print("\n".join(log))
-    (OBJ / "build.log").write_text("\n".join(log))
-    return LIB
+    (cu_obj / "build.log").write_text("\n".join(log))
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    argv = sys.argv[1:]
+    var = argv[argv.index("--variant") + 1] if "--variant" in argv else None
+    build(force="--force" in argv, verbose=var is None, variant=var,
+          defines=[a for a in argv if a.startswith("-D")])

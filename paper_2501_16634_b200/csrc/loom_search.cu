@@ -58,6 +58,11 @@ namespace {
 
 constexpr int64_t kNeg = -(int64_t(1) << 62);
 
+#ifndef LOOM_PAIR_UNROLL
+#define LOOM_PAIR_UNROLL 2
+#endif
+constexpr int kPairUnroll = LOOM_PAIR_UNROLL;
+
 // ---------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------
@@ -504,7 +509,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
         const int c_hi = min(o_hi, c_lo + 64);
         uint32_t hits = 0, bit = 1;
         int o = c_lo;
-#pragma unroll 2
+#pragma unroll kPairUnroll
         for (; o + 1 < c_hi; o += 2, bit <<= 1) {
           const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
           const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);

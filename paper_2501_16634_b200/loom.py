@@ -10,13 +10,15 @@ device calls raise DeviceError without an sm_100 GPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import json
 from dataclasses import dataclass
 from pathlib import Path
 from typing import Any, Sequence
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libloom_b200.so"
+# LOOM_B200_LIB: an experiment build of the same library (build.py --variant)
+LIB_PATH = Path(os.environ["LOOM_B200_LIB"]) if os.environ.get("LOOM_B200_LIB") else PKG / "libloom_b200.so"
 
 LOOM_OK, LOOM_INFEASIBLE, LOOM_INVALID, LOOM_DEVICE_ERROR = 0, 1, 2, 3
 CRITERIA = {"min_cost_dollars": 0, "min_energy": 1, "min_latency": 2, "max_quality": 3}

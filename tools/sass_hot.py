@@ -9,7 +9,8 @@ from pathlib import Path
 
 K, P, NV = sys.argv[1:4]
 PT = sys.argv[4] if len(sys.argv) > 4 else "1"
-obj = Path(__file__).resolve().parents[1] / "paper_2501_16634_b200" / "_build" / "loom_search.cu.o"
+import os
+obj = Path(os.path.abspath(os.environ.get("SASS_OBJ")) if os.environ.get("SASS_OBJ") else Path(__file__).resolve().parents[1] / "paper_2501_16634_b200" / "_build" / "loom_search.cu.o")
 with tempfile.TemporaryDirectory() as td:
     subprocess.run(["cuobjdump", "-xelf", "all", str(obj)], cwd=td, capture_output=True)
     cubin = next(Path(td).glob("*.cubin"))
