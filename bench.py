@@ -279,9 +279,15 @@ def b200_arm(args) -> None:
         f_mhz = clk["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)
         props = torch.cuda.get_device_properties(local)
         sms = props.multi_processor_count
-        inst_per_plan = ISSUE_INSTR_PER_PLAN
-        issue_peak = sms * 4 * 32 * f_mhz * 1e6 / 1e12  # Tinst/s (thread instructions)
-        achieved = (total / world) / (local_ms / 1e3) * inst_per_plan / 1e12
+        # Instruction-bound roofline of the compiled fast path:
+        # per 32 plans (one warp, one plan per lane) the SMSP spends
+        # max(issue slots, 2 x ALU-pipe instructions, 2 x FP64-pipe
+        # instructions) cycles -- both pipes retire 16 lanes per clock.
+        fp = FAST_PATH
+        cyc_per_plan = max(fp["issue"], 2 * fp["alu"], 2 * fp["fp64"]) / fp["plans_per_lane"]
+        bound_pipe = max((fp["issue"], "issue"), (2 * fp["alu"], "alu"), (2 * fp["fp64"], "fp64"))[1]
+        peak_plans = sms * 4 * 32 * f_mhz * 1e6 / cyc_per_plan
+        achieved = (total / world) / (local_ms / 1e3)
         traffic = None
         prof = ROOT / "profiles" / "ncu_summary.json"
         if prof.exists():
@@ -300,17 +306,20 @@ def b200_arm(args) -> None:
                     "h2d_bytes_per_step": dp.image_bytes + 64, "d2h_bytes_per_step": 64,
                     "path": "loom_exhaustive_search_json: JSON parse + lowering + H2D + kernel + D2H + decode"
                     if world == 1 else "lowering + loom_search_argmin(shard) + NCCL all-gather + reduce + decode"},
-            "roofline": {"bound": "issue", "achieved": achieved, "peak": issue_peak, "unit": "Tinst/s",
-                         "frac": achieved / issue_peak, "traffic": traffic,
-                         "inst_per_plan": inst_per_plan,
-                         "note": "thread-instructions per plan of the compiled inner loop (DESIGN.md §5); "
-                                 f"peak = {sms} SMs x 4 issue/clk x 32 lanes x measured SM clock"},
+            "roofline": {"bound": f"instruction ({bound_pipe} pipe)", "achieved": achieved, "peak": peak_plans,
+                         "unit": "plans/s per GPU", "frac": achieved / peak_plans, "traffic": traffic,
+                         "inst_per_plan": fp["issue"] / fp["plans_per_lane"],
+                         "cycles_per_plan": cyc_per_plan,
+                         "note": "peak = SMs x 4 SMSPs x 32 lanes x measured SM clock / SMSP cycles per plan of "
+                                 f"the compiled fast path ({fp['issue']} instructions, {fp['alu']} ALU-pipe, "
+                                 f"{fp['fp64']} FP64-pipe per {fp['plans_per_lane']} plans per lane; both pipes take "
+                                 "2 cycles per warp instruction); traffic = DRAM bytes per launch (ncu)"},
             "gpu_launches": launches,
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
-        if args.configs:
+        if not args.no_configs and world == 1:
             line["configs"] = other_configs(ctx, loom, W)
         print(json.dumps(line), flush=True)
     dp.close()
@@ -320,11 +329,11 @@ def b200_arm(args) -> None:
 
 
 # Compiled fast path of the innermost contexts of search_kernel<4, kPrimFp,
-# 16, true> (tools/sass_hot.py 4 0 16 1): 271 SASS instructions per 64 plans
-# (two unrolled two-context steps) -- 68 DADD, 64 DSETP, 69 ISETP, 32 PLOP3,
-# 12 LDCU, loads / loop control.
-# DESIGN.md §5.
-ISSUE_INSTR_PER_PLAN = 271 / 64
+# 16, true> (tools/sass_hot.py 4 0 16 1): per 64 plans per lane (two
+# unrolled two-context steps), 211 SASS instructions -- 64 DSETP, 69 ISETP,
+# 32 PLOP3, 12 LDCU, 8 LDS, 8 DADD, loop control -- of which 112 run on the
+# ALU pipe and 72 on the FP64 pipe.  DESIGN.md §5.
+FAST_PATH = {"issue": 211, "alu": 112, "fp64": 72, "plans_per_lane": 64}
 
 
 def other_configs(ctx, loom, W) -> dict:
@@ -384,7 +393,8 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--configs", action="store_true", help="also report time-to-plan for C1/C2/C4")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the time-to-plan lines of C1/C2/C4/C5 and C3 greedy")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

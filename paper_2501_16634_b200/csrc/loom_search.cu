@@ -363,14 +363,24 @@ struct Hot {
   int od[4];
   uint64_t s_index;  // subrow index (row * radix[P] + o0)
   double hi;         // thresholds mirrored from the shared slot
+  double hi_up;      // the double above hi (see ctx_bound)
   int64_t lat_s;
   int32_t bq;
 };
+
+// The double above x (x itself for +inf).
+__device__ __forceinline__ double next_up(double x) {
+  if (x == INFINITY || x != x) return x;
+  if (x == 0.0) return __longlong_as_double(1);
+  const long long b = __double_as_longlong(x);
+  return __longlong_as_double(x > 0 ? b + 1 : b - 1);
+}
 
 __device__ __forceinline__ void reload(Hot& H) {
   const Slots s = make_slots(H.slot_base);
   const int t = threadIdx.x;
   H.hi = s.hi[t];
+  H.hi_up = next_up(H.hi);
   H.lat_s = s.lat_s[t];
   H.bq = s.bq[t];
 }
@@ -432,6 +442,13 @@ struct Inner {
     return (w_ <= tw) & (min(qv, q_) >= H.bq);
   }
 
+  // The fast loop's per-plan test: both criteria compared in the innermost
+  // option's own table domain against per-context bounds (see ctx_bound).
+  __device__ __forceinline__ bool pass_bound(int32_t w_, double g_, int32_t tw, double tu) const {
+    if (PRIM == kPrimFp) return (w_ <= tw) & (g_ <= tu);
+    return w_ <= tw;
+  }
+
   // NV > 0: does any plan of the context pass?  (one predicate OR per plan)
   __device__ __forceinline__ bool any_pass(const Hot& H, const InnerParams& ip, int32_t tw, double ea,
                                            int32_t qv) const {
@@ -453,6 +470,20 @@ struct Inner {
 // J = 1 .. K-2: the input vector of level J (2^(K-J) int64 entries) sits at
 // column offset sum_{1<=j<J} 2^(K-j), entry S at [S * kBlock + tid] (conflict
 // free).  Level 0's vector (read once per subrow) lives in local memory.
+// Per-context energy bound in the innermost option's table domain.  A plan
+// of the context has energy fl(eu + g) (the dag-order fold's last term,
+// estimator.hpp:50-60) and passes the energy test iff fl(eu + g) <= hi.  If
+// fl(x) <= hi under round-to-nearest then x <= hi + (hi_up - hi) / 2, where
+// hi_up is the double above hi, so every passing g satisfies
+//   g <= hi_up - eu <= tu = round_up(hi_up - eu).
+// The fast loop therefore tests g <= tu per plan (one compare, no add) and
+// lets through a superset of the passing plans: at most those whose g lies
+// within about one ulp of the exact bound.  Survivors are re-tested exactly
+// (fl(eu + g) <= hi) in slow_scan, so the selected plan is unchanged.
+// Latency is handled the same way: w <= tw (inner_tw) is the exact latency
+// test of the plan, expressed on the option's own wall.
+__device__ __forceinline__ double ctx_bound(const Hot& H, double eu) { return __dadd_ru(H.hi_up, -eu); }
+
 template <int K>
 __device__ __forceinline__ int64_t* coef_col(uint8_t* coef_base, int J) {
   int off = 0;
@@ -514,11 +545,12 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
           const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
           const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
           const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
+          const double tu0 = ctx_bound(H, eu0), tu1 = ctx_bound(H, eu1);
           bool a = false;
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
-            a |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw0, eu0, INT_MAX);
-            a |= in.pass(H, in.W(ip, j), in.G(ip, j), 0, tw1, eu1, INT_MAX);
+            a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw0, tu0);
+            a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw1, tu1);
           }
           // a real (rarely taken) branch keeps the per-plan tests a predicate
           // OR chain; the empty asm stops if-conversion into per-plan selects

@@ -42,5 +42,10 @@ for sec in re.split(r"\n\s*\.section\s+\.text\.", sass)[1:]:
     ops = [l.split()[1] if l.startswith("@") else (l.split()[1] if l.startswith("/*") else l.split()[0])
            for l in body if not l.startswith(".L_x")]
     from collections import Counter
-    print(len(ops), Counter(o.split(".")[0] for o in ops).most_common())
+    cnt = Counter(o.split(".")[0] for o in ops)
+    print(len(ops), cnt.most_common())
+    # pipes at 16 lanes/clk/SMSP (2 issue cycles per warp instruction)
+    fp64 = sum(cnt[o] for o in ("DADD", "DSETP", "DMUL", "DFMA", "DMNMX"))
+    alu = sum(cnt[o] for o in ("ISETP", "PLOP3", "SEL", "LOP3", "IADD3", "VIADDMNMX", "VIADD", "SHF", "LEA", "IMNMX"))
+    print(f"issue {len(ops)}  alu {alu} ({2 * alu} cycles)  fp64 {fp64} ({2 * fp64} cycles)")
     break
