@@ -184,6 +184,19 @@ int loom_search_argmin_batch(loom_ctx* ctx, const loom_problem* problems,
                              const loom_objective* objectives, int32_t n_jobs,
                              loom_winner* out, int32_t* status);
 
+/* Multi-tenant batch on lowered handles (config 4): one objective for every
+ * job; a NULL handle gets status LOOM_INVALID.  No per-job marshalling. */
+int loom_search_argmin_lowered(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n,
+                               const loom_objective* objective, loom_winner* out, int32_t* status);
+
+/* The whole multi-tenant call on reference-format JSON: n DAGs against one
+ * library bundle, bounds and objective -> n winners (a loop of
+ * exhaustive_search, optimizer.hpp:173-188, with lowering on `threads` host
+ * threads and one batched device search).  status[i] is the job's status. */
+int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const char* bounds_json,
+                                 const char* const* dag_jsons, int32_t n, const char* objective_json,
+                                 int32_t threads, loom_winner* out, int32_t* status);
+
 /* Resident problems: upload once, search many times (bench "value" path). */
 int loom_problem_upload(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
                         loom_device_problem** out);

@@ -117,9 +117,10 @@ class AgentLibrary {
 
  private:
   std::map<std::string, bool> capabilities_;
-  std::map<std::string, HardwareSku> skus_;
-  std::map<std::string, Implementation> impls_;
-  std::map<std::tuple<std::string, std::string, int>, ExecutionProfile> profiles_;
+  // std::less<>: heterogeneous lookup (no key copies on the lowering path)
+  std::map<std::string, HardwareSku, std::less<>> skus_;
+  std::map<std::string, Implementation, std::less<>> impls_;
+  std::map<std::tuple<std::string, std::string, int>, ExecutionProfile, std::less<>> profiles_;
 };
 
 // ---- dag + objective (workflow.hpp:67-106, 259-301) ---------------------

@@ -1,5 +1,7 @@
 #include "json.hpp"
 
+#include <charconv>
+
 #include <cerrno>
 #include <cmath>
 #include <cstdio>
@@ -129,6 +131,15 @@ class Parser {
   }
   std::string string() {
     ++p_;  // opening quote
+    // fast path: no escapes before the closing quote
+    for (std::size_t q = p_; q < n_; ++q) {
+      if (s_[q] == '"') {
+        std::string out(s_ + p_, q - p_);
+        p_ = q + 1;
+        return out;
+      }
+      if (s_[q] == '\\') break;
+    }
     std::string out;
     while (p_ < n_) {
       const char c = s_[p_++];
@@ -171,16 +182,21 @@ class Parser {
       break;
     }
     if (p_ == start) fail("unexpected character");
-    const std::string tok(s_ + start, p_ - start);
+    // std::from_chars: correctly rounded, locale independent, no copy
+    const char* b = s_ + start;
+    const char* e = s_ + p_;
     if (!is_real) {
-      errno = 0;
-      char* end = nullptr;
-      const long long v = std::strtoll(tok.c_str(), &end, 10);
-      if (errno == 0 && end && *end == '\0') return Value::make_int(v);
+      long long v = 0;
+      const auto r = std::from_chars(b, e, v);
+      if (r.ec == std::errc() && r.ptr == e) return Value::make_int(v);
     }
-    char* end = nullptr;
-    const double d = std::strtod(tok.c_str(), &end);
-    if (!end || *end != '\0') fail("bad number '" + tok + "'");
+    double d = 0.0;
+    const auto r = std::from_chars(b, e, d);
+    if (r.ec == std::errc::result_out_of_range && r.ptr == e) {  // +-inf / 0 like strtod
+      const std::string tok(b, e);
+      return Value::make_real(std::strtod(tok.c_str(), nullptr));
+    }
+    if (r.ec != std::errc() || r.ptr != e) fail("bad number '" + std::string(b, e) + "'");
     return Value::make_real(d);
   }
 

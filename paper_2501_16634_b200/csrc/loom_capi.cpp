@@ -508,6 +508,52 @@ int loom_lower_batch(const char* library_json, const char* bounds_json, const ch
 
 const loom_problem* loom_lowered_problem(const loom_lowered* lw) { return lw ? &lw->view : nullptr; }
 
+int loom_search_argmin_lowered(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n,
+                               const loom_objective* objective, loom_winner* out, int32_t* status) {
+  if (!ctx || (n > 0 && (!lowered || !out || !status)) || !objective || n < 0)
+    return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  // only the lowered jobs go to the device; the rest keep LOOM_INVALID
+  std::vector<int> idx;
+  std::vector<loom_problem> probs;
+  for (int i = 0; i < n; ++i) {
+    std::memset(&out[i], 0, sizeof out[i]);
+    status[i] = LOOM_INVALID;
+    if (lowered[i]) {
+      idx.push_back(i);
+      probs.push_back(lowered[i]->view);
+    }
+  }
+  const int m = static_cast<int>(idx.size());
+  std::vector<loom_objective> objs(m, *objective);
+  std::vector<loom_winner> w(m);
+  std::vector<int32_t> st(m, LOOM_OK);
+  const int rc = loom_search_argmin_batch(ctx, probs.data(), objs.data(), m, w.data(), st.data());
+  for (int k = 0; k < m; ++k) {
+    out[idx[k]] = w[k];
+    status[idx[k]] = st[k];
+  }
+  return rc;
+}
+
+int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const char* bounds_json,
+                                 const char* const* dag_jsons, int32_t n, const char* objective_json,
+                                 int32_t threads, loom_winner* out, int32_t* status) {
+  if (!ctx || !objective_json || (n > 0 && (!out || !status)) || n < 0)
+    return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  loom_objective obj;
+  if (int rc = loom_objective_parse(objective_json, &obj)) return rc;
+  std::vector<loom_lowered*> lw(n, nullptr);
+  std::vector<int32_t> lst(n, LOOM_OK);
+  int rc = loom_lower_batch(library_json, bounds_json, dag_jsons, n, threads, lw.data(), lst.data());
+  if (rc == LOOM_OK) {
+    rc = loom_search_argmin_lowered(ctx, lw.data(), n, &obj, out, status);
+    for (int i = 0; i < n; ++i)
+      if (lst[i] != LOOM_OK) status[i] = lst[i];
+  }
+  for (loom_lowered* h : lw) loom_lowered_destroy(h);
+  return rc;
+}
+
 int loom_lowered_config_json(const loom_lowered* lw, uint64_t plan_index, char* buf, size_t cap, size_t* needed) {
   if (!lw) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null lowered");
   if (plan_index >= lw->L.total) return loomi::fail(LOOM_INVALID, "InvalidConfigError: plan index out of range");

@@ -162,7 +162,7 @@ const Implementation* AgentLibrary::implementation(const std::string& name) cons
   return it == impls_.end() ? nullptr : &it->second;
 }
 const ExecutionProfile* AgentLibrary::profile(const std::string& impl, const std::string& sku, int units) const {
-  auto it = profiles_.find(std::make_tuple(impl, sku, units));
+  auto it = profiles_.find(std::forward_as_tuple(impl, sku, units));
   return it == profiles_.end() ? nullptr : &it->second;
 }
 
@@ -182,7 +182,8 @@ std::vector<const ExecutionProfile*> AgentLibrary::profiles_for(const std::strin
   std::vector<const ExecutionProfile*> out;
   // The map key is (implementation, sku, units): start at the first key of
   // this implementation and walk while it matches.
-  for (auto it = profiles_.lower_bound(std::make_tuple(implementation, std::string(), INT_MIN));
+  static const std::string kEmpty;
+  for (auto it = profiles_.lower_bound(std::forward_as_tuple(implementation, kEmpty, INT_MIN));
        it != profiles_.end() && std::get<0>(it->first) == implementation; ++it)
     out.push_back(&it->second);
   return out;
@@ -344,18 +345,18 @@ int node_quality(const DagNode& node, const Implementation& impl, int path_count
 }
 
 NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const AgentLibrary& library) {
-  const std::string where = "node '" + node.id + "'";
+  const auto where = [&] { return "node '" + node.id + "'"; };  // only built on error
   const Implementation* impl = library.implementation(a.implementation);
-  if (!impl) throw InvalidConfigError(where + ": unknown implementation '" + a.implementation + "'");
+  if (!impl) throw InvalidConfigError(where() + ": unknown implementation '" + a.implementation + "'");
   if (impl->capability != node.capability)
-    throw InvalidConfigError(where + ": implementation '" + impl->name + "' realizes '" + impl->capability +
+    throw InvalidConfigError(where() + ": implementation '" + impl->name + "' realizes '" + impl->capability +
                              "', not '" + node.capability + "'");
-  if (a.placements.empty()) throw InvalidConfigError(where + ": no placements");
-  if (a.path_count < 1) throw InvalidConfigError(where + ": path_count must be >= 1");
+  if (a.placements.empty()) throw InvalidConfigError(where() + ": no placements");
+  if (a.path_count < 1) throw InvalidConfigError(where() + ": path_count must be >= 1");
   if (a.path_count > 1 && !node.multi_path)
-    throw InvalidConfigError(where + " is not flagged multi-path in the lexicon");
+    throw InvalidConfigError(where() + " is not flagged multi-path in the lexicon");
   const int fan = a.fan_out();
-  if (fan > 1 && !node.splittable) throw InvalidConfigError(where + " is not splittable; fan-out must be 1");
+  if (fan > 1 && !node.splittable) throw InvalidConfigError(where() + " is not splittable; fan-out must be 1");
 
   struct Worker {
     const ExecutionProfile* profile;
@@ -364,16 +365,16 @@ NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const
   std::vector<Worker> workers;
   for (const Placement& p : a.placements) {
     const HardwareSku* sku = library.sku(p.sku);
-    if (!sku) throw InvalidConfigError(where + ": unknown sku '" + p.sku + "'");
+    if (!sku) throw InvalidConfigError(where() + ": unknown sku '" + p.sku + "'");
     if (!impl->supports(sku->hardware_class))
-      throw InvalidConfigError(where + ": implementation '" + impl->name + "' does not support " +
+      throw InvalidConfigError(where() + ": implementation '" + impl->name + "' does not support " +
                                (sku->hardware_class == HardwareClass::gpu ? "gpu" : "cpu") + " sku '" +
                                sku->id + "'");
     const ExecutionProfile* prof = library.profile(impl->name, sku->id, p.units);
     if (!prof)
-      throw InvalidConfigError(where + ": no profile for (" + impl->name + ", " + sku->id + ", " +
+      throw InvalidConfigError(where() + ": no profile for (" + impl->name + ", " + sku->id + ", " +
                                std::to_string(p.units) + ")");
-    if (p.workers < 1) throw InvalidConfigError(where + ": workers must be >= 1");
+    if (p.workers < 1) throw InvalidConfigError(where() + ": workers must be >= 1");
     for (int w = 0; w < p.workers; ++w) workers.push_back({prof, sku});
   }
 
@@ -383,7 +384,7 @@ NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const
   } else if (a.placements.size() <= 1) {
     chunk = equal_split(node.work_units, fan, node.min_chunk);
     if (static_cast<int>(chunk.size()) != fan)
-      throw InvalidConfigError(where + ": fan-out " + std::to_string(fan) + " exceeds the chunk capacity of " +
+      throw InvalidConfigError(where() + ": fan-out " + std::to_string(fan) + " exceeds the chunk capacity of " +
                                std::to_string(chunk_capacity(node.work_units, node.min_chunk)));
   } else {
     std::vector<double> speeds;
@@ -391,7 +392,7 @@ NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const
     chunk = water_fill_split(node.work_units, node.min_chunk, speeds);
     for (double c : chunk)
       if (c <= 0.0 && node.work_units > 0.0)
-        throw InvalidConfigError(where + ": degenerate hybrid placement; a worker receives no work");
+        throw InvalidConfigError(where() + ": degenerate hybrid placement; a worker receives no work");
   }
 
   NodePlan plan;

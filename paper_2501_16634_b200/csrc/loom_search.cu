@@ -37,6 +37,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <climits>
 #include <cstdio>
@@ -1318,6 +1320,10 @@ int align16(int x) { return (x + 15) & ~15; }
 int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_threads, Built& b) {
   uint64_t total = 0;
   if (int rc = loomi::check_problem(p, &total)) return rc;
+  if (total == 0) {  // empty dag or a node without options: nothing to search (optimizer.hpp:117-120)
+    b = Built{};
+    return LOOM_OK;
+  }
   const int n = p->n_nodes;
   if (n > kMaxNodes) return loomi::fail(LOOM_INVALID, "InvalidConfigError: more than 32 dag nodes");
   if (p->n_edges > kMaxEdges) return loomi::fail(LOOM_INVALID, "InvalidConfigError: more than 512 dag edges");
@@ -1680,6 +1686,39 @@ void winner_from_rec(const Rec& r, loom_winner* w) {
   w->quality = r.qual;
 }
 
+// Host work over many jobs on up to 32 threads (small batches stay inline).
+template <class F>
+void parallel_for(int n, F&& f) {
+  const int t = n < 64 ? 1 : static_cast<int>(std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency())));
+  if (t <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::atomic<int> next{0};
+  for (int w = 0; w < t; ++w)
+    pool.emplace_back([&] {
+      for (int i; (i = next.fetch_add(64)) < n;)
+        for (int k = i; k < std::min(n, i + 64); ++k) f(k);
+    });
+  for (auto& th : pool) th.join();
+}
+
+// LOOM_TRACE=1: phase timings of the host side of a call on stderr.
+struct Trace {
+  const char* name;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  explicit Trace(const char* n) : name(n), on(std::getenv("LOOM_TRACE") != nullptr), t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[loom trace] %s %s %.3f ms\n", name, what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
 int finish_winner(const loom_problem* p, const Rec& r, loom_winner* out) {
   winner_from_rec(r, out);
   if (!r.found)
@@ -1789,10 +1828,11 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   if (n_jobs == 0) return LOOM_OK;
   LOOM_CUDA(cudaSetDevice(c->device));
-  // Build every image; group jobs by kernel instantiation.
+  Trace tr("argmin_batch");
+  // Build every image (host threads); group jobs by kernel instantiation.
   std::vector<Built> built(n_jobs);
   std::vector<int> ok(n_jobs, 0);
-  for (int j = 0; j < n_jobs; ++j) {
+  parallel_for(n_jobs, [&](int j) {
     std::memset(&out[j], 0, sizeof out[j]);
     int rc = build_image(&problems[j], &objectives[j], kBlock, built[j]);
     if (rc == LOOM_OK && built[j].total == 0) {
@@ -1800,7 +1840,8 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
     }
     if (status) status[j] = rc;
     ok[j] = rc == LOOM_OK;
-  }
+  });
+  tr.mark("build_images");
   struct Group {
     KernelFn fn;
     std::vector<int> jobs;
@@ -1829,10 +1870,10 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
       arena += built[j].blob.size();
     }
   std::vector<uint8_t> host_arena(arena);
-  std::vector<JobDesc> descs;
-  descs.reserve(n_jobs);
-  for (int j = 0; j < n_jobs; ++j)
+  parallel_for(n_jobs, [&](int j) {
     if (ok[j]) std::memcpy(host_arena.data() + off[j], built[j].blob.data(), built[j].blob.size());
+  });
+  tr.mark("pack");
   if (int rc = ensure(c->d_arena, c->arena_cap, arena)) return rc;
   if (int rc = ensure(c->d_jobs, c->jobs_cap, static_cast<size_t>(n_jobs))) return rc;
   if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(n_jobs))) return rc;
@@ -1861,12 +1902,17 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
   }
   LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, all.size() * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
-  size_t k = 0;
+  tr.mark("device");
+  std::vector<std::pair<int, size_t>> order;  // (job, slot in h_out)
+  order.reserve(all.size());
   for (auto& g : groups)
-    for (int j : g.jobs) {
-      const int rc = finish_winner(&problems[j], c->h_out[k++], &out[j]);
-      if (status) status[j] = rc;
-    }
+    for (int j : g.jobs) order.emplace_back(j, order.size());
+  parallel_for(static_cast<int>(order.size()), [&](int i) {
+    const int j = order[i].first;
+    const int rc = finish_winner(&problems[j], c->h_out[order[i].second], &out[j]);
+    if (status) status[j] = rc;
+  });
+  tr.mark("finish");
   return LOOM_OK;
 }
 

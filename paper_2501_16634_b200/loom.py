@@ -158,6 +158,9 @@ def lib() -> C.CDLL:
         "loom_search_argmin": ([vp, P, O, C.c_uint64, C.c_uint64, W], C.c_int),
         "loom_search_argmin_algo": ([vp, P, O, C.c_uint64, C.c_uint64, C.c_int32, W], C.c_int),
         "loom_search_argmin_batch": ([vp, P, O, C.c_int32, W, C.POINTER(C.c_int32)], C.c_int),
+        "loom_search_argmin_lowered": ([vp, C.POINTER(vp), C.c_int32, O, W, C.POINTER(C.c_int32)], C.c_int),
+        "loom_exhaustive_search_batch": ([vp, C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p), C.c_int32, C.c_char_p,
+                                          C.c_int32, W, C.POINTER(C.c_int32)], C.c_int),
         "loom_problem_upload": ([vp, P, O, C.POINTER(vp)], C.c_int),
         "loom_problem_release": ([vp], C.c_int),
         "loom_search_argmin_async": ([vp, vp, C.c_uint64, C.c_uint64], C.c_int),
@@ -224,12 +227,13 @@ class Lowered:
         else:
             h = _handle
         self._h = h
+        self._owned = True
         self.problem: Problem = lib().loom_lowered_problem(h).contents
 
     def close(self) -> None:
-        if self._h:
+        if self._h and self._owned:
             lib().loom_lowered_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -293,6 +297,85 @@ def lower_batch(dags: Sequence[Any], library: Any, bounds: Any, threads: int = 0
         if st[i] != LOOM_OK:
             _raise(st[i], f"job {i}: " + last_error())
         res.append(Lowered(None, None, None, _handle=C.c_void_p(out[i])))
+    return res
+
+
+class LoweredBatch:
+    """Many lowered DAGs as one array of C handles (config 4): no per-job
+    Python objects on the batch path.  batch[i] is a non-owning view."""
+
+    def __init__(self, dags: Sequence[Any], library: Any, bounds: Any, threads: int = 0):
+        n = len(dags)
+        self.n = n
+        texts = [_text(d) for d in dags]
+        arr = (C.c_char_p * max(1, n))(*texts)
+        self.handles = (C.c_void_p * max(1, n))()
+        self.status = (C.c_int32 * max(1, n))()
+        _check(lib().loom_lower_batch(_text(library), _text(bounds), arr, n, threads, self.handles, self.status))
+
+    def __len__(self) -> int:
+        return self.n
+
+    def __getitem__(self, i: int) -> "Lowered":
+        if self.status[i] != LOOM_OK:
+            _raise(self.status[i], f"job {i} was not lowered")
+        v = Lowered.__new__(Lowered)
+        v._h = C.c_void_p(self.handles[i])
+        v._owned = False  # the batch destroys its handles
+        v.problem = lib().loom_lowered_problem(v._h).contents
+        return v
+
+    def close(self) -> None:
+        if self.handles is not None:
+            for i in range(self.n):
+                if self.handles[i]:
+                    lib().loom_lowered_destroy(self.handles[i])
+            self.handles = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class BatchResult:
+    """Per-job winners of a multi-tenant batch, kept in the C arrays the
+    library filled (decoded to dicts only on request)."""
+
+    def __init__(self, n: int):
+        self.n = n
+        self.winners = (Winner * max(1, n))()
+        self.status = (C.c_int32 * max(1, n))()
+
+    def __len__(self) -> int:
+        return self.n
+
+    def __getitem__(self, i: int) -> tuple[int, dict]:
+        return self.status[i], self.winners[i].as_dict()
+
+    def feasible(self) -> int:
+        return sum(1 for i in range(self.n) if self.status[i] == LOOM_OK)
+
+
+def search_lowered_batch(ctx: "Context", batch: LoweredBatch, obj: Objective) -> BatchResult:
+    """Per-job argmin of every lowered DAG of the batch under one objective."""
+    res = BatchResult(batch.n)
+    _check(lib().loom_search_argmin_lowered(ctx.handle, batch.handles, batch.n, C.byref(obj), res.winners,
+                                            res.status))
+    return res
+
+
+def exhaustive_search_batch(dags: Sequence[Any], library: Any, objective: Any, bounds: Any, *,
+                            ctx: "Context", threads: int = 0) -> BatchResult:
+    """The multi-tenant call on reference-format JSON: exhaustive_search
+    (optimizer.hpp:173-188) for every DAG against one library, objective and
+    bounds, lowered on host threads and searched in one batched launch."""
+    n = len(dags)
+    arr = (C.c_char_p * max(1, n))(*[_text(d) for d in dags])
+    res = BatchResult(n)
+    _check(lib().loom_exhaustive_search_batch(ctx.handle, _text(library), _text(bounds), arr, n, _text(objective),
+                                              threads, res.winners, res.status))
     return res
 
 

@@ -4,6 +4,8 @@ bar is bit-exact: same selected plan (identifier / plan index), same integer
 latency and quality, bit-identical doubles."""
 import random
 
+import json
+
 import pytest
 
 from conftest import cpu_threads
@@ -203,6 +205,28 @@ def test_c4_batch(ctx, golden):
         elif k < 40:
             p = O.problem(jobs[k].dag, jobs[k].library, jobs[k].bounds)
             _check_oracle(got, O.argmin(p, jobs[k].objective, threads=cpu_threads()))
+
+
+def test_c4_batch_json_and_lowered(ctx, golden):
+    """The multi-tenant entry points (one JSON call; lowered handles + one
+    objective) return exactly the per-job batch results, which are pinned to
+    the reference goldens above.  Includes an invalid DAG (per-job status)."""
+    gold = golden("c4/jobs.json")["jobs"]
+    jobs = W.config4(64)
+    dags = [j.dag for j in jobs] + [{"nodes": [{"id": "x"}], "edges": []}, {"nodes": [], "edges": []}]
+    lib_t, bounds_t = json.dumps(jobs[0].library), json.dumps(jobs[0].bounds)
+    res = loom.exhaustive_search_batch(dags, lib_t, jobs[0].objective, bounds_t, ctx=ctx)
+    assert len(res) == 66 and res.feasible() == 64
+    assert res.status[64] == loom.LOOM_INVALID and res.status[65] == loom.LOOM_INFEASIBLE
+    batch = loom.LoweredBatch(dags[:64], lib_t, bounds_t)
+    res2 = loom.search_lowered_batch(ctx, batch, loom.objective(jobs[0].objective))
+    per_job = loom.search_argmin_batch(ctx, [batch[k].problem for k in range(64)],
+                                       [loom.objective(j.objective) for j in jobs])
+    for k in range(64):
+        assert res[k] == res2[k] == per_job[k]
+        if str(k) in gold:
+            _check_ref(res[k][1], gold[str(k)]["result"], batch[k])
+    batch.close()
 
 
 def test_resident_problem_async(ctx):
