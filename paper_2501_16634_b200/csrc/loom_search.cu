@@ -45,6 +45,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <queue>
 #include <string>
@@ -1029,128 +1030,194 @@ __device__ __forceinline__ GuardView load_guard(uint8_t* s, const ParetoPoint* g
 
 constexpr size_t kGuardBytes = static_cast<size_t>(kGuardMax) * (8 + 8 + 8 + 4);
 
-// Phase 1 over [begin, end): rows = all digits but the last two fixed.
+// Is the (uniform) point dominated by a guard point?  The warp splits the
+// guard: lane l tests points l, l + 32, ...
+__device__ __forceinline__ bool guarded_warp(const GuardView& g, double d, double e, int64_t l, int32_t q) {
+  bool hit = false;
+  for (int k = threadIdx.x & 31; k < g.n && !hit; k += 32) hit = dominates(g.d[k], g.e[k], g.l[k], g.q[k], d, e, l, q);
+  return __any_sync(0xffffffffu, hit);
+}
+
+// Per-warp shared scratch of the Pareto evaluation: warp_dp's f[n][32] and
+// c[32] (int64).
+__host__ __device__ constexpr size_t pareto_dp_bytes(int n) { return dp_bytes_per_warp(n) * (kBlock / 32); }
+
+// Phase 1 over [begin, end).  For n >= 3 the space is cut into groups that
+// fix every digit but the last three (x = n-3, u = n-2, w = n-1); groups are
+// dealt to warps dynamically.  Each coordinate of a plan is monotone in each
+// of its options' own values (FP addition rounds monotonically, latency is a
+// max-plus polynomial of the walls, quality a min), so the coordinate-wise
+// best point a set of plans can reach -- its corner -- is an exact lower
+// bound: a guard point (a real plan) that dominates the corner dominates
+// every plan of the set, because each plan is no better than the corner in
+// every coordinate (the strict one stays strict).  Pruning goes group ->
+// row (x fixed) -> plan; the plans of live rows are evaluated exactly and the
+// ones no guard point dominates are appended with warp-ballot compaction.
+// Range edges (partial groups) and n < 3 take the one-plan-per-thread path.
 __global__ void __launch_bounds__(kBlock)
     pareto_eval_kernel(const uint8_t* __restrict__ blob_g, uint32_t blob_bytes, uint64_t begin, uint64_t end,
                        const ParetoPoint* __restrict__ guard, int n_guard, ParetoPoint* __restrict__ out,
-                       uint64_t cap, unsigned long long* __restrict__ count) {
+                       uint64_t cap, unsigned long long* __restrict__ count, unsigned long long* __restrict__ stats,
+                       unsigned long long* __restrict__ next_group) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mbar;
   load_blob(smem, blob_g, blob_bytes, &mbar);
   const View v = make_view(smem);
-  const GuardView gv = load_guard(smem + ((blob_bytes + 127) & ~127u), guard, n_guard);
+  uint8_t* guard_base = smem + ((blob_bytes + 127) & ~127u);
+  const GuardView gv = load_guard(guard_base, guard, n_guard);
   const int n = v.h->n_nodes;
   const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t nt = static_cast<uint64_t>(gridDim.x) * blockDim.x;
 
-  uint64_t R = 1, row_lo = 0, row_hi = 0;
-  if (n >= 2) {
-    R = static_cast<uint64_t>(v.radix[n - 2]) * v.radix[n - 1];
-    row_lo = (begin + R - 1) / R;
-    row_hi = end / R;
+  uint64_t G = 1, g_lo = 0, g_hi = 0;
+  if (n >= 3) {
+    G = static_cast<uint64_t>(v.radix[n - 3]) * v.radix[n - 2] * v.radix[n - 1];
+    g_lo = (begin + G - 1) / G;
+    g_hi = end / G;
   }
-  const bool rows = n >= 2 && row_lo < row_hi;
-  const uint64_t head_end = rows ? row_lo * R : end, tail_begin = rows ? row_hi * R : end;
+  const bool groups = n >= 3 && g_lo < g_hi;
+  const uint64_t head_end = groups ? g_lo * G : end, tail_begin = groups ? g_hi * G : end;
 
   // range edges: one plan per thread
   int d[kMaxNodes];
-  for (uint64_t base = begin; base < head_end; base += nt) {
-    const uint64_t i = base + gt;
-    ParetoPoint pt{};
-    bool keep = false;
-    if (i < head_end) {
-      decode_digits(v, i, d);
-      pt = eval_point(v, d, i);
-      keep = !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
+  for (int part = 0; part < 2; ++part) {
+    const uint64_t lo = part == 0 ? begin : tail_begin, hi = part == 0 ? head_end : end;
+    for (uint64_t base = lo; base < hi; base += nt) {
+      const uint64_t i = base + gt;
+      ParetoPoint pt{};
+      bool keep = false;
+      if (i < hi) {
+        decode_digits(v, i, d);
+        pt = eval_point(v, d, i);
+        keep = !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
+      }
+      append_point(keep, pt, out, cap, count);
     }
-    append_point(keep, pt, out, cap, count);
   }
-  for (uint64_t base = tail_begin; base < end; base += nt) {
-    const uint64_t i = base + gt;
-    ParetoPoint pt{};
-    bool keep = false;
-    if (i < end) {
-      decode_digits(v, i, d);
-      pt = eval_point(v, d, i);
-      keep = !guarded(gv, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
-    }
-    append_point(keep, pt, out, cap, count);
-  }
-  if (!rows) return;
+  if (!groups) return;
 
-  // whole rows, contiguous per thread (the row counts differ by at most one)
-  const uint64_t cnt = row_hi - row_lo, qn = cnt / nt, rn = cnt % nt;
-  const uint64_t my_lo = row_lo + gt * qn + min(gt, rn);
-  const uint64_t my_n = qn + (gt < rn ? 1 : 0);
-  const uint64_t max_n = qn + (rn ? 1 : 0);
-  const int u = n - 2, w = n - 1;
-  const int nu = v.radix[u], nw = v.radix[w];
-  const int offu = v.optoff[u], offw = v.optoff[w];
-  if (my_n) decode_digits(v, my_lo * R, d);
-  int64_t f[kMaxNodes][4];
-  int hint = 0;
-  for (uint64_t k = 0; k < max_n; ++k) {  // uniform trip count keeps the warp converged for the ballot
-    const bool live = k < my_n;
+  const int x = n - 3, u = n - 2, w = n - 1;
+  const int nx = v.radix[x], nu = v.radix[u], nw = v.radix[w];
+  const int offx = v.optoff[x], offu = v.optoff[u], offw = v.optoff[w];
+  // per-node extremes of the three free nodes (corner terms)
+  double gb_min[3] = {INFINITY, INFINITY, INFINITY}, ga_min[3] = {INFINITY, INFINITY, INFINITY};
+  int64_t w_min[3] = {INT64_MAX, INT64_MAX, INT64_MAX};
+  int32_t q_max[3] = {INT_MIN, INT_MIN, INT_MIN};
+  for (int t = 0; t < 3; ++t) {
+    const int node = x + t;
+    for (int o = v.optoff[node]; o < v.optoff[node + 1]; ++o) {
+      gb_min[t] = fmin(gb_min[t], v.gb[o]);
+      ga_min[t] = fmin(ga_min[t], v.ga[o]);
+      w_min[t] = min(w_min[t], v.wall[o]);
+      q_max[t] = max(q_max[t], v.q[o]);
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  int64_t* fw = reinterpret_cast<int64_t*>(guard_base + kGuardBytes + dp_bytes_per_warp(n) * (threadIdx.x >> 5));
+  int64_t* cw = fw + 32 * n;
+  const int row_plans = nu * nw;
+  int hint = 0, row_hint = 0;
+  unsigned long long st_groups = 0, st_live_groups = 0, st_rows = 0, st_live_rows = 0;
+
+  for (;;) {
+    unsigned long long gi = 0;
+    if (lane == 0) gi = atomicAdd(next_group, 1ull);
+    const uint64_t g = g_lo + __shfl_sync(0xffffffffu, gi, 0);
+    if (g >= g_hi) break;
+    // digits of nodes [0, x): lane-parallel decode, then shared
+    {
+      uint64_t r = g;
+      int mine = 0;
+      for (int i = x - 1; i >= 0; --i) {
+        const uint64_t rad = static_cast<uint64_t>(v.radix[i]);
+        const int di = static_cast<int>(r % rad);
+        r /= rad;
+        if (i == lane) mine = di;
+      }
+      for (int i = 0; i < x; ++i) d[i] = __shfl_sync(0xffffffffu, mine, i & 31);
+    }
     double e0 = 0.0, d0 = 0.0;
     int32_t q0 = INT_MAX;
-    int64_t c[4] = {0, kNeg, kNeg, kNeg};
-    if (live) {
-      for (int i = 0; i < u; ++i) {
-        const int o = v.optoff[i] + d[i];
-        e0 = __dadd_rn(e0, v.ga[o]);
-        d0 = __dadd_rn(d0, v.gb[o]);
-        q0 = min(q0, v.q[o]);
+    for (int i = 0; i < x; ++i) {
+      const int o = v.optoff[i] + d[i];
+      e0 = __dadd_rn(e0, v.ga[o]);
+      d0 = __dadd_rn(d0, v.gb[o]);
+      q0 = min(q0, v.q[o]);
+    }
+    warp_dp<3>(v, d, x, fw, cw);  // cw[S], S over subsets of {x (bit 0), u (bit 1), w (bit 2)}
+    ++st_groups;
+    // group corner
+    {
+      const double dl = __dadd_rn(__dadd_rn(__dadd_rn(d0, gb_min[0]), gb_min[1]), gb_min[2]);
+      const double el = __dadd_rn(__dadd_rn(__dadd_rn(e0, ga_min[0]), ga_min[1]), ga_min[2]);
+      int64_t ll = kNeg;
+      for (int S = 0; S < 8; ++S) {
+        int64_t t = cw[S];
+        for (int b = 0; b < 3; ++b)
+          if (S >> b & 1) t += w_min[b];
+        ll = max(ll, t);
       }
-      // longest paths with u (bit 0) and w (bit 1) symbolic
-      c[1] = c[2] = c[3] = kNeg;
-      c[0] = 0;
-      for (int t = 0; t < n; ++t) {
-        const int x = v.topo[t];
-        const int pb = v.predoff[x], pe = v.predoff[x + 1];
-        for (int S = 0; S < 4; ++S) {
-          int64_t val = kNeg;
-          if (x < u) {
-            int64_t b = S == 0 ? 0 : kNeg;
-            for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S]);
-            val = b + v.wall[v.optoff[x] + d[x]];
-          } else {
-            const int bit = x == u ? 1 : 2;
-            if (S & bit) {
-              const int S2 = S ^ bit;
-              int64_t b = S2 == 0 ? 0 : kNeg;
-              for (int e = pb; e < pe; ++e) b = max(b, f[v.pred[e]][S2]);
-              val = b;
-            }
+      const int32_t qb = min(q0, min(q_max[0], min(q_max[1], q_max[2])));
+      if (guarded_warp(gv, dl, el, ll, qb)) continue;
+    }
+    ++st_live_groups;
+    const uint64_t gbase = g * G;
+    for (int r0 = 0; r0 < nx; r0 += 32) {
+      // row r0 + lane: x fixed -> 4-entry vector over subsets of {u, w}
+      const int ox = r0 + lane;
+      const bool has = ox < nx;
+      double e1 = 0.0, d1 = 0.0;
+      int32_t q1 = INT_MAX;
+      int64_t c4[4] = {kNeg, kNeg, kNeg, kNeg};
+      bool row_live = false;
+      if (has) {
+        const int o = offx + ox;
+        const int64_t wx = v.wall[o];
+        for (int T = 0; T < 4; ++T) c4[T] = max(cw[T << 1], cw[(T << 1) | 1] + wx);
+        e1 = __dadd_rn(e0, v.ga[o]);
+        d1 = __dadd_rn(d0, v.gb[o]);
+        q1 = min(q0, v.q[o]);
+        const double dl = __dadd_rn(__dadd_rn(d1, gb_min[1]), gb_min[2]);
+        const double el = __dadd_rn(__dadd_rn(e1, ga_min[1]), ga_min[2]);
+        const int64_t ll = max(max(c4[0], c4[1] + w_min[1]), max(c4[2] + w_min[2], c4[3] + w_min[1] + w_min[2]));
+        const int32_t qb = min(q1, min(q_max[1], q_max[2]));
+        row_live = !guarded_hint(gv, row_hint, dl, el, ll, qb);
+      }
+      st_rows += __popc(__ballot_sync(0xffffffffu, has));
+      const unsigned live = __ballot_sync(0xffffffffu, row_live);
+      st_live_rows += __popc(live);
+      // live rows: the warp splits each row's plans
+      for (unsigned m = live; m; m &= m - 1) {
+        const int src = __ffs(m) - 1;
+        const double re = __shfl_sync(0xffffffffu, e1, src), rd = __shfl_sync(0xffffffffu, d1, src);
+        const int32_t rq = __shfl_sync(0xffffffffu, q1, src);
+        const int64_t a0 = __shfl_sync(0xffffffffu, c4[0], src), a1 = __shfl_sync(0xffffffffu, c4[1], src);
+        const int64_t a2 = __shfl_sync(0xffffffffu, c4[2], src), a3 = __shfl_sync(0xffffffffu, c4[3], src);
+        const uint64_t rbase = gbase + static_cast<uint64_t>(r0 + src) * row_plans;
+        for (int j0 = 0; j0 < row_plans; j0 += 32) {
+          const int j = j0 + lane;
+          ParetoPoint pt{};
+          bool keep = false;
+          if (j < row_plans) {
+            const int ou = j / nw, ow = j - ou * nw;
+            const int64_t wu = v.wall[offu + ou];
+            pt.index = rbase + static_cast<uint64_t>(j);
+            pt.latency_us = max(max(a0, a1 + wu), max(a2, a3 + wu) + v.wall[offw + ow]);
+            pt.gpu_wh = __dadd_rn(__dadd_rn(re, v.ga[offu + ou]), v.ga[offw + ow]);
+            pt.dollars = __dadd_rn(__dadd_rn(rd, v.gb[offu + ou]), v.gb[offw + ow]);
+            pt.quality = min(min(rq, v.q[offu + ou]), v.q[offw + ow]);
+            keep = !guarded_hint(gv, hint, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
           }
-          f[x][S] = val;
-          c[S] = max(c[S], val);
+          append_point(keep, pt, out, cap, count);
         }
       }
     }
-    const uint64_t row_base = (my_lo + k) * R;
-    for (int ou = 0; ou < nu; ++ou) {
-      const int64_t wu = v.wall[offu + ou];
-      const int64_t X = max(c[0], c[1] + wu), Y = max(c[2], c[3] + wu);
-      const double eu = __dadd_rn(e0, v.ga[offu + ou]);
-      const double du = __dadd_rn(d0, v.gb[offu + ou]);
-      const int32_t qu = min(q0, v.q[offu + ou]);
-      for (int ow = 0; ow < nw; ++ow) {
-        ParetoPoint pt;
-        pt.index = row_base + static_cast<uint64_t>(ou) * nw + ow;
-        pt.latency_us = max(X, Y + v.wall[offw + ow]);
-        pt.gpu_wh = __dadd_rn(eu, v.ga[offw + ow]);
-        pt.dollars = __dadd_rn(du, v.gb[offw + ow]);
-        pt.quality = min(qu, v.q[offw + ow]);
-        pt.pad = 0;
-        const bool keep = live && !guarded_hint(gv, hint, pt.dollars, pt.gpu_wh, pt.latency_us, pt.quality);
-        append_point(keep, pt, out, cap, count);
-      }
-    }
-    if (live)  // next row: odometer over the prefix digits
-      for (int i = u - 1; i >= 0; --i) {
-        if (++d[i] < v.radix[i]) break;
-        d[i] = 0;
-      }
+  }
+  if (stats && lane == 0) {  // LOOM_DEBUG: groups, live groups, rows, live rows
+    atomicAdd(&stats[0], st_groups);
+    atomicAdd(&stats[1], st_live_groups);
+    atomicAdd(&stats[2], st_rows);
+    atomicAdd(&stats[3], st_live_rows);
   }
 }
 
@@ -1191,8 +1258,12 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // Phase 2: keep[i] = no j != i dominates point i (tiles staged in smem).
+// span > 0: point i is compared only with the points of its own span-sized
+// block (a multiple of the CTA size) -- the first stage of a blocked filter,
+// exact because frontier(A u B) = frontier(frontier(A) u frontier(B)).
 __global__ void __launch_bounds__(kBlock)
-    pareto_filter_kernel(const ParetoPoint* __restrict__ pts, uint64_t n, uint8_t* __restrict__ keep) {
+    pareto_filter_kernel(const ParetoPoint* __restrict__ pts, uint64_t n, uint8_t* __restrict__ keep,
+                         uint64_t span) {
   constexpr int T = 512;
   __shared__ double sd[T], se[T];
   __shared__ int64_t sl[T];
@@ -1201,9 +1272,12 @@ __global__ void __launch_bounds__(kBlock)
   ParetoPoint me{};
   if (i < n) me = pts[i];
   bool dom = i >= n;
-  for (uint64_t t0 = 0; t0 < n; t0 += T) {
-    __syncthreads();
-    for (int k = threadIdx.x; k < T && t0 + k < n; k += blockDim.x) {
+  const uint64_t first = static_cast<uint64_t>(blockIdx.x) * blockDim.x;
+  const uint64_t lo = span ? first / span * span : 0;
+  const uint64_t hi = span ? min(n, lo + span) : n;
+  for (uint64_t t0 = lo; t0 < hi; t0 += T) {
+    if (!__syncthreads_or(!dom)) break;  // every point of the block already has a dominator
+    for (int k = threadIdx.x; k < T && t0 + k < hi; k += blockDim.x) {
       const ParetoPoint p = pts[t0 + k];
       sd[k] = p.dollars;
       se[k] = p.gpu_wh;
@@ -1211,7 +1285,7 @@ __global__ void __launch_bounds__(kBlock)
       sq[k] = p.quality;
     }
     __syncthreads();
-    const int lim = static_cast<int>(n - t0 < static_cast<uint64_t>(T) ? n - t0 : static_cast<uint64_t>(T));
+    const int lim = static_cast<int>(hi - t0 < static_cast<uint64_t>(T) ? hi - t0 : static_cast<uint64_t>(T));
     if (!dom)
       for (int k = 0; k < lim; ++k)
         if (dominates(sd[k], se[k], sl[k], sq[k], me.dollars, me.gpu_wh, me.latency_us, me.quality)) {
@@ -1583,6 +1657,11 @@ struct loom_ctx {
   size_t out_cap = 0;
   Rec* h_out = nullptr;  // pinned
   size_t h_out_cap = 0;
+  // Device scratch pool (grow-only size classes, reused across calls; all
+  // work of a ctx is ordered on its one stream, so reuse needs no sync).
+  std::mutex pool_mu;
+  std::multimap<size_t, void*> pool_free;
+  std::vector<void*> pool_all;
   // last Pareto frontier (size-query-then-fill without a second search)
   std::vector<loom_point> pareto_cache;
   uint64_t pareto_key = 0;
@@ -1774,6 +1853,7 @@ int loom_ctx_destroy(loom_ctx* c) {
   cudaFree(c->d_scratch);
   cudaFree(c->d_tickets);
   cudaFree(c->d_out);
+  for (void* q : c->pool_all) cudaFree(q);
   if (c->h_out) cudaFreeHost(c->h_out);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -2031,11 +2111,47 @@ static_assert(sizeof(ParetoPoint) == sizeof(loom_point), "ParetoPoint must match
 
 template <class T>
 struct DevBuf {
+  // Scratch from the ctx's pool (returned on scope exit, freed with the ctx).
+  explicit DevBuf(loom_ctx* ctx) : c(ctx) {}
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  loom_ctx* c;
   T* p = nullptr;
+  size_t cls = 0;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) {
+      std::lock_guard<std::mutex> g(c->pool_mu);
+      c->pool_free.emplace(cls, p);
+    }
   }
-  cudaError_t alloc(size_t n) { return cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T)); }
+  cudaError_t alloc(size_t n) {
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    // size classes: powers of two up to 4 MiB, then multiples of 4 MiB
+    size_t k = 256;
+    if (bytes <= (size_t(4) << 20)) {
+      while (k < bytes) k <<= 1;
+    } else {
+      k = (bytes + (size_t(4) << 20) - 1) & ~((size_t(4) << 20) - 1);
+    }
+    {
+      std::lock_guard<std::mutex> g(c->pool_mu);
+      auto it = c->pool_free.find(k);
+      if (it != c->pool_free.end()) {
+        p = static_cast<T*>(it->second);
+        c->pool_free.erase(it);
+        cls = k;
+        return cudaSuccess;
+      }
+    }
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, k);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(c->pool_mu);
+    c->pool_all.push_back(q);
+    p = static_cast<T*>(q);
+    cls = k;
+    return cudaSuccess;
+  }
 };
 
 uint64_t fnv(uint64_t h, const void* data, size_t n) {
@@ -2060,14 +2176,18 @@ uint64_t problem_hash(const loom_problem* p, uint64_t begin, uint64_t end) {
   return fnv(h, &end, 8);
 }
 
-// Exact frontier of device points [0, n) -> host vector.
+// Exact frontier of device points [0, n) -> host vector.  Large sets are
+// filtered blockwise first (each point against its 8K block), the block
+// frontiers are compacted on the host and filtered pairwise.
 int filter_device(loom_ctx* c, const ParetoPoint* d_pts, uint64_t n, std::vector<ParetoPoint>& out) {
   out.clear();
   if (n == 0) return LOOM_OK;
-  DevBuf<uint8_t> keep;
+  constexpr uint64_t kSpan = 8192;
+  DevBuf<uint8_t> keep(c);
   LOOM_CUDA(keep.alloc(n));
   const uint64_t blocks = (n + kBlock - 1) / kBlock;
-  pareto_filter_kernel<<<static_cast<unsigned>(blocks), kBlock, 0, c->stream>>>(d_pts, n, keep.p);
+  const uint64_t span = n > 2 * kSpan ? kSpan : 0;
+  pareto_filter_kernel<<<static_cast<unsigned>(blocks), kBlock, 0, c->stream>>>(d_pts, n, keep.p, span);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   std::vector<uint8_t> hk(n);
@@ -2077,6 +2197,13 @@ int filter_device(loom_ctx* c, const ParetoPoint* d_pts, uint64_t n, std::vector
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   for (uint64_t i = 0; i < n; ++i)
     if (hk[i]) out.push_back(hp[i]);
+  if (span == 0) return LOOM_OK;
+  DevBuf<ParetoPoint> d2(c);
+  LOOM_CUDA(d2.alloc(out.size()));
+  LOOM_CUDA(cudaMemcpyAsync(d2.p, out.data(), out.size() * sizeof(ParetoPoint), cudaMemcpyHostToDevice, c->stream));
+  std::vector<ParetoPoint> f;
+  if (int rc = filter_device(c, d2.p, out.size(), f)) return rc;
+  out = std::move(f);
   return LOOM_OK;
 }
 
@@ -2096,8 +2223,8 @@ std::vector<ParetoPoint> guard_of(std::vector<ParetoPoint> f) {
 int refine_and_filter(loom_ctx* c, ParetoPoint* d_in, uint64_t n, std::vector<ParetoPoint> guard,
                       std::vector<ParetoPoint>& front) {
   const uint64_t kSub = 1 << 16;
-  DevBuf<ParetoPoint> d_a, d_sub, d_g;
-  DevBuf<unsigned long long> d_cnt;
+  DevBuf<ParetoPoint> d_a(c), d_sub(c), d_g(c);
+  DevBuf<unsigned long long> d_cnt(c);
   LOOM_CUDA(d_a.alloc(n));
   LOOM_CUDA(d_sub.alloc(kSub));
   LOOM_CUDA(d_g.alloc(kGuardMax));
@@ -2154,8 +2281,8 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
   if (begin >= end) return LOOM_OK;
   const uint64_t n = end - begin;
   const uint32_t bytes = static_cast<uint32_t>(b.blob.size());
-  const size_t smem = ((bytes + 127) & ~size_t(127)) + kGuardBytes;
-  DevBuf<uint8_t> d_blob;
+  const size_t smem = ((bytes + 127) & ~size_t(127)) + kGuardBytes + pareto_dp_bytes(p->n_nodes);
+  DevBuf<uint8_t> d_blob(c);
   LOOM_CUDA(d_blob.alloc(bytes));
   LOOM_CUDA(cudaMemcpyAsync(d_blob.p, b.blob.data(), bytes, cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pareto_eval_kernel),
@@ -2170,8 +2297,8 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
     std::vector<uint64_t> idx(kSample);
     for (uint64_t k = 0; k < kSample; ++k)
       idx[k] = begin + static_cast<uint64_t>((static_cast<unsigned __int128>(n) * k) / kSample);
-    DevBuf<uint64_t> d_idx;
-    DevBuf<ParetoPoint> d_s;
+    DevBuf<uint64_t> d_idx(c);
+    DevBuf<ParetoPoint> d_s(c);
     LOOM_CUDA(d_idx.alloc(kSample));
     LOOM_CUDA(d_s.alloc(kSample));
     LOOM_CUDA(cudaMemcpyAsync(d_idx.p, idx.data(), kSample * 8, cudaMemcpyHostToDevice, c->stream));
@@ -2185,8 +2312,9 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
   }
 
   const uint64_t cap = std::min<uint64_t>(uint64_t(1) << 22, n);
-  DevBuf<ParetoPoint> d_cand, d_guard;
-  DevBuf<unsigned long long> d_count;
+  DevBuf<ParetoPoint> d_cand(c), d_guard(c);
+  DevBuf<unsigned long long> d_count(c), d_next(c);
+  LOOM_CUDA(d_next.alloc(1));
   LOOM_CUDA(d_cand.alloc(cap));
   LOOM_CUDA(d_guard.alloc(kGuardMax));
   LOOM_CUDA(d_count.alloc(1));
@@ -2204,8 +2332,22 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
     if (!guard.empty())
       LOOM_CUDA(cudaMemcpyAsync(d_guard.p, guard.data(), guard.size() * sizeof(ParetoPoint), cudaMemcpyHostToDevice,
                                 c->stream));
+    DevBuf<unsigned long long> d_stats(c);
+    const bool dbg = std::getenv("LOOM_DEBUG") != nullptr;
+    if (dbg) {
+      LOOM_CUDA(d_stats.alloc(4));
+      LOOM_CUDA(cudaMemsetAsync(d_stats.p, 0, 32, c->stream));
+    }
+    LOOM_CUDA(cudaMemsetAsync(d_next.p, 0, sizeof(unsigned long long), c->stream));
     pareto_eval_kernel<<<grid, kBlock, smem, c->stream>>>(d_blob.p, bytes, begin, end, d_guard.p,
-                                                          static_cast<int>(guard.size()), d_cand.p, cap, d_count.p);
+                                                          static_cast<int>(guard.size()), d_cand.p, cap, d_count.p,
+                                                          d_stats.p, d_next.p);
+    if (dbg) {
+      unsigned long long st[4];
+      LOOM_CUDA(cudaMemcpyAsync(st, d_stats.p, 32, cudaMemcpyDeviceToHost, c->stream));
+      LOOM_CUDA(cudaStreamSynchronize(c->stream));
+      std::fprintf(stderr, "[loom pareto] groups %llu live %llu, rows %llu live %llu\n", st[0], st[1], st[2], st[3]);
+    }
     LOOM_CUDA(cudaGetLastError());
     ++c->launches;
     LOOM_CUDA(cudaMemcpyAsync(&count, d_count.p, sizeof count, cudaMemcpyDeviceToHost, c->stream));
@@ -2223,10 +2365,10 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
       return LOOM_OK;
     }
     std::vector<ParetoPoint> f;
-    if (int rc = filter_device(c, d_cand.p, cap, f)) return rc;
+    if (int rc = refine_and_filter(c, d_cand.p, cap, guard, f)) return rc;
     // overflow: the frontier of what was collected (real plans) joins the guard
     f.insert(f.end(), guard.begin(), guard.end());
-    DevBuf<ParetoPoint> d_g2;
+    DevBuf<ParetoPoint> d_g2(c);
     LOOM_CUDA(d_g2.alloc(f.size()));
     LOOM_CUDA(cudaMemcpyAsync(d_g2.p, f.data(), f.size() * sizeof(ParetoPoint), cudaMemcpyHostToDevice, c->stream));
     std::vector<ParetoPoint> g2;
@@ -2273,12 +2415,12 @@ extern "C" int loom_pareto_filter_points(loom_ctx* c, const loom_point* pts, uin
   if (!c || (n && (!pts || !keep))) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   if (n == 0) return LOOM_OK;
   LOOM_CUDA(cudaSetDevice(c->device));
-  DevBuf<ParetoPoint> d;
-  DevBuf<uint8_t> k;
+  DevBuf<ParetoPoint> d(c);
+  DevBuf<uint8_t> k(c);
   LOOM_CUDA(d.alloc(n));
   LOOM_CUDA(k.alloc(n));
   LOOM_CUDA(cudaMemcpyAsync(d.p, pts, n * sizeof(loom_point), cudaMemcpyHostToDevice, c->stream));
-  pareto_filter_kernel<<<static_cast<unsigned>((n + kBlock - 1) / kBlock), kBlock, 0, c->stream>>>(d.p, n, k.p);
+  pareto_filter_kernel<<<static_cast<unsigned>((n + kBlock - 1) / kBlock), kBlock, 0, c->stream>>>(d.p, n, k.p, 0);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(keep, k.p, n, cudaMemcpyDeviceToHost, c->stream));
@@ -2325,9 +2467,9 @@ extern "C" int loom_search_greedy(loom_ctx* c, const loom_problem* p, const loom
   Built b;
   if (int rc = build_image(p, o, 1, b)) return rc;
   const uint32_t bytes = static_cast<uint32_t>(b.blob.size());
-  DevBuf<uint8_t> d_blob;
-  DevBuf<int32_t> d_ord, d_seed, d_sw;
-  DevBuf<Rec> d_out;
+  DevBuf<uint8_t> d_blob(c);
+  DevBuf<int32_t> d_ord(c), d_seed(c), d_sw(c);
+  DevBuf<Rec> d_out(c);
   LOOM_CUDA(d_blob.alloc(bytes));
   LOOM_CUDA(d_ord.alloc(n));
   LOOM_CUDA(d_seed.alloc(n));
