@@ -87,3 +87,60 @@ def test_shard_ranges_cover_space():
         parts = [D.shard_range(total, r, world) for r in range(world)]
         assert parts[0][0] == 0 and parts[-1][1] == total
         assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+
+
+def _pareto_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from oracle import oracle as O
+    from paper_2501_16634_b200 import dist as D, workloads as W
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = W.config5(n_nodes=4)
+        p = O.problem(w.dag, w.library, w.bounds)
+        total = 10 ** 4
+        b, e = D.shard_range(total, rank, world)
+        # the oracle stands in for the per-rank GPU frontier search
+        mine = [{"plan_index": o["index"], "dollars": o["dollars"], "gpu_wh": o["gpu_wh"],
+                 "latency_us": o["latency_us"], "quality": o["quality"]} for o in O.pareto(p, b, e, threads=1)]
+        got = D.allgather_frontiers(mine)
+        assert len(got) == world and got[rank] == mine
+
+        def keep(points):  # checker-side pairwise filter (the product uses loom_pareto_filter_points)
+            def dom(a, b):
+                le = (a["dollars"] <= b["dollars"] and a["gpu_wh"] <= b["gpu_wh"]
+                      and a["latency_us"] <= b["latency_us"] and a["quality"] >= b["quality"])
+                lt = (a["dollars"] < b["dollars"] or a["gpu_wh"] < b["gpu_wh"]
+                      or a["latency_us"] < b["latency_us"] or a["quality"] > b["quality"])
+                return le and lt
+            return [not any(dom(o, x) for o in points) for x in points]
+
+        merged = D.combine_frontiers(got, keep)
+        if rank == 0:
+            q.put([m["plan_index"] for m in merged])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_frontier_allgather(world):
+    """Per-rank frontiers all-gathered over torch.distributed (counts, then a
+    padded all-gather) and merged equal the whole-space frontier."""
+    from oracle import oracle as O
+    from paper_2501_16634_b200 import workloads as W
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pareto_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    w = W.config5(n_nodes=4)
+    assert got == [o["index"] for o in O.pareto(O.problem(w.dag, w.library, w.bounds), threads=2)]
+    assert len(got) > 3

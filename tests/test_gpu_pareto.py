@@ -80,3 +80,17 @@ def test_c5_full_space_properties(ctx):
         x = np.array([e["dollars"], e["gpu_wh"], e["latency_us"]])
         le = (F <= x).all(axis=1)
         assert le.any(), i  # some frontier point is no worse on every axis
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_frontier_merge(ctx, world):
+    """per-rank frontiers of contiguous index shards, merged by
+    one device filter of their union, equal the whole-space frontier (C5 with
+    7 tasks: 1e7 plans, every shard boundary inside a group)."""
+    from paper_2501_16634_b200 import dist as D
+    w = W.config5(n_nodes=7)
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    whole = loom.search_pareto_points(ctx, lw.problem)
+    shards = [loom.search_pareto_points(ctx, lw.problem, *D.shard_range(lw.total, r, world)) for r in range(world)]
+    merged = D.combine_frontiers(shards, lambda pts: loom.pareto_filter_points(ctx, pts))
+    assert merged == whole and len(whole) > 10
