@@ -33,6 +33,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "plans evaluated/sec (1/2/4/8 B200, % of roofline) vs CPU ref; time-to-plan"
+WORKLOAD = ("C3: 10-task layered DAG x 16 options/task = 1.1e12 plans, MIN_COST (min gpu energy, then latency) "
+            "under a latency SLO")
 UNIT = "plans/s"
 
 
@@ -135,8 +137,10 @@ def reference_arm(args) -> None:
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "C3: 10-task DAG x 16 options/task (1.1e12 plans), MIN_COST + latency SLO",
-                       "sample_plans_per_step": sample},
+            "config": {"workload": WORKLOAD, "plans_per_step": sample,
+                       "parallelism": f"reference CPU range driver, {threads} host threads",
+                       "sample": "a bounded slice of the same plan space per step (the full space would take "
+                                 "~1e6 s on the host)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"{sample} consecutive plan indices of C3 per step, range driver over the "
                                        f"reference's estimate/objective_less on {threads} threads"},
@@ -296,8 +300,7 @@ def b200_arm(args) -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic",
-            "config": {"workload": "C3: 10-task layered DAG x 16 options/task = 1.1e12 plans, MIN_COST "
-                                   "(min gpu energy, then latency) under a latency SLO",
+            "config": {"workload": WORKLOAD,
                        "plans_per_step": total, "parallelism": f"plan-index range x{world}",
                        "l2": "flushed between timed steps (256 MiB write); the problem image is 8 KB in smem",
                        "chosen_plan_index": chosen["plan_index"], "chosen_latency_us": chosen["latency_us"],
