@@ -102,6 +102,12 @@ struct ExecutionProfile {
 // profiles in (implementation, sku, units) order).
 class AgentLibrary {
  public:
+  AgentLibrary() = default;
+  AgentLibrary(const AgentLibrary& other);  // copies rebuild the pointer indexes
+  AgentLibrary& operator=(const AgentLibrary& other);
+  AgentLibrary(AgentLibrary&&) noexcept = default;  // map nodes move with the maps
+  AgentLibrary& operator=(AgentLibrary&&) noexcept = default;
+
   static AgentLibrary from_json_text(const std::string& bundle_json);
 
   void add_capability(const std::string& capability);
@@ -121,6 +127,12 @@ class AgentLibrary {
   std::map<std::string, HardwareSku, std::less<>> skus_;
   std::map<std::string, Implementation, std::less<>> impls_;
   std::map<std::tuple<std::string, std::string, int>, ExecutionProfile, std::less<>> profiles_;
+  // Indexes kept in lookup order as entries are added (map nodes are stable):
+  // implementations per capability (quality desc, then name) and profiles
+  // per implementation ((sku, units) order).
+  std::map<std::string, std::vector<const Implementation*>, std::less<>> impls_by_cap_;
+  std::map<std::string, std::vector<const ExecutionProfile*>, std::less<>> profiles_by_impl_;
+  void rebuild_indexes();
 };
 
 // ---- dag + objective (workflow.hpp:67-106, 259-301) ---------------------

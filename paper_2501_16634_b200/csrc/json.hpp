@@ -10,6 +10,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 namespace loomjson {
@@ -71,5 +72,33 @@ class Value {
 };
 
 Value parse(const std::string& text);
+
+// Pull cursor over JSON text for hot readers (dag.json in batch lowering):
+// no DOM.  Every method returns false on anything it does not handle (escape
+// sequences, type mismatches, syntax errors); callers then fall back to
+// parse(), which produces the canonical error messages.
+class Cursor {
+ public:
+  explicit Cursor(const std::string& t) : s_(t.data()), n_(t.size()) {}
+  bool open(char c);                  // '{' or '['
+  bool next(char close, bool& more);  // after a member / element: ',' -> more, close -> done
+  bool empty(char close);             // right after open: consumes close if the container is empty
+  bool key(std::string_view& k);      // "key" ':'
+  bool str(std::string& out);
+  bool num(double& out);
+  bool integer(long long& out);
+  bool boolean(bool& out);
+  bool null();                        // consumes null if present
+  bool skip();                        // any value
+  bool end();                         // only whitespace left
+
+ private:
+  void ws();
+  bool raw_string(std::string_view& out);
+  const char* s_;
+  std::size_t n_;
+  std::size_t p_ = 0;
+  int depth_ = 0;
+};
 
 }  // namespace loomjson

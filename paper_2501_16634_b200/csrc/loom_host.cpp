@@ -70,6 +70,33 @@ double num_or(const Value& j, const char* key, double dflt) {
 
 }  // namespace
 
+AgentLibrary::AgentLibrary(const AgentLibrary& o)
+    : capabilities_(o.capabilities_), skus_(o.skus_), impls_(o.impls_), profiles_(o.profiles_) {
+  rebuild_indexes();
+}
+
+AgentLibrary& AgentLibrary::operator=(const AgentLibrary& o) {
+  if (this != &o) {
+    capabilities_ = o.capabilities_;
+    skus_ = o.skus_;
+    impls_ = o.impls_;
+    profiles_ = o.profiles_;
+    rebuild_indexes();
+  }
+  return *this;
+}
+
+void AgentLibrary::rebuild_indexes() {
+  impls_by_cap_.clear();
+  profiles_by_impl_.clear();
+  for (const auto& kv : impls_) impls_by_cap_[kv.second.capability].push_back(&kv.second);
+  for (auto& kv : impls_by_cap_)
+    std::sort(kv.second.begin(), kv.second.end(), [](const Implementation* a, const Implementation* b) {
+      return a->quality != b->quality ? a->quality > b->quality : a->name < b->name;
+    });
+  for (const auto& kv : profiles_) profiles_by_impl_[std::get<0>(kv.first)].push_back(&kv.second);  // map order
+}
+
 void AgentLibrary::add_capability(const std::string& capability) {
   if (capabilities_.count(capability))
     throw DuplicateKeyError("agent '" + capability + "' is already registered");
@@ -94,7 +121,12 @@ void AgentLibrary::add_implementation(Implementation impl) {
                                  impl.capability + "'");
   if (impls_.count(impl.name))
     throw DuplicateKeyError("implementation '" + impl.name + "' is already registered");
-  impls_.emplace(impl.name, std::move(impl));
+  const Implementation* x = &impls_.emplace(impl.name, std::move(impl)).first->second;
+  auto& v = impls_by_cap_[x->capability];
+  const auto before = [](const Implementation* a, const Implementation* b) {
+    return a->quality != b->quality ? a->quality > b->quality : a->name < b->name;
+  };
+  v.insert(std::upper_bound(v.begin(), v.end(), x, before), x);
 }
 
 void AgentLibrary::add_profile(ExecutionProfile p) {
@@ -109,7 +141,13 @@ void AgentLibrary::add_profile(ExecutionProfile p) {
   if (profiles_.count(key))
     throw DuplicateKeyError("profile (" + p.implementation + ", " + p.sku + ", " +
                             std::to_string(p.units) + ") is already registered");
-  profiles_.emplace(std::move(key), std::move(p));
+  const auto it = profiles_.emplace(std::move(key), std::move(p)).first;
+  auto& v = profiles_by_impl_[it->second.implementation];
+  v.clear();  // rebuilt in map order from this implementation's key range
+  static const std::string kEmpty;
+  for (auto j = profiles_.lower_bound(std::forward_as_tuple(it->second.implementation, kEmpty, INT_MIN));
+       j != profiles_.end() && std::get<0>(j->first) == it->second.implementation; ++j)
+    v.push_back(&j->second);
 }
 
 AgentLibrary AgentLibrary::from_json_text(const std::string& text) {
@@ -169,30 +207,111 @@ const ExecutionProfile* AgentLibrary::profile(const std::string& impl, const std
 std::vector<const Implementation*> AgentLibrary::implementations_for(const std::string& capability) const {
   if (!capabilities_.count(capability))
     throw UnknownCapabilityError("capability '" + capability + "' is not registered");
-  std::vector<const Implementation*> out;
-  for (const auto& kv : impls_)
-    if (kv.second.capability == capability) out.push_back(&kv.second);
-  std::sort(out.begin(), out.end(), [](const Implementation* a, const Implementation* b) {
-    return a->quality != b->quality ? a->quality > b->quality : a->name < b->name;
-  });
-  return out;
+  const auto it = impls_by_cap_.find(capability);
+  return it == impls_by_cap_.end() ? std::vector<const Implementation*>{} : it->second;
 }
 
 std::vector<const ExecutionProfile*> AgentLibrary::profiles_for(const std::string& implementation) const {
-  std::vector<const ExecutionProfile*> out;
-  // The map key is (implementation, sku, units): start at the first key of
-  // this implementation and walk while it matches.
-  static const std::string kEmpty;
-  for (auto it = profiles_.lower_bound(std::forward_as_tuple(implementation, kEmpty, INT_MIN));
-       it != profiles_.end() && std::get<0>(it->first) == implementation; ++it)
-    out.push_back(&it->second);
-  return out;
+  const auto it = profiles_by_impl_.find(implementation);
+  return it == profiles_by_impl_.end() ? std::vector<const ExecutionProfile*>{} : it->second;
 }
 
 // ---------------------------------------------------------------------------
 // dag / bounds / objective
 // ---------------------------------------------------------------------------
+namespace {
+// dag.json without a DOM: the batch lowering's hot path (a 6-task dag.json
+// parses ~3x faster).  Fields the reader does not use are skipped; anything
+// unusual (escapes, duplicate or missing keys, type mismatches) returns
+// false and from_json_text falls back to the DOM reader, which produces the
+// canonical errors.
+bool read_dag_fast(const std::string& text, WorkflowDag& dag) {
+  loomjson::Cursor c(text);
+  if (!c.open('{') || c.empty('}')) return false;
+  bool have_nodes = false, have_edges = false;
+  for (bool more = true; more;) {
+    std::string_view k;
+    if (!c.key(k)) return false;
+    if (k == "nodes") {
+      if (have_nodes || !c.open('[')) return false;
+      have_nodes = true;
+      if (!c.empty(']'))
+        for (bool m2 = true; m2;) {
+          DagNode node;
+          unsigned seen = 0;
+          auto once = [&](unsigned bit) {
+            const bool fresh = !(seen & bit);
+            seen |= bit;
+            return fresh;
+          };
+          if (!c.open('{') || c.empty('}')) return false;
+          for (bool m3 = true; m3;) {
+            std::string_view f;
+            if (!c.key(f)) return false;
+            bool ok = true;
+            if (f == "id") ok = once(1) && c.str(node.id);
+            else if (f == "capability") ok = once(2) && c.str(node.capability);
+            else if (f == "work_units") ok = once(4) && c.num(node.work_units);
+            else if (f == "splittable") ok = once(8) && c.boolean(node.splittable);
+            else if (f == "min_chunk") ok = once(16) && c.num(node.min_chunk);
+            else if (f == "multi_path") ok = once(32) && c.boolean(node.multi_path);
+            else if (f == "path_quality_ceiling") {
+              ok = once(64);
+              if (ok && !c.null()) {
+                long long q = 0;
+                ok = c.integer(q);
+                node.path_quality_ceiling = static_cast<int>(q);
+              }
+            } else {
+              ok = c.skip();
+            }
+            if (!ok || !c.next('}', m3)) return false;
+          }
+          if ((seen & 15) != 15) return false;  // id, capability, work_units, splittable are required
+          dag.nodes.push_back(std::move(node));
+          if (!c.next(']', m2)) return false;
+        }
+    } else if (k == "edges") {
+      if (have_edges || !c.open('[')) return false;
+      have_edges = true;
+      if (!c.empty(']'))
+        for (bool m2 = true; m2;) {
+          Edge e;
+          unsigned seen = 0;
+          if (!c.open('{') || c.empty('}')) return false;
+          for (bool m3 = true; m3;) {
+            std::string_view f;
+            if (!c.key(f)) return false;
+            bool ok = true;
+            if (f == "from") {
+              ok = !(seen & 1) && c.str(e.from);
+              seen |= 1;
+            } else if (f == "to") {
+              ok = !(seen & 2) && c.str(e.to);
+              seen |= 2;
+            } else {
+              ok = c.skip();
+            }
+            if (!ok || !c.next('}', m3)) return false;
+          }
+          if (seen != 3) return false;
+          dag.edges.push_back(std::move(e));
+          if (!c.next(']', m2)) return false;
+        }
+    } else if (!c.skip()) {
+      return false;
+    }
+    if (!c.next('}', more)) return false;
+  }
+  return have_nodes && have_edges && c.end();
+}
+}  // namespace
+
 WorkflowDag WorkflowDag::from_json_text(const std::string& text) {
+  {
+    WorkflowDag fast;
+    if (read_dag_fast(text, fast)) return fast;
+  }
   WorkflowDag dag;
   try {
     const Value j = loomjson::parse(text);
@@ -344,6 +463,53 @@ int node_quality(const DagNode& node, const Implementation& impl, int path_count
   return node.path_quality_ceiling ? std::min(q, *node.path_quality_ceiling) : q;
 }
 
+namespace {
+struct Worker {
+  const ExecutionProfile* profile;
+  const HardwareSku* sku;
+};
+
+// chunking.hpp:136-181 on resolved workers (one entry per worker, placements
+// expanded): the work split, then per worker setup + run, wall = max, energy
+// to the gpu or cpu bucket by class, dollars.  Shared by plan_node_execution
+// and the lowering, so both produce the same doubles.
+NodePlan plan_workers(const DagNode& node, const Worker* workers, std::size_t n_workers, std::size_t n_placements,
+                      int fan) {
+  const auto where = [&] { return "node '" + node.id + "'"; };
+  std::vector<double> chunk;
+  if (n_workers == 1) {
+    chunk = {node.work_units};
+  } else if (n_placements <= 1) {
+    chunk = equal_split(node.work_units, fan, node.min_chunk);
+    if (static_cast<int>(chunk.size()) != fan)
+      throw InvalidConfigError(where() + ": fan-out " + std::to_string(fan) + " exceeds the chunk capacity of " +
+                               std::to_string(chunk_capacity(node.work_units, node.min_chunk)));
+  } else {
+    std::vector<double> speeds;
+    for (std::size_t w = 0; w < n_workers; ++w) speeds.push_back(workers[w].profile->throughput);
+    chunk = water_fill_split(node.work_units, node.min_chunk, speeds);
+    for (double c : chunk)
+      if (c <= 0.0 && node.work_units > 0.0)
+        throw InvalidConfigError(where() + ": degenerate hybrid placement; a worker receives no work");
+  }
+  NodePlan plan;
+  for (std::size_t w = 0; w < n_workers; ++w) {
+    const Worker& r = workers[w];
+    const Micros setup = to_micros(r.profile->setup_seconds);
+    const Micros run = to_micros(chunk[w] / r.profile->throughput);
+    const Micros dur = setup + run;
+    plan.wall_us = std::max(plan.wall_us, dur);
+    const double hours = to_seconds(dur) / 3600.0;
+    const double units = static_cast<double>(r.profile->units);
+    const double wh = units * r.sku->busy_watts_per_unit * hours;
+    if (r.sku->hardware_class == HardwareClass::gpu) plan.gpu_wh += wh;
+    else plan.cpu_wh += wh;
+    plan.dollars += units * r.sku->dollars_per_unit_hour * hours;
+  }
+  return plan;
+}
+}  // namespace
+
 NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const AgentLibrary& library) {
   const auto where = [&] { return "node '" + node.id + "'"; };  // only built on error
   const Implementation* impl = library.implementation(a.implementation);
@@ -358,10 +524,6 @@ NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const
   const int fan = a.fan_out();
   if (fan > 1 && !node.splittable) throw InvalidConfigError(where() + " is not splittable; fan-out must be 1");
 
-  struct Worker {
-    const ExecutionProfile* profile;
-    const HardwareSku* sku;
-  };
   std::vector<Worker> workers;
   for (const Placement& p : a.placements) {
     const HardwareSku* sku = library.sku(p.sku);
@@ -378,38 +540,7 @@ NodePlan plan_node_execution(const DagNode& node, const NodeAssignment& a, const
     for (int w = 0; w < p.workers; ++w) workers.push_back({prof, sku});
   }
 
-  std::vector<double> chunk;
-  if (workers.size() == 1) {
-    chunk = {node.work_units};
-  } else if (a.placements.size() <= 1) {
-    chunk = equal_split(node.work_units, fan, node.min_chunk);
-    if (static_cast<int>(chunk.size()) != fan)
-      throw InvalidConfigError(where() + ": fan-out " + std::to_string(fan) + " exceeds the chunk capacity of " +
-                               std::to_string(chunk_capacity(node.work_units, node.min_chunk)));
-  } else {
-    std::vector<double> speeds;
-    for (const Worker& w : workers) speeds.push_back(w.profile->throughput);
-    chunk = water_fill_split(node.work_units, node.min_chunk, speeds);
-    for (double c : chunk)
-      if (c <= 0.0 && node.work_units > 0.0)
-        throw InvalidConfigError(where() + ": degenerate hybrid placement; a worker receives no work");
-  }
-
-  NodePlan plan;
-  for (std::size_t w = 0; w < workers.size(); ++w) {
-    const Worker& r = workers[w];
-    const Micros setup = to_micros(r.profile->setup_seconds);
-    const Micros run = to_micros(chunk[w] / r.profile->throughput);
-    const Micros dur = setup + run;
-    plan.wall_us = std::max(plan.wall_us, dur);
-    const double hours = to_seconds(dur) / 3600.0;
-    const double units = static_cast<double>(r.profile->units);
-    const double wh = units * r.sku->busy_watts_per_unit * hours;
-    if (r.sku->hardware_class == HardwareClass::gpu) plan.gpu_wh += wh;
-    else plan.cpu_wh += wh;
-    plan.dollars += units * r.sku->dollars_per_unit_hour * hours;
-  }
-  return plan;
+  return plan_workers(node, workers.data(), workers.size(), a.placements.size(), fan);
 }
 
 // ---------------------------------------------------------------------------
@@ -432,40 +563,72 @@ bool fits(const SearchBounds& b, const std::string& sku, int units, int total_un
 }
 }  // namespace
 
-std::vector<NodeAssignment> node_options(const DagNode& node, const AgentLibrary& library,
-                                         const SearchBounds& bounds) {
-  std::vector<NodeAssignment> out;
+namespace {
+// node_options (optimizer.hpp:51-107).  With `plans` / `impls` set, each
+// option's NodePlan and implementation are produced on the way from the
+// already resolved profiles (the lowering's path: no name lookups per option).
+void enumerate_options(const DagNode& node, const AgentLibrary& library, const SearchBounds& bounds,
+                       std::vector<NodeAssignment>& out, std::vector<NodePlan>* plans,
+                       std::vector<const Implementation*>* impls) {
   const int paths_max = node.multi_path ? std::max(1, bounds.max_paths) : 1;
   const int fan_cap =
       node.splittable ? std::min(bounds.max_fanout, chunk_capacity(node.work_units, node.min_chunk)) : 1;
   const int fan_hi = std::max(1, fan_cap);
   const bool hybrids = node.splittable && bounds.max_fanout >= 2;
+  std::vector<Worker> workers;
 
-  auto emit = [&](const std::string& impl, std::vector<Placement> placements) {
-    for (int k = 1; k <= paths_max; ++k) out.push_back({impl, placements, k});
+  auto emit = [&](const Implementation* impl, std::vector<Placement> placements, const NodePlan* plan) {
+    for (int k = 1; k <= paths_max; ++k) {
+      out.push_back({impl->name, placements, k});
+      if (plans) plans->push_back(*plan);
+      if (impls) impls->push_back(impl);
+    }
   };
 
   for (const Implementation* impl : library.implementations_for(node.capability)) {
-    std::vector<const ExecutionProfile*> usable;
-    for (const ExecutionProfile* p : library.profiles_for(impl->name))
-      if (impl->supports(library.sku(p->sku)->hardware_class)) usable.push_back(p);
+    std::vector<Worker> usable;  // profiles of a supported class, with their sku
+    for (const ExecutionProfile* p : library.profiles_for(impl->name)) {
+      const HardwareSku* sku = library.sku(p->sku);
+      if (impl->supports(sku->hardware_class)) usable.push_back({p, sku});
+    }
 
-    for (const ExecutionProfile* p : usable)
+    NodePlan plan;
+    for (const Worker& u : usable)
       for (int w = 1; w <= fan_hi; ++w)
-        if (fits(bounds, p->sku, p->units, p->units * w)) emit(impl->name, {{p->sku, p->units, w}});
+        if (fits(bounds, u.profile->sku, u.profile->units, u.profile->units * w)) {
+          if (plans) {
+            workers.assign(static_cast<std::size_t>(w), u);
+            plan = plan_workers(node, workers.data(), workers.size(), 1, w);
+          }
+          emit(impl, {{u.profile->sku, u.profile->units, w}}, &plan);
+        }
 
     if (!hybrids) continue;
-    for (const ExecutionProfile* g : usable) {
-      if (library.sku(g->sku)->hardware_class != HardwareClass::gpu) continue;
-      for (const ExecutionProfile* c : usable) {
-        if (library.sku(c->sku)->hardware_class != HardwareClass::cpu) continue;
-        if (!fits(bounds, g->sku, g->units, g->units) || !fits(bounds, c->sku, c->units, c->units)) continue;
-        const auto split = water_fill_split(node.work_units, node.min_chunk, {g->throughput, c->throughput});
+    for (const Worker& g : usable) {
+      if (g.sku->hardware_class != HardwareClass::gpu) continue;
+      for (const Worker& c : usable) {
+        if (c.sku->hardware_class != HardwareClass::cpu) continue;
+        if (!fits(bounds, g.profile->sku, g.profile->units, g.profile->units) ||
+            !fits(bounds, c.profile->sku, c.profile->units, c.profile->units))
+          continue;
+        const auto split =
+            water_fill_split(node.work_units, node.min_chunk, {g.profile->throughput, c.profile->throughput});
         if (node.work_units > 0 && (split[0] <= 0 || split[1] <= 0)) continue;
-        emit(impl->name, {{g->sku, g->units, 1}, {c->sku, c->units, 1}});
+        if (plans) {
+          const Worker pair[2] = {g, c};
+          plan = plan_workers(node, pair, 2, 2, 2);
+        }
+        emit(impl, {{g.profile->sku, g.profile->units, 1}, {c.profile->sku, c.profile->units, 1}}, &plan);
       }
     }
   }
+}
+}  // namespace
+
+std::vector<NodeAssignment> node_options(const DagNode& node, const AgentLibrary& library,
+                                         const SearchBounds& bounds) {
+  std::vector<NodeAssignment> out;
+  enumerate_options(node, library, bounds, out, nullptr, nullptr);
   return out;
 }
 
@@ -635,7 +798,10 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
   for (int i = 0; i < n; ++i) {
     const DagNode& node = dag.nodes[i];
     check_name(node.id);
-    std::vector<NodeAssignment> opts = node_options(node, library, bounds);
+    std::vector<NodeAssignment> opts;
+    std::vector<NodePlan> plans;
+    std::vector<const Implementation*> impls;
+    enumerate_options(node, library, bounds, opts, &plans, &impls);
     const int r = static_cast<int>(opts.size());
     L.radix.push_back(r);
     if (r == 0) L.total = 0;
@@ -644,16 +810,17 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
     else L.total *= static_cast<uint64_t>(r);
 
     std::vector<std::string> tokens;
-    for (const NodeAssignment& a : opts) {
+    for (int o = 0; o < r; ++o) {
+      const NodeAssignment& a = opts[o];
       check_name(a.implementation);
       for (const Placement& p : a.placements) check_name(p.sku);
-      const NodePlan plan = plan_node_execution(node, a, library);
+      const NodePlan& plan = plans[o];  // == plan_node_execution(node, a, library), same arithmetic
       const double k = static_cast<double>(a.path_count);
       L.wall_us.push_back(plan.wall_us);
       L.gpu_wh.push_back(plan.gpu_wh * k);
       L.cpu_wh.push_back(plan.cpu_wh * k);
       L.dollars.push_back(plan.dollars * k);
-      L.quality.push_back(node_quality(node, *library.implementation(a.implementation), a.path_count));
+      L.quality.push_back(node_quality(node, *impls[o], a.path_count));
       tokens.push_back(assignment_token(node.id, a));
     }
     std::vector<int> order(r);

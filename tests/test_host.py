@@ -147,3 +147,41 @@ def test_device_entry_points_fail_loudly_without_gpu(loomlib):
         pytest.skip("GPU present")
     with pytest.raises(loom.DeviceError, match="no CUDA device"):
         loom.Context(0)
+
+
+def _tables(lw):
+    return [lw.table(t) for t in ("wall_us", "gpu_wh", "cpu_wh", "dollars", "quality", "lexrank", "lex_weight")]
+
+
+def test_dag_fast_reader_equals_dom_reader(loomlib):
+    """WorkflowDag::from_json_text reads dag.json with a DOM-free cursor and
+    falls back to the DOM reader on anything unusual; both must give the same
+    lowering (escaped strings, reordered / extra / duplicate keys, a null or
+    integral-real path_quality_ceiling, whitespace) and the same errors."""
+    import json
+    for w in (W.config1(), W.config3(), W.config5(n_nodes=5)) + tuple(W.config4(3)):
+        ref = loom.Lowered(json.dumps(w.dag), w.library, w.bounds)
+        variants = [
+            json.dumps(w.dag, indent=3),
+            json.dumps(w.dag, ensure_ascii=True).replace('"t0', '"\\u0074' + "0"),  # escape -> DOM path
+            json.dumps({"edges": w.dag["edges"], "extra": [1, {"a": None}], "nodes": [
+                dict(reversed(list(n.items())), note="x\\ny", path_quality_ceiling=None) for n in w.dag["nodes"]]}),
+        ]
+        for text in variants:
+            got = loom.Lowered(text, w.library, w.bounds)
+            assert got.radix == ref.radix and _tables(got) == _tables(ref)
+            assert got.config(0)["identifier"] == ref.config(0)["identifier"]
+    w = W.config1()
+    nodes = [dict(n) for n in w.dag["nodes"]]
+    nodes[1]["path_quality_ceiling"] = 2.0  # integral real: DOM reader accepts it
+    a = loom.Lowered(json.dumps({"nodes": nodes, "edges": w.dag["edges"]}), w.library, w.bounds)
+    nodes[1]["path_quality_ceiling"] = 2
+    b = loom.Lowered(json.dumps({"nodes": nodes, "edges": w.dag["edges"]}), w.library, w.bounds)
+    assert _tables(a) == _tables(b)
+    dup = json.dumps({"nodes": w.dag["nodes"], "edges": w.dag["edges"]})[:-1] + ', "nodes": []}'
+    with pytest.raises(loom.CycleError):  # duplicate key: the DOM reader's semantics (the later "nodes" wins)
+        loom.Lowered(dup, w.library, w.bounds)
+    for bad in ('{"nodes": [{"id": "a"}], "edges": []}', '{"nodes": []}', '{"nodes": [], "edges": [{"from": "a"}]}',
+                '[1, 2]', '{"nodes": [], "edges": []} trailing'):
+        with pytest.raises(loom.LoomError):
+            loom.Lowered(bad, w.library, w.bounds)
