@@ -216,7 +216,8 @@ __device__ __forceinline__ Rec slot_load(const Slots& s, int t) {
 __device__ __forceinline__ void slot_thresholds(const Slots& s, int t, const BlobHeader* h) {
   const bool f = s.found[t];
   s.hi[t] = f ? hi_of(s.qa[t]) : INFINITY;
-  s.lat_s[t] = (h->prim == kPrimLat && f) ? min(h->slo_eff, s.lat[t]) : h->slo_eff;
+  const bool tight = f && (h->prim == kPrimLat || (h->tie_lat && s.qa[t] <= h->qa_floor));
+  s.lat_s[t] = tight ? min(h->slo_eff, s.lat[t]) : h->slo_eff;
   s.bq[t] = f ? s.qual[t] : INT_MIN;
 }
 
@@ -524,11 +525,9 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       const uint64_t lex_u = lex + H.lexw[off + o];
       slow_scan<K, PRIM>(H.smem, H.slot_base, H.dpre, H.P, H.od[0], H.od[1], H.od[2], g0, g0 + (NV > 0 ? NV : 8), tw,
                          eu, qu, lex_u, X, Y, H.s_index * H.h->r_sub + inner_base);
-      reload(H);
-      if (PRIM == kPrimLat) {
-        const int64_t cc[4] = {cin[0], cin[SI], cin[2 * SI], cin[3 * SI]};
-        pr = pre_inner(cc, H.lat_s, wmin, wu_max);
-      }
+      reload(H);  // the latency bound may have tightened (latency primary, or an energy tie at the floor)
+      const int64_t cc[4] = {cin[0], cin[SI], cin[2 * SI], cin[3 * SI]};
+      pr = pre_inner(cc, H.lat_s, wmin, wu_max);
     };
     if constexpr (NV > 0) {
       // Two contexts per step share the innermost table: twice the
@@ -792,6 +791,11 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
   uint8_t* slot_base = smem + ((jd.blob_bytes + 127) & ~127u);
   const Slots sl = make_slots(slot_base);
   slot_init(sl, threadIdx.x, h);
+  if (h->has_seed && h->seed_index >= jd.begin && h->seed_index < jd.end) {
+    Rec c;
+    full_eval(v, h->seed_index, c);
+    slot_offer(sl, threadIdx.x, h, c);
+  }
 
   const uint64_t gt = static_cast<uint64_t>(part) * kBlock + threadIdx.x;
   const uint64_t nt = static_cast<uint64_t>(ctas_per_job) * kBlock;
@@ -1540,6 +1544,26 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
     if (crit[i] == kFpB || (crit[i] == kQual && prim != kPrimQual)) hd.needs_full = 1;
   hd.bytes = off;
   hd.slo_eff = slo_eff;
+  hd.tie_lat = prim == kPrimFp && o->n_criteria >= 2 && crit[1] == kLat && fp_kind[0] >= 0;
+  if (hd.tie_lat) {
+    const double* a = fp_kind[0] == LOOM_MIN_ENERGY ? p->gpu_wh : p->dollars;
+    double x = 0.0;  // dag-order fold of per-node minima (estimator.hpp:50-60): no plan's sum is below it
+    for (int i = 0; i < n; ++i) {
+      double m = INFINITY;
+      for (int k = optoff[i]; k < optoff[i + 1]; ++k) m = std::min(m, a[k]);
+      x += m;
+    }
+    hd.qa_floor = static_cast<int64_t>(std::llround(x * 1e9));
+  }
+  {
+    std::vector<int32_t> sd(n);
+    if (loom_greedy_seed(p, o, sd.data()) == LOOM_OK) {
+      uint64_t idx = 0;
+      for (int i = 0; i < n; ++i) idx = idx * static_cast<uint64_t>(p->radix[i]) + static_cast<uint64_t>(sd[i]);
+      hd.has_seed = 1;
+      hd.seed_index = idx;
+    }
+  }
   hd.inner_wmin = wmin;
   hd.pre_wmax = pre_wmax;
   hd.total = total;
@@ -1657,6 +1681,8 @@ struct loom_ctx {
   size_t out_cap = 0;
   Rec* h_out = nullptr;  // pinned
   size_t h_out_cap = 0;
+  uint8_t* h_arena = nullptr;  // pinned staging of batch problem images
+  size_t h_arena_cap = 0;
   // Device scratch pool (grow-only size classes, reused across calls; all
   // work of a ctx is ordered on its one stream, so reuse needs no sync).
   std::mutex pool_mu;
@@ -1729,6 +1755,17 @@ int ensure_host(loom_ctx* c, size_t need) {
   c->h_out_cap = 0;
   LOOM_CUDA(cudaMallocHost(&c->h_out, std::max<size_t>(need, 1) * sizeof(Rec)));
   c->h_out_cap = need;
+  return LOOM_OK;
+}
+
+int ensure_host_arena(loom_ctx* c, size_t need) {
+  if (need <= c->h_arena_cap && c->h_arena) return LOOM_OK;
+  if (c->h_arena) cudaFreeHost(c->h_arena);
+  c->h_arena = nullptr;
+  c->h_arena_cap = 0;
+  const size_t cap = std::max<size_t>(need + need / 4, 1 << 20);  // grow with headroom
+  LOOM_CUDA(cudaMallocHost(&c->h_arena, cap));
+  c->h_arena_cap = cap;
   return LOOM_OK;
 }
 
@@ -1855,6 +1892,7 @@ int loom_ctx_destroy(loom_ctx* c) {
   cudaFree(c->d_out);
   for (void* q : c->pool_all) cudaFree(q);
   if (c->h_out) cudaFreeHost(c->h_out);
+  if (c->h_arena) cudaFreeHost(c->h_arena);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return LOOM_OK;
@@ -1949,9 +1987,10 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
       off[j] = arena;
       arena += built[j].blob.size();
     }
-  std::vector<uint8_t> host_arena(arena);
+  if (int rc = ensure_host_arena(c, arena)) return rc;
+  uint8_t* host_arena = c->h_arena;  // pinned: the copy below runs at full link speed
   parallel_for(n_jobs, [&](int j) {
-    if (ok[j]) std::memcpy(host_arena.data() + off[j], built[j].blob.data(), built[j].blob.size());
+    if (ok[j]) std::memcpy(host_arena + off[j], built[j].blob.data(), built[j].blob.size());
   });
   tr.mark("pack");
   if (int rc = ensure(c->d_arena, c->arena_cap, arena)) return rc;
@@ -1960,7 +1999,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
   if (int rc = ensure_tickets(c, static_cast<size_t>(n_jobs))) return rc;
   if (int rc = ensure(c->d_out, c->out_cap, static_cast<size_t>(n_jobs))) return rc;
   if (int rc = ensure_host(c, static_cast<size_t>(n_jobs))) return rc;
-  LOOM_CUDA(cudaMemcpyAsync(c->d_arena, host_arena.data(), arena, cudaMemcpyHostToDevice, c->stream));
+  LOOM_CUDA(cudaMemcpyAsync(c->d_arena, host_arena, arena, cudaMemcpyHostToDevice, c->stream));
   std::vector<JobDesc> all;
   for (auto& g : groups) {
     for (int j : g.jobs) {

@@ -59,6 +59,20 @@ struct alignas(16) BlobHeader {
   uint64_t r_sub;        // plans per subrow = product of the last K-1 radices
   uint64_t n_sub;        // subrows in the whole space = total / r_sub
   uint64_t group;        // subrows per DP group (unit of work dealt to a warp)
+  // Incumbent: every thread starts from the exact record of the greedy
+  // seed plan (node-local minima, loom_greedy_seed) when it lies in the
+  // searched range, so no thread spends its first plans with empty
+  // thresholds -- a job of the multi-tenant batch gives each thread only
+  // ~1,000 plans.  Offering a real plan of the range never changes the argmin.
+  int32_t has_seed;
+  // Energy-then-latency objectives: once a thread's best sits in the lowest
+  // achievable energy bucket (qa_floor = quantize of the dag-order fold of
+  // per-node minima), no plan can beat it on energy, so its fast latency test
+  // tightens from the SLO to the best's latency.
+  int32_t tie_lat;
+  uint64_t seed_index;
+  int64_t qa_floor;
+  int64_t pad_;
 };
 
 // A candidate / winner inside the kernels: the quantized criteria, exact
