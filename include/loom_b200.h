@@ -14,6 +14,9 @@
  *                             applied to estimate(p) for p in ConfigEnumerator order
  *   loom_winner_reduce        objective_less as a total-order reduce (multi-GPU combine)
  *   loom_evaluate_plan        loom::estimate               estimator.hpp:43-78 (one plan)
+ *   loom_estimate_range(_device) / loom_estimate_plans
+ *                             estimate() over an index range / an index list,
+ *                             as per-plan score streams (SoA)
  *   loom_lower                node_options optimizer.hpp:51-107 + plan_node_execution
  *                             chunking.hpp:85-184 + ConfigPoint::identifier config.hpp:49-61
  *   loom_exhaustive_search_json   the whole drop-in call on reference-format JSON
@@ -222,6 +225,34 @@ int loom_search_pareto_points(loom_ctx* ctx, const loom_problem* problem, uint64
 /* pareto_filter on an arbitrary point set (optimizer.hpp:153-171):
  * keep[i] = 1 iff no other point dominates point i.  Runs on the device. */
 int loom_pareto_filter_points(loom_ctx* ctx, const loom_point* points, uint64_t n, uint8_t* keep);
+
+/* ---- per-plan estimate streams (estimator.hpp:43-78) ----------------------- */
+/* Structure-of-arrays score streams: element i holds one field of
+ * estimate(plan) (ConfigEstimate, estimator.hpp:20-30).  A NULL stream is not
+ * written (and costs no memory traffic). */
+typedef struct loom_estimate_streams {
+  int64_t* latency_us;
+  double* gpu_wh;
+  double* cpu_wh;
+  double* total_wh;
+  double* dollars;
+  int32_t* quality;
+} loom_estimate_streams;
+
+/* estimate(p) for every plan p in [begin, end) (end clamped to the total) in
+ * ConfigEnumerator order (optimizer.hpp:131-143): element i = plan begin + i.
+ * The reference's equivalent is a loop of ConfigEnumerator::next + estimate.
+ * HOST arrays, filled when the call returns. */
+int loom_estimate_range(loom_ctx* ctx, const loom_problem* problem, uint64_t begin, uint64_t end,
+                        const loom_estimate_streams* out);
+/* Same into DEVICE arrays on the ctx's device, enqueued on the ctx stream
+ * without synchronising (16-byte aligned arrays leave through TMA bulk stores). */
+int loom_estimate_range_device(loom_ctx* ctx, const loom_problem* problem, uint64_t begin, uint64_t end,
+                               const loom_estimate_streams* out);
+/* Batched estimate of arbitrary plans: element i =
+ * estimate(indices[i]); LOOM_INVALID if an index is out of range.  HOST arrays. */
+int loom_estimate_plans(loom_ctx* ctx, const loom_problem* problem, const uint64_t* indices, uint64_t n,
+                        const loom_estimate_streams* out);
 
 /* ---- greedy_search (optimizer.hpp:227-291) -------------------------------- */
 /* Node-local seed of greedy_search (optimizer.hpp:194-220, 256-268): per node,

@@ -29,7 +29,7 @@ CU_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xptxas", "-v",
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              "-Wno-unused-parameter", *INCLUDES, "-I", "/usr/local/cuda/include"]
 
-CU_SOURCES = ["loom_search.cu"]
+CU_SOURCES = ["loom_search.cu", "loom_scores.cu"]
 CXX_SOURCES = ["loom_capi.cpp", "loom_host.cpp", "json.cpp"]
 
 

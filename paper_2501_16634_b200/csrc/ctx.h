@@ -1,0 +1,107 @@
+// The device context (loom_ctx of the C ABI) and its scratch pool, shared by
+// the kernel translation units of libloom_b200.so.  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "loom_b200.h"
+#include "search_common.h"
+
+struct loom_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sms = 148;
+  uint64_t launches = 0;
+  // scratch reused across calls
+  uint8_t* d_arena = nullptr;
+  size_t arena_cap = 0;
+  loomk::JobDesc* d_jobs = nullptr;
+  size_t jobs_cap = 0;
+  loomk::Rec* d_scratch = nullptr;
+  size_t scratch_cap = 0;
+  loomk::JobSync* d_tickets = nullptr;
+  size_t tickets_cap = 0;
+  loomk::Rec* d_out = nullptr;
+  size_t out_cap = 0;
+  loomk::Rec* h_out = nullptr;  // pinned
+  size_t h_out_cap = 0;
+  uint8_t* h_arena = nullptr;  // pinned staging of batch problem images
+  size_t h_arena_cap = 0;
+  // Device scratch pool (grow-only size classes, reused across calls; all
+  // work of a ctx is ordered on its one stream, so reuse needs no sync).
+  std::mutex pool_mu;
+  std::multimap<size_t, void*> pool_free;
+  std::vector<void*> pool_all;
+  // last Pareto frontier (size-query-then-fill without a second search)
+  std::vector<loom_point> pareto_cache;
+  uint64_t pareto_key = 0;
+  bool pareto_valid = false;
+};
+
+namespace loomi {
+
+inline int cuda_fail(cudaError_t e, const char* what) {
+  return loomi::fail(LOOM_DEVICE_ERROR, std::string("DeviceError: ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DevBuf {
+  // Scratch from the ctx's pool (returned on scope exit, freed with the ctx).
+  explicit DevBuf(loom_ctx* ctx) : c(ctx) {}
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  loom_ctx* c;
+  T* p = nullptr;
+  size_t cls = 0;
+  ~DevBuf() {
+    if (p) {
+      std::lock_guard<std::mutex> g(c->pool_mu);
+      c->pool_free.emplace(cls, p);
+    }
+  }
+  cudaError_t alloc(size_t n) {
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    // size classes: powers of two up to 4 MiB, then multiples of 4 MiB
+    size_t k = 256;
+    if (bytes <= (size_t(4) << 20)) {
+      while (k < bytes) k <<= 1;
+    } else {
+      k = (bytes + (size_t(4) << 20) - 1) & ~((size_t(4) << 20) - 1);
+    }
+    {
+      std::lock_guard<std::mutex> g(c->pool_mu);
+      auto it = c->pool_free.find(k);
+      if (it != c->pool_free.end()) {
+        p = static_cast<T*>(it->second);
+        c->pool_free.erase(it);
+        cls = k;
+        return cudaSuccess;
+      }
+    }
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, k);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(c->pool_mu);
+    c->pool_all.push_back(q);
+    p = static_cast<T*>(q);
+    cls = k;
+    return cudaSuccess;
+  }
+};
+
+}  // namespace loomi
+
+#define LOOM_CUDA(call)                                          \
+  do {                                                           \
+    cudaError_t e_ = (call);                                     \
+    if (e_ != cudaSuccess) return loomi::cuda_fail(e_, #call);   \
+  } while (0)

@@ -54,8 +54,12 @@
 #include "internal.h"
 #include "loom_b200.h"
 #include "search_common.h"
+#include "ctx.h"
+#include "tma.cuh"
 
 using namespace loomk;
+using loomi::DevBuf;
+using loomi::cuda_fail;
 
 namespace {
 
@@ -119,38 +123,6 @@ __device__ __forceinline__ View make_view(const uint8_t* s) {
   v.q = reinterpret_cast<const int32_t*>(s + v.h->off_q);
   v.inner = reinterpret_cast<const InnerEntry*>(s + v.h->off_inner);
   return v;
-}
-
-// The problem image arrives in shared memory through one TMA bulk copy
-// (cp.async.bulk, SASS UBLKCP) completing on an mbarrier.
-__device__ __forceinline__ void load_blob(uint8_t* smem, const uint8_t* g, uint32_t bytes, uint64_t* mbar) {
-  const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
-  const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-    constexpr uint32_t kChunk = 16384;
-    for (uint32_t off = 0; off < bytes; off += kChunk) {
-      const uint32_t n = min(kChunk, bytes - off);
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + off),
-          "l"(g + off), "r"(n), "r"(mb)
-          : "memory");
-    }
-  }
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "LOOM_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-      "@!p bra LOOM_WAIT_%=;\n"
-      "}\n" ::"r"(mb)
-      : "memory");
 }
 
 __device__ __forceinline__ bool rec_better(const Rec& a, const Rec& b, const BlobHeader* h) {
@@ -1662,37 +1634,6 @@ JobDesc make_desc(const Built& b, uint64_t begin, uint64_t end, bool full_eval_o
 // ---------------------------------------------------------------------------
 // context + C ABI
 // ---------------------------------------------------------------------------
-struct loom_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  int sms = 148;
-  uint64_t launches = 0;
-  // scratch reused across calls
-  uint8_t* d_arena = nullptr;
-  size_t arena_cap = 0;
-  JobDesc* d_jobs = nullptr;
-  size_t jobs_cap = 0;
-  Rec* d_scratch = nullptr;
-  size_t scratch_cap = 0;
-  JobSync* d_tickets = nullptr;
-  size_t tickets_cap = 0;
-  Rec* d_out = nullptr;
-  size_t out_cap = 0;
-  Rec* h_out = nullptr;  // pinned
-  size_t h_out_cap = 0;
-  uint8_t* h_arena = nullptr;  // pinned staging of batch problem images
-  size_t h_arena_cap = 0;
-  // Device scratch pool (grow-only size classes, reused across calls; all
-  // work of a ctx is ordered on its one stream, so reuse needs no sync).
-  std::mutex pool_mu;
-  std::multimap<size_t, void*> pool_free;
-  std::vector<void*> pool_all;
-  // last Pareto frontier (size-query-then-fill without a second search)
-  std::vector<loom_point> pareto_cache;
-  uint64_t pareto_key = 0;
-  bool pareto_valid = false;
-};
 
 struct loom_device_problem {
   loom_ctx* ctx = nullptr;
@@ -1716,15 +1657,6 @@ struct loom_device_problem {
 
 namespace {
 
-int cuda_fail(cudaError_t e, const char* what) {
-  return loomi::fail(LOOM_DEVICE_ERROR, std::string("DeviceError: ") + what + ": " + cudaGetErrorString(e));
-}
-
-#define LOOM_CUDA(call)                                   \
-  do {                                                    \
-    cudaError_t e_ = (call);                              \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
-  } while (0)
 
 template <class T>
 int ensure(T*& ptr, size_t& cap, size_t need) {
@@ -2148,50 +2080,6 @@ namespace {
 
 static_assert(sizeof(ParetoPoint) == sizeof(loom_point), "ParetoPoint must match loom_point");
 
-template <class T>
-struct DevBuf {
-  // Scratch from the ctx's pool (returned on scope exit, freed with the ctx).
-  explicit DevBuf(loom_ctx* ctx) : c(ctx) {}
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  loom_ctx* c;
-  T* p = nullptr;
-  size_t cls = 0;
-  ~DevBuf() {
-    if (p) {
-      std::lock_guard<std::mutex> g(c->pool_mu);
-      c->pool_free.emplace(cls, p);
-    }
-  }
-  cudaError_t alloc(size_t n) {
-    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
-    // size classes: powers of two up to 4 MiB, then multiples of 4 MiB
-    size_t k = 256;
-    if (bytes <= (size_t(4) << 20)) {
-      while (k < bytes) k <<= 1;
-    } else {
-      k = (bytes + (size_t(4) << 20) - 1) & ~((size_t(4) << 20) - 1);
-    }
-    {
-      std::lock_guard<std::mutex> g(c->pool_mu);
-      auto it = c->pool_free.find(k);
-      if (it != c->pool_free.end()) {
-        p = static_cast<T*>(it->second);
-        c->pool_free.erase(it);
-        cls = k;
-        return cudaSuccess;
-      }
-    }
-    void* q = nullptr;
-    const cudaError_t e = cudaMalloc(&q, k);
-    if (e != cudaSuccess) return e;
-    std::lock_guard<std::mutex> g(c->pool_mu);
-    c->pool_all.push_back(q);
-    p = static_cast<T*>(q);
-    cls = k;
-    return cudaSuccess;
-  }
-};
 
 uint64_t fnv(uint64_t h, const void* data, size_t n) {
   const uint8_t* b = static_cast<const uint8_t*>(data);

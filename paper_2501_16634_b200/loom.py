@@ -123,6 +123,16 @@ class Point(C.Structure):
 assert C.sizeof(Point) == 40
 
 
+class EstimateStreams(C.Structure):
+    _fields_ = [("latency_us", C.c_void_p), ("gpu_wh", C.c_void_p), ("cpu_wh", C.c_void_p),
+                ("total_wh", C.c_void_p), ("dollars", C.c_void_p), ("quality", C.c_void_p)]
+
+
+# ConfigEstimate fields of a score stream and their element types
+STREAM_FIELDS = {"latency_us": "int64", "gpu_wh": "float64", "cpu_wh": "float64", "total_wh": "float64",
+                 "dollars": "float64", "quality": "int32"}
+
+
 _lib = None
 
 
@@ -171,6 +181,9 @@ def lib() -> C.CDLL:
         "loom_search_pareto_points": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(Point), C.c_uint64,
                                        C.POINTER(C.c_uint64)], C.c_int),
         "loom_pareto_filter_points": ([vp, C.POINTER(Point), C.c_uint64, C.POINTER(C.c_uint8)], C.c_int),
+        "loom_estimate_range": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(EstimateStreams)], C.c_int),
+        "loom_estimate_range_device": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(EstimateStreams)], C.c_int),
+        "loom_estimate_plans": ([vp, P, C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(EstimateStreams)], C.c_int),
         "loom_greedy_seed": ([P, O, C.POINTER(C.c_int32)], C.c_int),
         "loom_search_greedy": ([vp, P, O, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, W], C.c_int),
         "loom_lowered_sweep_order": ([vp, C.POINTER(C.c_int32)], C.c_int),
@@ -516,6 +529,54 @@ def pareto_filter_points(ctx: Context, points: Sequence[dict]) -> list[bool]:
 
 # ---- the drop-in call ----------------------------------------------------
 _default_ctx: Context | None = None
+
+
+# ---- per-plan estimate streams (estimator.hpp:43-78) --------------------------
+def _streams_struct(arrays: dict, ptr) -> EstimateStreams:
+    st = EstimateStreams()
+    for k, a in arrays.items():
+        if k not in STREAM_FIELDS:
+            raise ValueError(f"unknown estimate stream {k!r}")
+        setattr(st, k, ptr(a))
+    return st
+
+
+def estimate_range(ctx: Context, problem: Problem, begin: int, end: int,
+                   fields: Sequence[str] = tuple(STREAM_FIELDS)) -> dict:
+    """estimate(p) for every plan p in [begin, end) (ConfigEnumerator order),
+    as numpy arrays keyed by ConfigEstimate field.  Host arrays."""
+    import numpy as np
+    n = max(0, end - begin)
+    out = {k: np.empty(n, dtype=STREAM_FIELDS[k]) for k in fields}
+    st = _streams_struct(out, lambda a: a.ctypes.data)
+    _check(lib().loom_estimate_range(ctx.handle, C.byref(problem), begin, end, C.byref(st)))
+    return out
+
+
+def estimate_range_device(ctx: Context, problem: Problem, begin: int, end: int, tensors: dict) -> None:
+    """Same into device tensors (torch, on the ctx's device), enqueued on the
+    ctx stream without synchronising."""
+    st = _streams_struct(tensors, lambda t: t.data_ptr())
+    _check(lib().loom_estimate_range_device(ctx.handle, C.byref(problem), begin, end, C.byref(st)))
+
+
+def estimate_range_host(ctx: Context, problem: Problem, begin: int, end: int, tensors: dict) -> None:
+    """Same into caller-owned host tensors (e.g. pinned torch CPU tensors);
+    returns when they are filled."""
+    st = _streams_struct(tensors, lambda t: t.data_ptr())
+    _check(lib().loom_estimate_range(ctx.handle, C.byref(problem), begin, end, C.byref(st)))
+
+
+def estimate_plans(ctx: Context, problem: Problem, indices: Sequence[int],
+                   fields: Sequence[str] = tuple(STREAM_FIELDS)) -> dict:
+    """Batched estimate of arbitrary plan indices (element i = plan indices[i])."""
+    import numpy as np
+    idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
+    out = {k: np.empty(len(idx), dtype=STREAM_FIELDS[k]) for k in fields}
+    st = _streams_struct(out, lambda a: a.ctypes.data)
+    _check(lib().loom_estimate_plans(ctx.handle, C.byref(problem), idx.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                     len(idx), C.byref(st)))
+    return out
 
 
 def default_context() -> Context:
