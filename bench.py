@@ -393,7 +393,59 @@ def other_configs(ctx, loom, W) -> dict:
     t5 = time.perf_counter() - t0
     out["c5"] = {"plans": lw5.total, "frontier_points": len(front), "time_to_frontier_ms": 1e3 * t5,
                  "plans_per_s": lw5.total / t5}
+    out["c3_score_stream"] = score_stream(ctx, loom, W)
     return out
+
+
+def score_stream(ctx, loom, W, log2: int = 28) -> dict:
+    """Per-plan estimate streams (loom_estimate_range_device): estimate() of
+    2^28 consecutive C3 plans written to HBM as six SoA streams (44 B/plan,
+    11.8 GB per launch, larger than L2).  HBM-bound: the roofline is the
+    measured copy bandwidth.  e2e = the host-buffer call (kernel + D2H of
+    every stream into pinned memory)."""
+    import torch
+    w = W.config3()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    n, b = 1 << log2, 1000
+    dt = {"int64": torch.int64, "float64": torch.float64, "int32": torch.int32}
+    dev = {f: torch.empty(n, dtype=dt[t], device="cuda") for f, t in loom.STREAM_FIELDS.items()}
+    bpp = sum(t.element_size() for t in dev.values())
+    stream = torch.cuda.current_stream()
+    sctx = loom.Context(torch.cuda.current_device(), stream.cuda_stream)
+    loom.estimate_range_device(sctx, lw.problem, b, b + n, dev)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        loom.estimate_range_device(sctx, lw.problem, b, b + n, dev)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms) / 1e3
+    # spot-check a few plans against the host's exact per-plan estimate
+    for k in (0, n // 3, n - 1):
+        ref = lw.evaluate(b + k)
+        assert dev["latency_us"][k].item() == ref["latency_us"] and dev["gpu_wh"][k].item() == ref["gpu_wh"]
+    del dev
+    nh = 1 << 24
+    host = {f: torch.empty(nh, dtype=dt[t_], pin_memory=True) for f, t_ in loom.STREAM_FIELDS.items()}
+    loom.estimate_range_host(sctx, lw.problem, b, b + nh, host)
+    th = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        loom.estimate_range_host(sctx, lw.problem, b, b + nh, host)
+        th.append(time.perf_counter() - t0)
+    sctx.close()
+    hbm = peaks().get("hbm_gbs", 6548.5)
+    gbs = n * bpp / t / 1e9
+    return {"plans": n, "bytes_per_plan": bpp, "ms": 1e3 * t, "plans_per_s": n / t,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                         "traffic_per_plan_bytes": bpp},
+            "e2e": {"plans": nh, "ms": 1e3 * min(th), "plans_per_s": nh / min(th),
+                    "d2h_gbs": nh * bpp / min(th) / 1e9, "d2h_bytes": nh * bpp,
+                    "path": "loom_estimate_range into pinned host arrays (kernel + D2H per 4M-plan chunk)"}}
+
 
 
 def main() -> None:

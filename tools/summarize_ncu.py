@@ -50,18 +50,19 @@ for (i, name), m in launch.items():
 summary["launch_time_share"] = {k: round(v / total_ns, 4) for k, v in sorted(kern_ns.items(), key=lambda x: -x[1])}
 summary["launches"] = len(launch)
 
-# full capture
-rep = src / "prof_full.ncu-rep"
-if rep.exists():
+# full captures
+KEEP = ["Duration", "Elapsed Cycles", "SM Frequency", "Compute (SM) Throughput", "Memory Throughput",
+        "DRAM Throughput", "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread",
+        "Achieved Occupancy", "Theoretical Occupancy", "Achieved Active Warps Per SM", "Executed Instructions",
+        "Warp Cycles Per Issued Instruction", "Eligible Warps Per Scheduler", "Branch Efficiency",
+        "Dynamic Shared Memory Per Block", "Grid Size", "Block Size", "L1/TEX Hit Rate", "L2 Hit Rate"]
+
+
+def full_summary(rep: Path, name: str) -> dict:
     det = subprocess.run(["ncu", "-i", str(rep), "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    keep = ["Duration", "Elapsed Cycles", "SM Frequency", "Compute (SM) Throughput", "Memory Throughput",
-            "DRAM Throughput", "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread",
-            "Achieved Occupancy", "Theoretical Occupancy", "Achieved Active Warps Per SM", "Executed Instructions",
-            "Warp Cycles Per Issued Instruction", "Eligible Warps Per Scheduler", "Branch Efficiency",
-            "Dynamic Shared Memory Per Block", "Grid Size", "Block Size", "L1/TEX Hit Rate", "L2 Hit Rate"]
     lines = []
     for r in csv.DictReader(det.splitlines()):
-        if r.get("Metric Name") in keep:
+        if r.get("Metric Name") in KEEP:
             lines.append(f'{r["Section Name"][:34]:34s} {r["Metric Name"][:40]:40s} {r["Metric Value"]:>16s} {r["Metric Unit"]}')
     src_csv = subprocess.run(["ncu", "-i", str(rep), "--page", "source", "--csv"], capture_output=True,
                              text=True).stdout.splitlines()
@@ -80,7 +81,30 @@ if rep.exists():
             lines.append(f"  {k:32s} {100 * v / tot:5.1f}%")
     except StopIteration:
         pass
-    (out / "search_kernel_full.txt").write_text("\n".join(lines) + "\n")
+    (out / name).write_text("\n".join(lines) + "\n")
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    vals = {}
+    if len(rr) >= 3:
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "": 1}
+        for k, u, v in zip(rr[0], rr[1], rr[2]):
+            if k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "smsp__inst_executed.sum"):
+                vals[k] = float(v.replace(",", "")) * scale.get(u, 1)
+    return vals
+
+
+if (src / "prof_full.ncu-rep").exists():
+    full_summary(src / "prof_full.ncu-rep", "search_kernel_full.txt")
+if (src / "prof_scores.ncu-rep").exists():
+    # tools/time_scores.py --log2 26: 2^26 C3 plans, six streams, 44 B per plan
+    v = full_summary(src / "prof_scores.ncu-rep", "score_kernel_full.txt")
+    plans = 1 << 26
+    if v:
+        summary["score_stream"] = {
+            "plans_per_launch": plans, "algorithmic_bytes_per_launch": plans * 44,
+            "dram_bytes_per_launch": v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0),
+            "launch_ns_cold": v.get("gpu__time_duration.sum"),
+            "thread_inst_per_plan": v.get("smsp__inst_executed.sum", 0) * 32 / plans}
 if (src / "bench.json").exists():
     shutil.copy(src / "bench.json", out / "bench.json")
 (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
