@@ -69,6 +69,9 @@ constexpr int64_t kNeg = -(int64_t(1) << 62);
 #define LOOM_PAIR_UNROLL 2
 #endif
 constexpr int kPairUnroll = LOOM_PAIR_UNROLL;
+#ifndef LOOM_ENERGY_FIRST
+#define LOOM_ENERGY_FIRST 1
+#endif
 
 // ---------------------------------------------------------------------------
 // device helpers
@@ -400,6 +403,10 @@ struct Inner {
   // table entry j: kernel parameter (PT) or register copy
   __device__ __forceinline__ double G(const InnerParams& ip, int j) const { return PT ? ip.g[j] : g[PT ? 0 : j]; }
   __device__ __forceinline__ int32_t W(const InnerParams& ip, int j) const { return PT ? ip.w[j] : w[PT ? 0 : j]; }
+  // high word of g (a register half for the register table)
+  __device__ __forceinline__ int32_t GH(const InnerParams& ip, int j) const {
+    return PT ? ip.gh[j] : __double2hiint(g[PT ? 0 : j]);
+  }
 
   __device__ __forceinline__ void load(const Hot& H) {
     if constexpr (NV > 0 && !PT) {
@@ -423,6 +430,32 @@ struct Inner {
   __device__ __forceinline__ bool pass_bound(int32_t w_, double g_, int32_t tw, double tu) const {
     if (PRIM == kPrimFp) return (w_ <= tw) & (g_ <= tu);
     return w_ <= tw;
+  }
+
+  // Energy-first fast test of two contexts: can any plan of either context
+  // tie or beat the running best on the primary FP criterion?  A plan whose
+  // energy is worse than the best's cannot be selected whatever its latency
+  // (objective_less compares the primary criterion first, estimator.hpp:
+  // 98-112), so its one test decides it; the few plans that pass are tested
+  // on both criteria in the flagged contexts.  Even options are tested on the
+  // FP64 pipe (DSETP), odd ones on the ALU pipe with the high words
+  // (g <= t => hi(g) <= hi(t) for g >= +0; t < 0 has a negative high word),
+  // so both pipes carry half of the plans.  A superset of the passing plans,
+  // like every fast test.
+  __device__ __forceinline__ bool any_energy2(const InnerParams& ip, double tu0, double tu1) const {
+    const int32_t th0 = __double2hiint(tu0), th1 = __double2hiint(tu1);
+    bool af = false, ai = false;
+#pragma unroll
+    for (int j = 0; j < (NV > 0 ? NV : 1); ++j) {
+      if (j & 1) {
+        ai |= GH(ip, j) <= th0;
+        ai |= GH(ip, j) <= th1;
+      } else {
+        af |= G(ip, j) <= tu0;
+        af |= G(ip, j) <= tu1;
+      }
+    }
+    return af | ai;
   }
 
   // NV > 0: does any plan of the context pass?  (one predicate OR per plan)
@@ -516,15 +549,19 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
         int o = c_lo;
 #pragma unroll kPairUnroll
         for (; o + 1 < c_hi; o += 2, bit <<= 1) {
-          const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
           const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
-          const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
           const double tu0 = ctx_bound(H, eu0), tu1 = ctx_bound(H, eu1);
           bool a = false;
+          if constexpr (PRIM == kPrimFp && LOOM_ENERGY_FIRST) {
+            a = in.any_energy2(ip, tu0, tu1);
+          } else {
+            const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
+            const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
 #pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw0, tu0);
-            a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw1, tu1);
+            for (int j = 0; j < NV; ++j) {
+              a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw0, tu0);
+              a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw1, tu1);
+            }
           }
           // a real (rarely taken) branch keeps the per-plan tests a predicate
           // OR chain; the empty asm stops if-conversion into per-plan selects
@@ -1576,14 +1613,16 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   }
   InnerEntry* inner = reinterpret_cast<InnerEntry*>(base + hd.off_inner);
   for (int o2 = 0; o2 < inner_pad; ++o2) {
-    if (o2 >= p->radix[inner_node]) {  // padding: can never pass the wall test
-      inner[o2].g = 0.0;
+    if (o2 >= p->radix[inner_node]) {  // padding: can never pass the wall (or the energy) test
+      inner[o2].g = INFINITY;
       inner[o2].w = INT_MAX;
       inner[o2].q = INT_MIN;
       continue;
     }
     const int k = optoff[inner_node] + o2;
-    inner[o2].g = ga[k];
+    // an option failing the quality floor can never pass; an infinite g lets
+    // the energy-only fast test see that too (every exact test checks w first)
+    inner[o2].g = floor_ok(k) ? ga[k] : INFINITY;
     inner[o2].w = floor_ok(k) ? static_cast<int32_t>(p->wall_us[k] - wmin) : INT_MAX;
     inner[o2].q = p->quality[k];
   }
@@ -1592,8 +1631,11 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   b.full_only = full_only;
   b.nv = nv;
   for (int j = 0; j < 16; ++j) {
-    b.ip.g[j] = j < inner_pad ? inner[j].g : 0.0;
+    b.ip.g[j] = j < inner_pad ? inner[j].g : INFINITY;
     b.ip.w[j] = j < inner_pad ? inner[j].w : INT_MAX;
+    int64_t bits;
+    std::memcpy(&bits, &b.ip.g[j], sizeof bits);
+    b.ip.gh[j] = static_cast<int32_t>(bits >> 32);
   }
   b.total = total;
   b.r_sub = r_sub;

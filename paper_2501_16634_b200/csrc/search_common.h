@@ -25,7 +25,7 @@ enum Prim : int32_t { kPrimFp = 0, kPrimLat = 1, kPrimQual = 2 };
 
 // Innermost node's option, 16 bytes = one LDS.128 broadcast per plan.
 struct alignas(16) InnerEntry {
-  double g;     // FP_A contribution of this option
+  double g;     // FP_A contribution of this option (+inf when w is INT_MAX)
   int32_t w;    // wall_us - inner_wmin (INT32_MAX if the option fails the quality floor)
   int32_t q;    // node quality
 };
@@ -90,8 +90,9 @@ struct Rec {
 // Innermost table of a single-problem launch, passed as a kernel parameter so
 // the fast path reads it as constant-bank operands instead of registers.
 struct InnerParams {
-  double g[16];
+  double g[16];    // +inf where w is INT_MAX (padding / quality-floor failure)
   int32_t w[16];
+  int32_t gh[16];  // high word of g: g <= t  =>  gh <= hi(t) for g >= 0 (ALU-pipe form of the energy test)
 };
 
 // One plan's Pareto coordinates (40 bytes; same layout as loom_point).
