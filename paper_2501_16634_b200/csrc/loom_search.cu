@@ -69,6 +69,23 @@ constexpr int64_t kNeg = -(int64_t(1) << 62);
 #define LOOM_PAIR_UNROLL 2
 #endif
 constexpr int kPairUnroll = LOOM_PAIR_UNROLL;
+// LOOM_STATS=1 (experiment builds): event counters of the search kernel,
+// read with loom_debug_counters.  0: flagged steps, 1: contexts passing the
+// bound re-test, 2: contexts passing the exact test (slow scans), 3: steps.
+#ifndef LOOM_STATS
+#define LOOM_STATS 0
+#endif
+__device__ unsigned long long g_stats[8];
+#define LOOM_COUNT(i, n)                                      \
+  do {                                                        \
+    if (LOOM_STATS) atomicAdd(&g_stats[i], (unsigned long long)(n)); \
+  } while (0)
+#ifndef LOOM_JOB_BOUND
+#define LOOM_JOB_BOUND 1
+#endif
+#ifndef LOOM_EF_ADAPT
+#define LOOM_EF_ADAPT 0
+#endif
 #ifndef LOOM_ENERGY_FIRST
 #define LOOM_ENERGY_FIRST 1
 #endif
@@ -204,8 +221,23 @@ __device__ __forceinline__ void slot_init(const Slots& s, int t, const BlobHeade
   slot_thresholds(s, t, h);
 }
 
+// Job-wide bound on the primary FP criterion (energy-first objectives): every
+// thread publishes the quantized primary criterion of its feasible bests, and
+// reads the job's minimum at each DP group.  A plan whose bucket is above the
+// minimum is strictly worse than a feasible plan of the searched range, so it
+// cannot be the argmin; the bound only tightens the fast tests.
+__shared__ unsigned long long* s_gbest;
+
+__device__ __forceinline__ void publish_best(const BlobHeader* h, const Rec& c) {
+  if (h->prim == kPrimFp && c.found && s_gbest && c.qa >= 0)
+    atomicMax(s_gbest, static_cast<unsigned long long>(INT64_MAX - c.qa));
+}
+
 __device__ __forceinline__ void slot_offer(const Slots& s, int t, const BlobHeader* h, const Rec& c) {
   if (rec_better(c, slot_load(s, t), h)) {
+    // publish only a strictly better bucket (a handful per thread): ties
+    // improving on latency or rank would hammer one address
+    if (c.found && (!s.found[t] || c.qa < s.qa[t])) publish_best(h, c);
     s.qa[t] = c.qa;
     s.qb[t] = c.qb;
     s.lat[t] = c.lat;
@@ -345,6 +377,8 @@ struct Hot {
   double hi_up;      // the double above hi (see ctx_bound)
   int64_t lat_s;
   int32_t bq;
+  int32_t ef_skip;   // upcoming innermost sweeps to run with the two-criteria test (energy-first was dense)
+  unsigned sync_mask;  // lanes of the warp working on the current subrow step
 };
 
 // The double above x (x itself for +inf).
@@ -543,31 +577,49 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       // the then-current thresholds) and scanned exactly after the loop.
       // Testing with thresholds older than the running best only lets more
       // contexts through, so no candidate is lost.
+      // Energy-first (PRIM == kPrimFp): one compare per plan on the primary
+      // criterion.  Where it passes many contexts (a region whose low-energy
+      // plans are latency-infeasible) the two-criteria test is cheaper; a
+      // sweep that flags >= 3/8 of its steps switches the warp to it for the
+      // next 16 sweeps, then energy-first is probed again.
+      const bool ef = PRIM == kPrimFp && LOOM_ENERGY_FIRST && (!LOOM_EF_ADAPT || __all_sync(__activemask(), H.ef_skip == 0));
       for (int c_lo = o_lo; c_lo < o_hi; c_lo += 64) {
         const int c_hi = min(o_hi, c_lo + 64);
         uint32_t hits = 0, bit = 1;
         int o = c_lo;
+        if (ef) {
 #pragma unroll kPairUnroll
-        for (; o + 1 < c_hi; o += 2, bit <<= 1) {
-          const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
-          const double tu0 = ctx_bound(H, eu0), tu1 = ctx_bound(H, eu1);
-          bool a = false;
-          if constexpr (PRIM == kPrimFp && LOOM_ENERGY_FIRST) {
-            a = in.any_energy2(ip, tu0, tu1);
-          } else {
+          for (; o + 1 < c_hi; o += 2, bit <<= 1) {
+            const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
+            const bool a = in.any_energy2(ip, ctx_bound(H, eu0), ctx_bound(H, eu1));
+            if (__builtin_expect(a, 0)) {
+              asm volatile("");
+              hits |= bit;
+            }
+          }
+          if (LOOM_EF_ADAPT && 2 * __popc(hits) * 8 >= 3 * (c_hi - c_lo)) H.ef_skip = 16;
+          LOOM_COUNT(3, (c_hi - c_lo) / 2);
+          LOOM_COUNT(0, __popc(hits));
+        } else {
+          if (H.ef_skip > 0) --H.ef_skip;
+#pragma unroll kPairUnroll
+          for (; o + 1 < c_hi; o += 2, bit <<= 1) {
             const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
+            const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
             const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
+            const double tu0 = ctx_bound(H, eu0), tu1 = ctx_bound(H, eu1);
+            bool a = false;
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw0, tu0);
               a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw1, tu1);
             }
-          }
-          // a real (rarely taken) branch keeps the per-plan tests a predicate
-          // OR chain; the empty asm stops if-conversion into per-plan selects
-          if (__builtin_expect(a, 0)) {
-            asm volatile("");
-            hits |= bit;
+            // a real (rarely taken) branch keeps the per-plan tests a predicate
+            // OR chain; the empty asm stops if-conversion into per-plan selects
+            if (__builtin_expect(a, 0)) {
+              asm volatile("");
+              hits |= bit;
+            }
           }
         }
         if (o < c_hi) {
@@ -575,16 +627,32 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
           const double eu = __dadd_rn(ea, H.ga[off + o]);
           if (in.any_pass(H, ip, inner_tw(pr, wu), eu, INT_MAX)) hits |= bit;
         }
+        // Flagged steps: the two-criteria bound test per context, then the
+        // exact test, then the exact scan.  The step loop holds no call, so
+        // the table stays in uniform registers across steps; testing with
+        // thresholds older than the running best only lets more through.
         while (__builtin_expect(hits != 0, 0)) {
           const int p = __ffs(hits) - 1;
           hits &= hits - 1;
           for (int oo = c_lo + 2 * p; oo < min(c_hi, c_lo + 2 * p + 2); ++oo) {
             const double eu = __dadd_rn(ea, H.ga[off + oo]);
             const int32_t tw = inner_tw(pr, H.w32[off + oo]);
-            if (in.any_pass(H, ip, tw, eu, INT_MAX)) context_slow(oo, eu, INT_MAX, tw, 0);
+            const double tu = ctx_bound(H, eu);
+            bool b = false;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) b |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw, tu);
+            if (b) LOOM_COUNT(1, 1);
+            if (b && in.any_pass(H, ip, tw, eu, INT_MAX)) {
+              LOOM_COUNT(2, 1);
+              context_slow(oo, eu, INT_MAX, tw, 0);
+            }
           }
         }
       }
+      // Reconverge after the (divergent) flagged-context work: left alone,
+      // the lanes that took the slow path and the ones that did not keep
+      // running the step loop as separate groups, issuing it twice.
+      __syncwarp(H.sync_mask);
     } else {
       for (int o = o_lo; o < o_hi; ++o) {
         const int32_t wu = H.w32[off + o];
@@ -605,6 +673,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
           }
         }
       }
+      __syncwarp(H.sync_mask);
     }
   } else {
     constexpr int NS = 1 << (K - J - 1);
@@ -688,6 +757,7 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
   H.inner = v.inner;
   H.P = v.h->n_nodes - K;
   H.od[0] = H.od[1] = H.od[2] = H.od[3] = 0;
+  H.ef_skip = 0;
   reload(H);
   Inner<K, PRIM, NV, PT> in;
   in.load(H);
@@ -705,7 +775,15 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
   int32_t q_pre = INT_MAX;
   uint64_t lex_pre = 0;
   bool fresh_row = true;
-  for (uint64_t s = s_begin; s < s_end; ++s) {
+  // Every lane of the warp runs the same number of steps (lanes with fewer
+  // subrows idle through the last one), so the sweeps can reconverge with
+  // __syncwarp(sync_mask).
+  const unsigned n_mine = static_cast<unsigned>(s_end - s_begin);
+  const unsigned n_steps = __reduce_max_sync(0xffffffffu, n_mine);
+  uint64_t s = s_begin;
+  for (unsigned step = 0; step < n_steps; ++step) {
+    H.sync_mask = __ballot_sync(0xffffffffu, step < n_mine);
+    if (step >= n_mine) continue;
     if (fresh_row) {
       if (P == 0) {
 #pragma unroll 1
@@ -731,6 +809,7 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
       fresh_row = true;
       if (P >= 1) ++d[P - 1];
     }
+    ++s;
   }
 }
 
@@ -794,7 +873,8 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
   const int job = blockIdx.x / ctas_per_job;
   const int part = blockIdx.x % ctas_per_job;
   const JobDesc jd = jobs[job];
-  load_blob(smem, arena + jd.blob_off, jd.blob_bytes, &mbar);
+  if (threadIdx.x == 0) s_gbest = LOOM_JOB_BOUND ? &sync[job].best_neg : nullptr;
+  load_blob(smem, arena + jd.blob_off, jd.blob_bytes, &mbar);  // (its __syncthreads publishes s_gbest)
   const View v = make_view(smem);
   const BlobHeader* h = v.h;
   uint8_t* slot_base = smem + ((jd.blob_bytes + 127) & ~127u);
@@ -838,9 +918,19 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
     // the exact slow path is data dependent, so a static split would leave
     // warps idle at the end.
     auto next_group = [&]() -> uint64_t {
-      unsigned long long x = 0;
-      if (lane == 0) x = atomicAdd(&sync[job].next_group, 1ull);
-      return g_first + __shfl_sync(0xffffffffu, x, 0);
+      unsigned long long x = 0, gb = 0;
+      if (lane == 0) {
+        x = atomicAdd(&sync[job].next_group, 1ull);
+        if (s_gbest) gb = __ldcg(s_gbest);
+      }
+      x = __shfl_sync(0xffffffffu, x, 0);
+      gb = __shfl_sync(0xffffffffu, gb, 0);
+      // tighten this thread's energy bound to the job's best bucket
+      if (gb != 0) {
+        const double hg = hi_of(INT64_MAX - static_cast<int64_t>(gb));
+        if (hg < sl.hi[threadIdx.x]) sl.hi[threadIdx.x] = hg;
+      }
+      return g_first + x;
     };
     for (uint64_t g = next_group(); g < g_end; g = next_group()) {
       // digits of nodes [0, P-1) shared by the group, and their folds
@@ -865,8 +955,8 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
       const uint64_t lo = max(g * G, jd.sub_lo), hi = min((g + 1) * G, jd.sub_hi);
       const uint64_t len = hi - lo;
       const uint64_t a = lo + len * lane / 32, b = lo + len * (lane + 1) / 32;
-      if (a < b)
-        run_subrows<K, PRIM, NV, PT>(smem, slot_base, coef_base, v, ip, a, b, dtop, cw, ea_top, q_top, lex_top);
+      // every lane enters (an empty run just joins the warp's step syncs)
+      run_subrows<K, PRIM, NV, PT>(smem, slot_base, coef_base, v, ip, a, b, dtop, cw, ea_top, q_top, lex_top);
       __syncwarp();
     }
   }
@@ -891,6 +981,7 @@ __global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
       out[job] = acc;
       sync[job].ticket = 0;
       sync[job].next_group = 0;
+      sync[job].best_neg = 0;
     }
   }
 }
@@ -1824,6 +1915,17 @@ int finish_winner(const loom_problem* p, const Rec& r, loom_winner* out) {
 }  // namespace
 
 extern "C" {
+
+// Experiment builds (LOOM_STATS=1): copy (and optionally reset) the search
+// kernel's event counters.  Not part of the public ABI.
+int loom_debug_counters(uint64_t* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_stats, sizeof(uint64_t) * 8) != cudaSuccess) return LOOM_DEVICE_ERROR;
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(g_stats, z, sizeof z) != cudaSuccess) return LOOM_DEVICE_ERROR;
+  }
+  return LOOM_OK;
+}
 
 int loom_ctx_create(int32_t device, void* cuda_stream, loom_ctx** out) {
   if (!out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null out");

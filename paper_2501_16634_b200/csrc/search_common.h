@@ -106,12 +106,16 @@ struct ParetoPoint {
 };
 
 // Per-job device counters (global memory, zero between launches): the CTA
-// arrival ticket of the final reduction and the next DP group to deal out.
-// The last CTA to arrive resets both.
+// arrival ticket of the final reduction, the next DP group to deal out and the
+// job-wide energy bound.  The last CTA to arrive resets them.
 struct alignas(16) JobSync {
   unsigned ticket;
   unsigned pad;
   unsigned long long next_group;
+  // INT64_MAX - (quantized primary FP criterion of the best feasible plan
+  // found by any thread of the job so far); 0 = none.  atomicMax only.
+  unsigned long long best_neg;
+  unsigned long long pad2;
 };
 
 // Per-job launch descriptor (global memory).
