@@ -333,10 +333,12 @@ def b200_arm(args) -> None:
 
 # Compiled fast path of the innermost contexts of search_kernel<4, kPrimFp,
 # 16, true> (tools/sass_hot.py 4 0 16 1): per 64 plans per lane (two
-# unrolled two-context steps), 211 SASS instructions -- 64 DSETP, 69 ISETP,
-# 32 PLOP3, 12 LDCU, 8 LDS, 8 DADD, loop control -- of which 112 run on the
-# ALU pipe and 72 on the FP64 pipe.  DESIGN.md §5.
-FAST_PATH = {"issue": 211, "alu": 112, "fp64": 72, "plans_per_lane": 64}
+# unrolled steps of two contexts), 108 SASS instructions -- 28 DSETP and 27
+# ISETP (the energy-first test: half the options on the FP64 pipe, half on
+# the ALU pipe with high words), 8 DADD, 13 LDCU, 4 LDS, loop control -- of
+# which 34 run on the ALU pipe and 36 on the FP64 pipe: issue-bound.
+# DESIGN.md §5.
+FAST_PATH = {"issue": 108, "alu": 34, "fp64": 36, "plans_per_lane": 64}
 
 
 def other_configs(ctx, loom, W) -> dict:

@@ -83,9 +83,6 @@ __device__ unsigned long long g_stats[8];
 #ifndef LOOM_JOB_BOUND
 #define LOOM_JOB_BOUND 1
 #endif
-#ifndef LOOM_EF_ADAPT
-#define LOOM_EF_ADAPT 0
-#endif
 #ifndef LOOM_ENERGY_FIRST
 #define LOOM_ENERGY_FIRST 1
 #endif
@@ -377,7 +374,6 @@ struct Hot {
   double hi_up;      // the double above hi (see ctx_bound)
   int64_t lat_s;
   int32_t bq;
-  int32_t ef_skip;   // upcoming innermost sweeps to run with the two-criteria test (energy-first was dense)
   unsigned sync_mask;  // lanes of the warp working on the current subrow step
 };
 
@@ -536,6 +532,30 @@ __device__ __forceinline__ int64_t* coef_col(uint8_t* coef_base, int J) {
 
 constexpr int kCoefEntries = 8 + 4;  // K = 4: levels 1 and 2
 
+// The suffix-level-J input coefficient vector (entries 0..3 are all the
+// innermost pair needs), folded from the row's level-0 vector through the
+// digits of suffix levels 0..J-1.  Energy-first sweeps need latency only in
+// flagged contexts, so they skip the per-level folds and call this instead.
+// Energy-first sweeps (register / parameter innermost table) fold latency
+// coefficients only for flagged contexts.
+template <int PRIM, int NV>
+constexpr bool kLazyCoef = PRIM == kPrimFp && NV > 0 && LOOM_ENERGY_FIRST;
+
+template <int K>
+__device__ __noinline__ void lazy_coef(const int64_t* c0, const int64_t* wall, const int32_t* optoff, int P, int J,
+                                       int o0, int o1, int64_t* out) {
+  int64_t v[1 << K];
+#pragma unroll
+  for (int S = 0; S < (1 << K); ++S) v[S] = c0[S];
+  int ns = 1 << K;
+  for (int jj = 0; jj < J; ++jj) {
+    const int64_t w = wall[optoff[P + jj] + (jj == 0 ? o0 : o1)];
+    ns >>= 1;
+    for (int S = 0; S < ns; ++S) v[S] = max(v[2 * S], v[2 * S + 1] + w);
+  }
+  for (int S = 0; S < 4; ++S) out[S * kBlock] = v[S];  // the level's coefficient column
+}
+
 template <int K, int PRIM, int NV, bool PT, int J>
 __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, const InnerParams& ip, double ea,
                                       int32_t qv, uint64_t lex,
@@ -550,8 +570,24 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
   if constexpr (J == K - 2) {
     const int n_in = H.radix[node + 1];
     const int64_t wmin = H.h->inner_wmin, wu_max = H.h->pre_wmax;
-    const int64_t c[4] = {cin[0], cin[SI], cin[2 * SI], cin[3 * SI]};
-    PreInner pr = pre_inner(c, H.lat_s, wmin, wu_max);
+    // The pair's coefficient vector is the level's input column; lazy
+    // (energy-first) sweeps fill that column on the first flagged context.
+    PreInner pr{};
+    bool have_c = !kLazyCoef<PRIM, NV>;
+    auto cvec = [&]() {
+      const int64_t cc[4] = {cin[0], cin[SI], cin[2 * SI], cin[3 * SI]};
+      pr = pre_inner(cc, H.lat_s, wmin, wu_max);
+    };
+    if constexpr (!kLazyCoef<PRIM, NV>) cvec();
+    auto need_c = [&]() {
+      if constexpr (kLazyCoef<PRIM, NV>) {
+        if (!have_c) {
+          if (J > 0) lazy_coef<K>(H.c0, H.wall, H.optoff, H.P, J, H.od[0], H.od[1], const_cast<int64_t*>(cin));
+          cvec();
+          have_c = true;
+        }
+      }
+    };
     // Exact slow path of one context (rare).
     auto context_slow = [&](int o, double eu, int32_t qu, int32_t tw, int g0) {
       H.od[J] = o;
@@ -565,8 +601,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       slow_scan<K, PRIM>(H.smem, H.slot_base, H.dpre, H.P, H.od[0], H.od[1], H.od[2], g0, g0 + (NV > 0 ? NV : 8), tw,
                          eu, qu, lex_u, X, Y, H.s_index * H.h->r_sub + inner_base);
       reload(H);  // the latency bound may have tightened (latency primary, or an energy tie at the floor)
-      const int64_t cc[4] = {cin[0], cin[SI], cin[2 * SI], cin[3 * SI]};
-      pr = pre_inner(cc, H.lat_s, wmin, wu_max);
+      cvec();
     };
     if constexpr (NV > 0) {
       // Two contexts per step share the innermost table: twice the
@@ -578,16 +613,13 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       // Testing with thresholds older than the running best only lets more
       // contexts through, so no candidate is lost.
       // Energy-first (PRIM == kPrimFp): one compare per plan on the primary
-      // criterion.  Where it passes many contexts (a region whose low-energy
-      // plans are latency-infeasible) the two-criteria test is cheaper; a
-      // sweep that flags >= 3/8 of its steps switches the warp to it for the
-      // next 16 sweeps, then energy-first is probed again.
-      const bool ef = PRIM == kPrimFp && LOOM_ENERGY_FIRST && (!LOOM_EF_ADAPT || __all_sync(__activemask(), H.ef_skip == 0));
+      // criterion (any_energy2); other objectives test both criteria per plan.
+      constexpr bool ef = kLazyCoef<PRIM, NV>;
       for (int c_lo = o_lo; c_lo < o_hi; c_lo += 64) {
         const int c_hi = min(o_hi, c_lo + 64);
         uint32_t hits = 0, bit = 1;
         int o = c_lo;
-        if (ef) {
+        if constexpr (ef) {
 #pragma unroll kPairUnroll
           for (; o + 1 < c_hi; o += 2, bit <<= 1) {
             const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
@@ -597,11 +629,9 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
               hits |= bit;
             }
           }
-          if (LOOM_EF_ADAPT && 2 * __popc(hits) * 8 >= 3 * (c_hi - c_lo)) H.ef_skip = 16;
           LOOM_COUNT(3, (c_hi - c_lo) / 2);
           LOOM_COUNT(0, __popc(hits));
         } else {
-          if (H.ef_skip > 0) --H.ef_skip;
 #pragma unroll kPairUnroll
           for (; o + 1 < c_hi; o += 2, bit <<= 1) {
             const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
@@ -623,6 +653,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
           }
         }
         if (o < c_hi) {
+          need_c();
           const int32_t wu = H.w32[off + o];
           const double eu = __dadd_rn(ea, H.ga[off + o]);
           if (in.any_pass(H, ip, inner_tw(pr, wu), eu, INT_MAX)) hits |= bit;
@@ -634,6 +665,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
         while (__builtin_expect(hits != 0, 0)) {
           const int p = __ffs(hits) - 1;
           hits &= hits - 1;
+          need_c();
           for (int oo = c_lo + 2 * p; oo < min(c_hi, c_lo + 2 * p + 2); ++oo) {
             const double eu = __dadd_rn(ea, H.ga[off + oo]);
             const int32_t tw = inner_tw(pr, H.w32[off + oo]);
@@ -679,9 +711,11 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
     constexpr int NS = 1 << (K - J - 1);
     int64_t* cout = coef_col<K>(H.coef_base, J + 1);
     for (int o = o_lo; o < o_hi; ++o) {
-      const int64_t w = H.wall[off + o];
+      if constexpr (!kLazyCoef<PRIM, NV>) {
+        const int64_t w = H.wall[off + o];
 #pragma unroll
-      for (int S = 0; S < NS; ++S) cout[S * kBlock] = max(cin[2 * S * SI], cin[(2 * S + 1) * SI] + w);
+        for (int S = 0; S < NS; ++S) cout[S * kBlock] = max(cin[2 * S * SI], cin[(2 * S + 1) * SI] + w);
+      }
       H.od[J] = o;
       const double e2 = __dadd_rn(ea, H.ga[off + o]);
       const int32_t q2 = (PRIM == kPrimQual) ? min(qv, H.q[off + o]) : INT_MAX;
@@ -757,7 +791,6 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
   H.inner = v.inner;
   H.P = v.h->n_nodes - K;
   H.od[0] = H.od[1] = H.od[2] = H.od[3] = 0;
-  H.ef_skip = 0;
   reload(H);
   Inner<K, PRIM, NV, PT> in;
   in.load(H);
