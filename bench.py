@@ -332,13 +332,13 @@ def b200_arm(args) -> None:
 
 
 # Compiled fast path of the innermost contexts of search_kernel<4, kPrimFp,
-# 16, true> (tools/sass_hot.py 4 0 16 1): per 64 plans per lane (two
-# unrolled steps of two contexts), 108 SASS instructions -- 28 DSETP and 27
-# ISETP (the energy-first test: half the options on the FP64 pipe, half on
-# the ALU pipe with high words), 8 DADD, 13 LDCU, 4 LDS, loop control -- of
-# which 34 run on the ALU pipe and 36 on the FP64 pipe: issue-bound.
-# DESIGN.md §5.
-FAST_PATH = {"issue": 108, "alu": 34, "fp64": 36, "plans_per_lane": 64}
+# 16, true> (tools/sass_blocks.py 4 0 16 1): per 128 plans per lane (four
+# unrolled steps of two contexts), 186 SASS instructions -- 64 DSETP.LE.OR
+# and 65 ISETP.LE.OR (one compare per plan on its primary criterion: half the
+# options on the FP64 pipe, half on the ALU pipe with high words), 16 DADD,
+# 16 LDCU, 8 LDS, loop control -- of which 76 run on the ALU pipe and 80 on
+# the FP64 pipe: issue-bound.  DESIGN.md §5.
+FAST_PATH = {"issue": 186, "alu": 76, "fp64": 80, "plans_per_lane": 128}
 
 
 def other_configs(ctx, loom, W) -> dict:

@@ -66,7 +66,7 @@ namespace {
 constexpr int64_t kNeg = -(int64_t(1) << 62);
 
 #ifndef LOOM_PAIR_UNROLL
-#define LOOM_PAIR_UNROLL 2
+#define LOOM_PAIR_UNROLL 4
 #endif
 constexpr int kPairUnroll = LOOM_PAIR_UNROLL;
 // LOOM_STATS=1 (experiment builds): event counters of the search kernel,
@@ -80,6 +80,12 @@ __device__ unsigned long long g_stats[8];
   do {                                                        \
     if (LOOM_STATS) atomicAdd(&g_stats[i], (unsigned long long)(n)); \
   } while (0)
+#ifndef LOOM_PT_CTAS
+#define LOOM_PT_CTAS 2  // resident CTAs per SM of single-problem launches (register cap 128)
+#endif
+#ifndef LOOM_SWEEP_SYNC
+#define LOOM_SWEEP_SYNC 1  // reconverge after every innermost sweep (else once per subrow step)
+#endif
 #ifndef LOOM_JOB_BOUND
 #define LOOM_JOB_BOUND 1
 #endif
@@ -472,20 +478,86 @@ struct Inner {
   // (g <= t => hi(g) <= hi(t) for g >= +0; t < 0 has a negative high word),
   // so both pipes carry half of the plans.  A superset of the passing plans,
   // like every fast test.
+  //
+  // The compares are written in PTX so each plan keeps its own compare: the
+  // OR over a context is otherwise an algebraic min over the (uniform) table
+  // that the compiler hoists, which would turn the per-plan test into a
+  // per-context bound.  One setp per plan, accumulated with setp's
+  // predicate-OR form (SASS DSETP.LE.OR / ISETP.LE.OR).
   __device__ __forceinline__ bool any_energy2(const InnerParams& ip, double tu0, double tu1) const {
+    static_assert(NV == 16 || NV == 8, "the PTX sweeps cover 8 or 16 options");
     const int32_t th0 = __double2hiint(tu0), th1 = __double2hiint(tu1);
-    bool af = false, ai = false;
-#pragma unroll
-    for (int j = 0; j < (NV > 0 ? NV : 1); ++j) {
-      if (j & 1) {
-        ai |= GH(ip, j) <= th0;
-        ai |= GH(ip, j) <= th1;
-      } else {
-        af |= G(ip, j) <= tu0;
-        af |= G(ip, j) <= tu1;
-      }
+    uint32_t flag;
+    if constexpr (NV == 16) {
+      asm("{\n\t"
+          ".reg .pred pf, pi;\n\t"
+          "setp.le.f64 pf, %1, %17;\n\t"
+          "setp.le.or.f64 pf, %2, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %3, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %4, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %5, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %6, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %7, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %8, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %1, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %2, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %3, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %4, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %5, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %6, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %7, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %8, %18, pf;\n\t"
+          "setp.le.s32 pi, %9, %19;\n\t"
+          "setp.le.or.s32 pi, %10, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %11, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %12, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %13, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %14, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %15, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %16, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %9, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %10, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %11, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %12, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %13, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %14, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %15, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %16, %20, pi;\n\t"
+          "or.pred pf, pf, pi;\n\t"
+          "selp.u32 %0, 1, 0, pf;\n\t"
+          "}"
+          : "=r"(flag)
+          : "d"(G(ip, 0)), "d"(G(ip, 2)), "d"(G(ip, 4)), "d"(G(ip, 6)), "d"(G(ip, 8)), "d"(G(ip, 10)),
+            "d"(G(ip, 12)), "d"(G(ip, 14)), "r"(GH(ip, 1)), "r"(GH(ip, 3)), "r"(GH(ip, 5)), "r"(GH(ip, 7)),
+            "r"(GH(ip, 9)), "r"(GH(ip, 11)), "r"(GH(ip, 13)), "r"(GH(ip, 15)), "d"(tu0), "d"(tu1), "r"(th0),
+            "r"(th1));
+    } else {
+      asm("{\n\t"
+          ".reg .pred pf, pi;\n\t"
+          "setp.le.f64 pf, %1, %9;\n\t"
+          "setp.le.or.f64 pf, %2, %9, pf;\n\t"
+          "setp.le.or.f64 pf, %3, %9, pf;\n\t"
+          "setp.le.or.f64 pf, %4, %9, pf;\n\t"
+          "setp.le.or.f64 pf, %1, %10, pf;\n\t"
+          "setp.le.or.f64 pf, %2, %10, pf;\n\t"
+          "setp.le.or.f64 pf, %3, %10, pf;\n\t"
+          "setp.le.or.f64 pf, %4, %10, pf;\n\t"
+          "setp.le.s32 pi, %5, %11;\n\t"
+          "setp.le.or.s32 pi, %6, %11, pi;\n\t"
+          "setp.le.or.s32 pi, %7, %11, pi;\n\t"
+          "setp.le.or.s32 pi, %8, %11, pi;\n\t"
+          "setp.le.or.s32 pi, %5, %12, pi;\n\t"
+          "setp.le.or.s32 pi, %6, %12, pi;\n\t"
+          "setp.le.or.s32 pi, %7, %12, pi;\n\t"
+          "setp.le.or.s32 pi, %8, %12, pi;\n\t"
+          "or.pred pf, pf, pi;\n\t"
+          "selp.u32 %0, 1, 0, pf;\n\t"
+          "}"
+          : "=r"(flag)
+          : "d"(G(ip, 0)), "d"(G(ip, 2)), "d"(G(ip, 4)), "d"(G(ip, 6)), "r"(GH(ip, 1)), "r"(GH(ip, 3)),
+            "r"(GH(ip, 5)), "r"(GH(ip, 7)), "d"(tu0), "d"(tu1), "r"(th0), "r"(th1));
     }
-    return af | ai;
+    return flag != 0;
   }
 
   // NV > 0: does any plan of the context pass?  (one predicate OR per plan)
@@ -684,7 +756,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       // Reconverge after the (divergent) flagged-context work: left alone,
       // the lanes that took the slow path and the ones that did not keep
       // running the step loop as separate groups, issuing it twice.
-      __syncwarp(H.sync_mask);
+      if (LOOM_SWEEP_SYNC) __syncwarp(H.sync_mask);
     } else {
       for (int o = o_lo; o < o_hi; ++o) {
         const int32_t wu = H.w32[off + o];
@@ -705,7 +777,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
           }
         }
       }
-      __syncwarp(H.sync_mask);
+      if (LOOM_SWEEP_SYNC) __syncwarp(H.sync_mask);
     }
   } else {
     constexpr int NS = 1 << (K - J - 1);
@@ -816,33 +888,35 @@ __device__ void run_subrows(const uint8_t* smem, uint8_t* slot_base, uint8_t* co
   uint64_t s = s_begin;
   for (unsigned step = 0; step < n_steps; ++step) {
     H.sync_mask = __ballot_sync(0xffffffffu, step < n_mine);
-    if (step >= n_mine) continue;
-    if (fresh_row) {
-      if (P == 0) {
+    if (step < n_mine) {
+      if (fresh_row) {
+        if (P == 0) {
 #pragma unroll 1
-        for (int S = 0; S < NS; ++S) c0[S] = cw[S];
-        ea_pre = ea_top;
-        q_pre = q_top;
-        lex_pre = lex_top;
-      } else {
-        const int o = v.optoff[P - 1] + d[P - 1];
-        const int64_t w = v.wall[o];
+          for (int S = 0; S < NS; ++S) c0[S] = cw[S];
+          ea_pre = ea_top;
+          q_pre = q_top;
+          lex_pre = lex_top;
+        } else {
+          const int o = v.optoff[P - 1] + d[P - 1];
+          const int64_t w = v.wall[o];
 #pragma unroll 1
-        for (int S = 0; S < NS; ++S) c0[S] = max(cw[2 * S], cw[2 * S + 1] + w);
-        ea_pre = __dadd_rn(ea_top, v.ga[o]);
-        q_pre = min(q_top, v.q[o]);
-        lex_pre = lex_top + v.lexw[o];
+          for (int S = 0; S < NS; ++S) c0[S] = max(cw[2 * S], cw[2 * S + 1] + w);
+          ea_pre = __dadd_rn(ea_top, v.ga[o]);
+          q_pre = min(q_top, v.q[o]);
+          lex_pre = lex_top + v.lexw[o];
+        }
+        fresh_row = false;
       }
-      fresh_row = false;
+      H.s_index = s;
+      level<K, PRIM, NV, PT, 0>(H, in, ip, ea_pre, q_pre, lex_pre, o0, o0 + 1, 0);
+      if (static_cast<uint64_t>(++o0) == n0) {  // next row of the group
+        o0 = 0;
+        fresh_row = true;
+        if (P >= 1) ++d[P - 1];
+      }
+      ++s;
     }
-    H.s_index = s;
-    level<K, PRIM, NV, PT, 0>(H, in, ip, ea_pre, q_pre, lex_pre, o0, o0 + 1, 0);
-    if (static_cast<uint64_t>(++o0) == n0) {  // next row of the group
-      o0 = 0;
-      fresh_row = true;
-      if (P >= 1) ++d[P - 1];
-    }
-    ++s;
+    if (!LOOM_SWEEP_SYNC) __syncwarp(0xffffffffu);
   }
 }
 
@@ -894,7 +968,7 @@ __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
 }
 
 template <int K, int PRIM, int NV, bool PT>
-__global__ void __launch_bounds__(kBlock, PT ? 3 : 2)
+__global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 2)
     search_kernel(const uint8_t* __restrict__ arena, const JobDesc* __restrict__ jobs, int ctas_per_job,
                   Rec* __restrict__ scratch, JobSync* __restrict__ sync, Rec* __restrict__ out,
                   const InnerParams ip) {
