@@ -332,13 +332,14 @@ def b200_arm(args) -> None:
 
 
 # Compiled fast path of the innermost contexts of search_kernel<4, kPrimFp,
-# 16, true> (tools/sass_blocks.py 4 0 16 1): per 128 plans per lane (four
-# unrolled steps of two contexts), 186 SASS instructions -- 64 DSETP.LE.OR
-# and 65 ISETP.LE.OR (one compare per plan on its primary criterion: half the
-# options on the FP64 pipe, half on the ALU pipe with high words), 16 DADD,
-# 16 LDCU, 8 LDS, loop control -- of which 76 run on the ALU pipe and 80 on
-# the FP64 pipe: issue-bound.  DESIGN.md §5.
-FAST_PATH = {"issue": 186, "alu": 76, "fp64": 80, "plans_per_lane": 128}
+# 16, true> (tools/sass_blocks.py 4 0 16 1): one fully unrolled sweep over
+# the 16 options of the node above the innermost = 256 plans per lane in 346
+# SASS instructions -- 128 DSETP.LE.OR and 128 ISETP.LE.OR (one compare per
+# plan on its primary criterion: half the options on the FP64 pipe, half on
+# the ALU pipe with high words), 32 DADD, 16 LDCU, 16 LDS, step flags -- of
+# which 150 run on the ALU pipe and 160 on the FP64 pipe: issue-bound.
+# DESIGN.md §5.
+FAST_PATH = {"issue": 346, "alu": 150, "fp64": 160, "plans_per_lane": 256}
 
 
 def other_configs(ctx, loom, W) -> dict:

@@ -687,53 +687,11 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       // Energy-first (PRIM == kPrimFp): one compare per plan on the primary
       // criterion (any_energy2); other objectives test both criteria per plan.
       constexpr bool ef = kLazyCoef<PRIM, NV>;
-      for (int c_lo = o_lo; c_lo < o_hi; c_lo += 64) {
-        const int c_hi = min(o_hi, c_lo + 64);
-        uint32_t hits = 0, bit = 1;
-        int o = c_lo;
-        if constexpr (ef) {
-#pragma unroll kPairUnroll
-          for (; o + 1 < c_hi; o += 2, bit <<= 1) {
-            const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
-            const bool a = in.any_energy2(ip, ctx_bound(H, eu0), ctx_bound(H, eu1));
-            if (__builtin_expect(a, 0)) {
-              asm volatile("");
-              hits |= bit;
-            }
-          }
-          LOOM_COUNT(3, (c_hi - c_lo) / 2);
-          LOOM_COUNT(0, __popc(hits));
-        } else {
-#pragma unroll kPairUnroll
-          for (; o + 1 < c_hi; o += 2, bit <<= 1) {
-            const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
-            const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
-            const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
-            const double tu0 = ctx_bound(H, eu0), tu1 = ctx_bound(H, eu1);
-            bool a = false;
-#pragma unroll
-            for (int j = 0; j < NV; ++j) {
-              a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw0, tu0);
-              a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw1, tu1);
-            }
-            // a real (rarely taken) branch keeps the per-plan tests a predicate
-            // OR chain; the empty asm stops if-conversion into per-plan selects
-            if (__builtin_expect(a, 0)) {
-              asm volatile("");
-              hits |= bit;
-            }
-          }
-        }
-        if (o < c_hi) {
-          need_c();
-          const int32_t wu = H.w32[off + o];
-          const double eu = __dadd_rn(ea, H.ga[off + o]);
-          if (in.any_pass(H, ip, inner_tw(pr, wu), eu, INT_MAX)) hits |= bit;
-        }
-        // Flagged steps: the two-criteria bound test per context, then the
-        // exact test, then the exact scan.  The step loop holds no call, so
-        // the table stays in uniform registers across steps; testing with
-        // thresholds older than the running best only lets more through.
+      // Flagged steps: the two-criteria bound test per context, then the
+      // exact test, then the exact scan.  The step loop holds no call, so
+      // the table stays in uniform registers across steps; testing with
+      // thresholds older than the running best only lets more through.
+      auto flagged = [&](uint32_t hits, int c_lo, int c_hi) {
         while (__builtin_expect(hits != 0, 0)) {
           const int p = __ffs(hits) - 1;
           hits &= hits - 1;
@@ -752,11 +710,73 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
             }
           }
         }
+      };
+      if (ef && n == NV && o_lo == 0 && o_hi == NV) {
+        // The whole node above the innermost, radix == NV: one fully
+        // unrolled sweep of NV/2 steps, branch-free step flags.
+        uint32_t hits = 0;
+#pragma unroll
+        for (int st = 0; st < NV / 2; ++st) {
+          const double eu0 = __dadd_rn(ea, H.ga[off + 2 * st]), eu1 = __dadd_rn(ea, H.ga[off + 2 * st + 1]);
+          hits |= static_cast<uint32_t>(in.any_energy2(ip, ctx_bound(H, eu0), ctx_bound(H, eu1))) << st;
+        }
+        LOOM_COUNT(3, NV / 2);
+        LOOM_COUNT(0, __popc(hits));
+        flagged(hits, 0, NV);
+      } else {
+        for (int c_lo = o_lo; c_lo < o_hi; c_lo += 64) {
+          const int c_hi = min(o_hi, c_lo + 64);
+          uint32_t hits = 0, bit = 1;
+          int o = c_lo;
+          if constexpr (ef) {
+#pragma unroll kPairUnroll
+            for (; o + 1 < c_hi; o += 2, bit <<= 1) {
+              const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
+              const bool a = in.any_energy2(ip, ctx_bound(H, eu0), ctx_bound(H, eu1));
+              if (__builtin_expect(a, 0)) {
+                asm volatile("");
+                hits |= bit;
+              }
+            }
+            LOOM_COUNT(3, (c_hi - c_lo) / 2);
+            LOOM_COUNT(0, __popc(hits));
+          } else {
+#pragma unroll kPairUnroll
+            for (; o + 1 < c_hi; o += 2, bit <<= 1) {
+              const int32_t wu0 = H.w32[off + o], wu1 = H.w32[off + o + 1];
+              const double eu0 = __dadd_rn(ea, H.ga[off + o]), eu1 = __dadd_rn(ea, H.ga[off + o + 1]);
+              const int32_t tw0 = inner_tw(pr, wu0), tw1 = inner_tw(pr, wu1);
+              const double tu0 = ctx_bound(H, eu0), tu1 = ctx_bound(H, eu1);
+              bool a = false;
+#pragma unroll
+              for (int j = 0; j < NV; ++j) {
+                a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw0, tu0);
+                a |= in.pass_bound(in.W(ip, j), in.G(ip, j), tw1, tu1);
+              }
+              // a real (rarely taken) branch keeps the per-plan tests a predicate
+              // OR chain; the empty asm stops if-conversion into per-plan selects
+              if (__builtin_expect(a, 0)) {
+                asm volatile("");
+                hits |= bit;
+              }
+            }
+          }
+          if (o < c_hi) {
+            need_c();
+            const int32_t wu = H.w32[off + o];
+            const double eu = __dadd_rn(ea, H.ga[off + o]);
+            if (in.any_pass(H, ip, inner_tw(pr, wu), eu, INT_MAX)) hits |= bit;
+          }
+          flagged(hits, c_lo, c_hi);
+        }
       }
       // Reconverge after the (divergent) flagged-context work: left alone,
       // the lanes that took the slow path and the ones that did not keep
       // running the step loop as separate groups, issuing it twice.
-      if (LOOM_SWEEP_SYNC) __syncwarp(H.sync_mask);
+      if (LOOM_SWEEP_SYNC) {
+        if (H.sync_mask == 0xffffffffu) __syncwarp();
+        else __syncwarp(H.sync_mask);
+      }
     } else {
       for (int o = o_lo; o < o_hi; ++o) {
         const int32_t wu = H.w32[off + o];
@@ -777,7 +797,10 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
           }
         }
       }
-      if (LOOM_SWEEP_SYNC) __syncwarp(H.sync_mask);
+      if (LOOM_SWEEP_SYNC) {
+        if (H.sync_mask == 0xffffffffu) __syncwarp();
+        else __syncwarp(H.sync_mask);
+      }
     }
   } else {
     constexpr int NS = 1 << (K - J - 1);
