@@ -12,7 +12,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__b
   --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-configs > gpurun_out/bench_under_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:search_kernel -c 1 \
-  -o gpurun_out/prof_full -f python tools/prof_search.py --plans 68719476736 --repeat 1 > gpurun_out/prof_full.log 2>&1
+  -o gpurun_out/prof_full -f python tools/prof_search.py --plans 1099511627776 --repeat 1 > gpurun_out/prof_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:estimate_range -c 1 \
   -o gpurun_out/prof_scores -f python tools/time_scores.py --log2 26 --reps 1 --host-log2 10 > gpurun_out/prof_scores.log 2>&1
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
