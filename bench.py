@@ -218,8 +218,17 @@ def b200_arm(args) -> None:
             return D.empty_winner()
 
     # ---- value: resident problem, device-timed -------------------------------
+    # N > 1: each rank searches its index range plus the greedy seed as a common
+    # incumbent (loom_search_argmin_shard), so every shard prunes like the
+    # whole-space search; the reduce over ranks is still the exact argmin.
+    def search(b, e):
+        if world > 1:
+            dp.search_shard_async(b, e)
+        else:
+            dp.search_async(b, e)
+
     for _ in range(args.warmup):
-        dp.search_async(begin, end)
+        search(begin, end)
         shard_result()
     launches0 = ctx.launches
     step_ms = []
@@ -230,7 +239,7 @@ def b200_arm(args) -> None:
                 flush_l2(torch, scratch)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            dp.search_async(begin, end)
+            search(begin, end)
             e1.record(stream)
             shard_result()
             step_ms.append(e0.elapsed_time(e1))
@@ -255,10 +264,7 @@ def b200_arm(args) -> None:
             return loom.exhaustive_search(dag_t, lib_t, obj_t, bounds_t, ctx=ctx)
         low = loom.Lowered(dag_t, lib_t, bounds_t)
         o = loom.objective(obj_t)
-        try:
-            mine = loom.search_argmin(ctx, low.problem, o, begin, end)
-        except loom.NoFeasibleConfigError:
-            mine = D.empty_winner()
+        mine = D.search_shard(ctx, low.problem, o, rank, world)
         best = D.combine(D.allgather_winners(mine, device=red_dev), o)
         return low.config(best["plan_index"]) | best
 
@@ -308,7 +314,7 @@ def b200_arm(args) -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": float(te.item()),
                     "h2d_bytes_per_step": dp.image_bytes + 64, "d2h_bytes_per_step": 64,
                     "path": "loom_exhaustive_search_json: JSON parse + lowering + H2D + kernel + D2H + decode"
-                    if world == 1 else "lowering + loom_search_argmin(shard) + NCCL all-gather + reduce + decode"},
+                    if world == 1 else "lowering + loom_search_argmin_shard (range + greedy incumbent) + NCCL all-gather + reduce + decode"},
             "roofline": {"bound": f"instruction ({bound_pipe} pipe)", "achieved": achieved, "peak": peak_plans,
                          "unit": "plans/s per GPU", "frac": achieved / peak_plans, "traffic": traffic,
                          "inst_per_plan": fp["issue"] / fp["plans_per_lane"],

@@ -200,6 +200,17 @@ int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const 
                                  const char* const* dag_jsons, int32_t n, const char* objective_json,
                                  int32_t threads, loom_winner* out, int32_t* status);
 
+/* Shard search (multi-GPU partitions): the argmin of
+ * [begin, end) u {incumbent}, where the incumbent is any plan of the space --
+ * LOOM_INCUMBENT_GREEDY for the greedy seed (loom_greedy_seed).  Every rank
+ * starting from the same incumbent prunes like a whole-space search, and the
+ * reduce of the per-rank results over a partition of the space is still the
+ * exact argmin (the incumbent is itself a plan of the space).  out->plan_index
+ * may be the incumbent's, outside [begin, end). */
+#define LOOM_INCUMBENT_GREEDY UINT64_MAX
+int loom_search_argmin_shard(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
+                             uint64_t begin, uint64_t end, uint64_t incumbent, loom_winner* out);
+
 /* Resident problems: upload once, search many times (bench "value" path). */
 int loom_problem_upload(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
                         loom_device_problem** out);
@@ -208,6 +219,9 @@ int loom_problem_release(loom_device_problem* dp);
 uint64_t loom_device_problem_bytes(const loom_device_problem* dp);
 /* Enqueue a search on the ctx stream without synchronising. */
 int loom_search_argmin_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t begin, uint64_t end);
+/* loom_search_argmin_shard on a resident problem, enqueued without synchronising. */
+int loom_search_argmin_shard_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t begin, uint64_t end,
+                                   uint64_t incumbent);
 /* Wait for the last enqueued search of dp and decode its result. */
 int loom_search_argmin_result(loom_ctx* ctx, loom_device_problem* dp, loom_winner* out);
 

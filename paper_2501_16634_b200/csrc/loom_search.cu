@@ -1010,9 +1010,9 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 2)
   uint8_t* slot_base = smem + ((jd.blob_bytes + 127) & ~127u);
   const Slots sl = make_slots(slot_base);
   slot_init(sl, threadIdx.x, h);
-  if (h->has_seed && h->seed_index >= jd.begin && h->seed_index < jd.end) {
+  if (jd.has_seed) {
     Rec c;
-    full_eval(v, h->seed_index, c);
+    full_eval(v, jd.seed, c);
     slot_offer(sl, threadIdx.x, h, c);
   }
 
@@ -1613,6 +1613,7 @@ __global__ void __launch_bounds__(kBlock)
 // ---------------------------------------------------------------------------
 struct Built {
   std::vector<uint8_t> blob;
+  std::vector<int32_t> seed;  // loom_greedy_seed digits (empty: none)
   int K = 2;
   int prim = kPrimFp;
   bool full_only = false;
@@ -1792,6 +1793,7 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
       for (int i = 0; i < n; ++i) idx = idx * static_cast<uint64_t>(p->radix[i]) + static_cast<uint64_t>(sd[i]);
       hd.has_seed = 1;
       hd.seed_index = idx;
+      b.seed = sd;
     }
   }
   hd.inner_wmin = wmin;
@@ -1865,7 +1867,78 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
 }
 
 // Splits [begin, end) into whole subrows and edge plans.
-JobDesc make_desc(const Built& b, uint64_t begin, uint64_t end, bool full_eval_only) {
+// The incumbent of a searched range [begin, end): the greedy seed when it
+// lies in the range; otherwise the best feasible of a few in-range plans
+// built from it -- the digits the range's ends share, one digit of the first
+// node where they differ, the seed's digits below (a shard of a multi-GPU
+// search rarely holds the global seed, and a thread with no incumbent flags
+// every context until it finds one).  Any feasible plan of the range is a
+// valid start: it is a candidate the search would have seen anyway.
+void range_seed(const loom_problem* p, const loom_objective* o, const Built& b, JobDesc& d) {
+  const int n = p->n_nodes;
+  if (b.seed.empty() || d.begin >= d.end || n == 0) return;
+  auto index = [&](const std::vector<int32_t>& dg) {
+    uint64_t x = 0;
+    for (int i = 0; i < n; ++i) x = x * static_cast<uint64_t>(p->radix[i]) + static_cast<uint64_t>(dg[i]);
+    return x;
+  };
+  const uint64_t gs = index(b.seed);
+  if (gs >= d.begin && gs < d.end) {
+    d.has_seed = 1;
+    d.seed = gs;
+    return;
+  }
+  auto digits = [&](uint64_t x) {
+    std::vector<int32_t> dg(n);
+    for (int i = n - 1; i >= 0; --i) {
+      dg[i] = static_cast<int32_t>(x % static_cast<uint64_t>(p->radix[i]));
+      x /= static_cast<uint64_t>(p->radix[i]);
+    }
+    return dg;
+  };
+  const std::vector<int32_t> db = digits(d.begin), de = digits(d.end - 1);
+  int L = 0;
+  while (L < n && db[L] == de[L]) ++L;
+  loom_winner best{};
+  bool have = false;
+  auto offer = [&](uint64_t idx) {
+    if (idx < d.begin || idx >= d.end) return;
+    loom_winner w{};
+    w.plan_index = idx;
+    if (loomi::fill_winner(p, &w) != LOOM_OK) return;
+    w.found = (!o->has_latency_slo || w.latency_us <= o->latency_slo_us) &&
+              (!o->has_quality_floor || w.quality >= o->quality_floor);
+    if (w.found && (!have || loom_winner_less(&w, &best, o))) {
+      best = w;
+      have = true;
+    }
+  };
+  if (L == n) {
+    offer(d.begin);
+  } else {
+    std::vector<int32_t> dg = b.seed;
+    for (int i = 0; i < L; ++i) dg[i] = db[i];
+    const int lo = db[L], hi = de[L];
+    const int step = std::max(1, (hi - lo + 1) / 64);  // at most ~64 candidates
+    for (int x = lo; x <= hi; x += step) {
+      dg[L] = x;
+      offer(index(dg));
+    }
+  }
+  if (have) {
+    d.has_seed = 1;
+    d.seed = best.plan_index;
+  }
+}
+
+// incumbent: kNoIncumbent (a plain range search: the start is range_seed's
+// in-range plan), LOOM_INCUMBENT_GREEDY (the greedy seed, wherever it lies)
+// or a plan index of the space.  An out-of-range incumbent takes part in the
+// selection: the result is the argmin of [begin, end) u {incumbent}.
+constexpr uint64_t kNoIncumbent = UINT64_MAX - 1;
+
+JobDesc make_desc(const Built& b, uint64_t begin, uint64_t end, bool full_eval_only, const loom_problem* p = nullptr,
+                  const loom_objective* o = nullptr, uint64_t incumbent = kNoIncumbent) {
   JobDesc d;
   std::memset(&d, 0, sizeof d);
   end = std::min(end, b.total);
@@ -1873,6 +1946,16 @@ JobDesc make_desc(const Built& b, uint64_t begin, uint64_t end, bool full_eval_o
   d.begin = begin;
   d.end = end;
   d.blob_bytes = static_cast<uint32_t>(b.blob.size());
+  if (incumbent == LOOM_INCUMBENT_GREEDY) {
+    const BlobHeader* bh = reinterpret_cast<const BlobHeader*>(b.blob.data());
+    d.has_seed = bh->has_seed;
+    d.seed = bh->seed_index;
+  } else if (incumbent < b.total) {
+    d.has_seed = 1;
+    d.seed = incumbent;
+  } else if (p && o) {
+    range_seed(p, o, b, d);
+  }
   if (full_eval_only || b.full_only) {
     d.head_end = end;
     d.tail_begin = end;
@@ -2106,8 +2189,37 @@ int loom_ctx_destroy(loom_ctx* c) {
 
 uint64_t loom_ctx_launch_count(const loom_ctx* c) { return c ? c->launches : 0; }
 
+namespace {
+int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin, uint64_t end,
+                       int32_t algo, uint64_t incumbent, loom_winner* out);
+int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end, uint64_t incumbent);
+}  // namespace
+
 int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin,
                             uint64_t end, int32_t algo, loom_winner* out) {
+  return search_argmin_impl(c, p, o, begin, end, algo, kNoIncumbent, out);
+}
+
+int loom_search_argmin_shard(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin,
+                             uint64_t end, uint64_t incumbent, loom_winner* out) {
+  return search_argmin_impl(c, p, o, begin, end, 0, incumbent, out);
+}
+
+int loom_search_argmin_async(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end) {
+  return search_async_impl(c, dp, begin, end, kNoIncumbent);
+}
+
+int loom_search_argmin_shard_async(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end,
+                                   uint64_t incumbent) {
+  return search_async_impl(c, dp, begin, end, incumbent);
+}
+
+}  // extern "C"
+
+namespace {
+
+int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin, uint64_t end,
+                       int32_t algo, uint64_t incumbent, loom_winner* out) {
   if (!c || !p || !o || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   std::memset(out, 0, sizeof *out);
   LOOM_CUDA(cudaSetDevice(c->device));
@@ -2116,7 +2228,7 @@ int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objec
   if (int rc = build_image(p, o, target, b)) return rc;
   if (b.total == 0)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
-  const JobDesc d = make_desc(b, begin, end, algo == 1);
+  const JobDesc d = make_desc(b, begin, end, algo == 1, p, o, incumbent);
   if (d.begin >= d.end)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
@@ -2140,6 +2252,10 @@ int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objec
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   return finish_winner(p, c->h_out[0], out);
 }
+
+}  // namespace
+
+extern "C" {
 
 int loom_search_argmin(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin, uint64_t end,
                        loom_winner* out) {
@@ -2210,6 +2326,13 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
   for (auto& g : groups) {
     for (int j : g.jobs) {
       JobDesc d = make_desc(built[j], 0, built[j].total, false);
+      if (built[j].blob.size() && !built[j].seed.empty()) {  // whole space: the greedy seed is in range
+        uint64_t x = 0;
+        const BlobHeader* bh = reinterpret_cast<const BlobHeader*>(built[j].blob.data());
+        x = bh->seed_index;
+        d.has_seed = bh->has_seed;
+        d.seed = x;
+      }
       d.blob_off = off[j];
       all.push_back(d);
     }
@@ -2319,9 +2442,13 @@ uint64_t loom_device_problem_bytes(const loom_device_problem* dp) {
   return dp ? static_cast<uint64_t>(dp->built.blob.size()) : 0;
 }
 
-int loom_search_argmin_async(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end) {
+}  // extern "C"
+
+namespace {
+
+int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end, uint64_t incumbent) {
   if (!c || !dp) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
-  JobDesc d = make_desc(dp->built, begin, end, false);
+  JobDesc d = make_desc(dp->built, begin, end, false, &dp->host, &dp->objective, incumbent);
   d.blob_off = 0;
   if (d.begin >= d.end) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: empty range");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
@@ -2335,6 +2462,10 @@ int loom_search_argmin_async(loom_ctx* c, loom_device_problem* dp, uint64_t begi
   LOOM_CUDA(cudaEventRecord(dp->done, c->stream));
   return LOOM_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int loom_search_argmin_result(loom_ctx* c, loom_device_problem* dp, loom_winner* out) {
   if (!c || !dp || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");

@@ -128,7 +128,8 @@ struct JobDesc {
   uint64_t sub_lo;       // whole subrows [sub_lo, sub_hi): hierarchical path
   uint64_t sub_hi;
   uint32_t blob_bytes;
-  uint32_t pad;
+  uint32_t has_seed;     // an incumbent plan of [begin, end) every thread starts from
+  uint64_t seed;
 };
 
 }  // namespace loomk

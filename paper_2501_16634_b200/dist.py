@@ -22,6 +22,20 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     return total * rank // world, total * (rank + 1) // world
 
 
+def search_shard(ctx, problem, objective, rank: int, world: int) -> dict:
+    """This rank's shard search: argmin of its plan-index range plus the
+    greedy seed as a common incumbent (loom_search_argmin_shard), so every
+    rank prunes like a whole-space search.  Returns an empty (found == 0)
+    record when nothing in the shard, nor the incumbent, is feasible."""
+    lw_total = C.c_uint64()
+    loom._check(loom.lib().loom_problem_total(C.byref(problem), C.byref(lw_total)))
+    begin, end = shard_range(lw_total.value, rank, world)
+    try:
+        return loom.search_argmin_shard(ctx, problem, objective, begin, end)
+    except loom.NoFeasibleConfigError:
+        return empty_winner()
+
+
 def shard_jobs(n_jobs: int, rank: int, world: int) -> tuple[int, int]:
     return n_jobs * rank // world, n_jobs * (rank + 1) // world
 

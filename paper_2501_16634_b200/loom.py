@@ -174,6 +174,8 @@ def lib() -> C.CDLL:
         "loom_problem_upload": ([vp, P, O, C.POINTER(vp)], C.c_int),
         "loom_problem_release": ([vp], C.c_int),
         "loom_search_argmin_async": ([vp, vp, C.c_uint64, C.c_uint64], C.c_int),
+        "loom_search_argmin_shard": ([vp, P, O, C.c_uint64, C.c_uint64, C.c_uint64, W], C.c_int),
+        "loom_search_argmin_shard_async": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64], C.c_int),
         "loom_device_problem_bytes": ([vp], C.c_uint64),
         "loom_search_argmin_result": ([vp, vp, W], C.c_int),
         "loom_search_pareto": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64,
@@ -437,6 +439,19 @@ def search_argmin(ctx: Context, problem: Problem, obj: Objective, begin: int = 0
     return w.as_dict()
 
 
+INCUMBENT_GREEDY = (1 << 64) - 1
+
+
+def search_argmin_shard(ctx: Context, problem: Problem, obj: Objective, begin: int, end: int,
+                        incumbent: int = INCUMBENT_GREEDY) -> dict:
+    """argmin of [begin, end) u {incumbent} (a multi-GPU shard search); the
+    incumbent defaults to the greedy seed.  The result may be the incumbent."""
+    w = Winner()
+    _check(lib().loom_search_argmin_shard(ctx.handle, C.byref(problem), C.byref(obj), begin, end, incumbent,
+                                          C.byref(w)))
+    return w.as_dict()
+
+
 def search_argmin_batch(ctx: Context, problems: Sequence[Problem], objectives: Sequence[Objective]
                         ) -> list[tuple[int, dict]]:
     n = len(problems)
@@ -474,6 +489,10 @@ class DeviceProblem:
     def search_async(self, begin: int = 0, end: int | None = None) -> None:
         end = (1 << 64) - 1 if end is None else end
         _check(lib().loom_search_argmin_async(self.ctx.handle, self._h, begin, end))
+
+    def search_shard_async(self, begin: int, end: int, incumbent: int = INCUMBENT_GREEDY) -> None:
+        """Enqueue loom_search_argmin_shard_async (argmin of [begin, end) u {incumbent})."""
+        _check(lib().loom_search_argmin_shard_async(self.ctx.handle, self._h, begin, end, incumbent))
 
     @property
     def image_bytes(self) -> int:

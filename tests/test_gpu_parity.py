@@ -251,3 +251,46 @@ def test_infeasible_and_empty(ctx):
     with pytest.raises(loom.NoFeasibleConfigError):
         loom.exhaustive_search({"nodes": [], "edges": []}, w.library, "MIN_COST", w.bounds, ctx=ctx)
     assert ctx.launches > 0
+
+
+@pytest.mark.parametrize("cfg,ranks", [("c1", 3), ("c2", 8), ("c3", 8), ("c5", 4)])
+def test_shard_search_with_incumbent_combines_to_argmin(ctx, cfg, ranks):
+    """loom_search_argmin_shard: every rank searches its index range plus the
+    greedy seed as a common incumbent; the reduce over ranks equals the
+    whole-space search, and each rank's result is in its range or is the
+    incumbent."""
+    from paper_2501_16634_b200 import dist as D
+    w = {"c1": W.config1, "c2": W.config2, "c3": W.config3, "c5": W.config5}[cfg]()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    obj = loom.objective(w.objective if cfg != "c5" else {"constraint": "MIN_COST"})
+    total = lw.total if cfg != "c3" else 1 << 36  # C3: a 2^36-plan prefix keeps the test short
+    full = loom.search_argmin(ctx, lw.problem, obj, 0, total)
+    import ctypes as C
+    sd = (C.c_int32 * lw.problem.n_nodes)()
+    assert loom.lib().loom_greedy_seed(C.byref(lw.problem), C.byref(obj), sd) == 0
+    seed = 0
+    for i in range(lw.problem.n_nodes):
+        seed = seed * lw.problem.radix[i] + sd[i]
+    winners = []
+    for r in range(ranks):
+        b, e = D.shard_range(total, r, ranks)
+        try:
+            got = loom.search_argmin_shard(ctx, lw.problem, obj, b, e)
+        except loom.NoFeasibleConfigError:
+            got = D.empty_winner()
+        if got["found"]:
+            assert b <= got["plan_index"] < e or got["plan_index"] == seed
+        winners.append(got)
+    if seed < total:
+        best = D.combine(winners, obj)
+        assert best["plan_index"] == full["plan_index"]
+        for k in METRICS:
+            assert best[k] == full[k]
+    else:  # the incumbent lies outside the searched prefix: the reduce is over prefix u {seed}
+        ref = D.combine([full, lw.evaluate(seed) | {"found": 1}] if _feasible(lw.evaluate(seed), w) else [full], obj)
+        assert D.combine(winners, obj)["plan_index"] == ref["plan_index"]
+
+
+def _feasible(est: dict, w) -> bool:
+    slo = w.objective.get("latency_slo_us") if isinstance(w.objective, dict) else None
+    return slo is None or est["latency_us"] <= slo
