@@ -86,6 +86,9 @@ __device__ unsigned long long g_stats[8];
 #ifndef LOOM_SWEEP_SYNC
 #define LOOM_SWEEP_SYNC 1  // reconverge after every innermost sweep (else once per subrow step)
 #endif
+#ifndef LOOM_F32_SPLIT
+#define LOOM_F32_SPLIT 0  // energy-first sweep: also use the FP32 pipe (experiment)
+#endif
 #ifndef LOOM_JOB_BOUND
 #define LOOM_JOB_BOUND 1
 #endif
@@ -443,6 +446,10 @@ struct Inner {
   __device__ __forceinline__ int32_t GH(const InnerParams& ip, int j) const {
     return PT ? ip.gh[j] : __double2hiint(g[PT ? 0 : j]);
   }
+  // g rounded down to binary32 (register tables convert on the fly)
+  __device__ __forceinline__ float GF(const InnerParams& ip, int j) const {
+    return PT ? ip.gf[j] : __double2float_rd(g[PT ? 0 : j]);
+  }
 
   __device__ __forceinline__ void load(const Hot& H) {
     if constexpr (NV > 0 && !PT) {
@@ -488,7 +495,54 @@ struct Inner {
     static_assert(NV == 16 || NV == 8, "the PTX sweeps cover 8 or 16 options");
     const int32_t th0 = __double2hiint(tu0), th1 = __double2hiint(tu1);
     uint32_t flag;
-    if constexpr (NV == 16) {
+    if constexpr (NV == 16 && LOOM_F32_SPLIT) {
+      // three-way split: 6 options on the FP64 pipe, 5 on the ALU pipe (high
+      // words), 5 on the FP32 pipe (binary32 round-down vs round-up bound)
+      const float tf0 = __double2float_ru(tu0), tf1 = __double2float_ru(tu1);
+      asm("{\n\t"
+          ".reg .pred pf, pi, ps;\n\t"
+          "setp.le.f64 pf, %1, %17;\n\t"
+          "setp.le.or.f64 pf, %2, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %3, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %4, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %5, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %6, %17, pf;\n\t"
+          "setp.le.or.f64 pf, %1, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %2, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %3, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %4, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %5, %18, pf;\n\t"
+          "setp.le.or.f64 pf, %6, %18, pf;\n\t"
+          "setp.le.s32 pi, %7, %19;\n\t"
+          "setp.le.or.s32 pi, %8, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %9, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %10, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %11, %19, pi;\n\t"
+          "setp.le.or.s32 pi, %7, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %8, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %9, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %10, %20, pi;\n\t"
+          "setp.le.or.s32 pi, %11, %20, pi;\n\t"
+          "setp.le.f32 ps, %12, %21;\n\t"
+          "setp.le.or.f32 ps, %13, %21, ps;\n\t"
+          "setp.le.or.f32 ps, %14, %21, ps;\n\t"
+          "setp.le.or.f32 ps, %15, %21, ps;\n\t"
+          "setp.le.or.f32 ps, %16, %21, ps;\n\t"
+          "setp.le.or.f32 ps, %12, %22, ps;\n\t"
+          "setp.le.or.f32 ps, %13, %22, ps;\n\t"
+          "setp.le.or.f32 ps, %14, %22, ps;\n\t"
+          "setp.le.or.f32 ps, %15, %22, ps;\n\t"
+          "setp.le.or.f32 ps, %16, %22, ps;\n\t"
+          "or.pred pf, pf, pi;\n\t"
+          "or.pred pf, pf, ps;\n\t"
+          "selp.u32 %0, 1, 0, pf;\n\t"
+          "}"
+          : "=r"(flag)
+          : "d"(G(ip, 0)), "d"(G(ip, 3)), "d"(G(ip, 6)), "d"(G(ip, 9)), "d"(G(ip, 12)), "d"(G(ip, 15)),
+            "r"(GH(ip, 1)), "r"(GH(ip, 4)), "r"(GH(ip, 7)), "r"(GH(ip, 10)), "r"(GH(ip, 13)),
+            "f"(GF(ip, 2)), "f"(GF(ip, 5)), "f"(GF(ip, 8)), "f"(GF(ip, 11)), "f"(GF(ip, 14)),
+            "d"(tu0), "d"(tu1), "r"(th0), "r"(th1), "f"(tf0), "f"(tf1));
+    } else if constexpr (NV == 16) {
       asm("{\n\t"
           ".reg .pred pf, pi;\n\t"
           "setp.le.f64 pf, %1, %17;\n\t"
@@ -1859,6 +1913,11 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
     int64_t bits;
     std::memcpy(&bits, &b.ip.g[j], sizeof bits);
     b.ip.gh[j] = static_cast<int32_t>(bits >> 32);
+    {  // round down to binary32 (conservative for the <= test)
+      float f = static_cast<float>(b.ip.g[j]);
+      if (static_cast<double>(f) > b.ip.g[j]) f = std::nextafter(f, -INFINITY);
+      b.ip.gf[j] = f;
+    }
   }
   b.total = total;
   b.r_sub = r_sub;
