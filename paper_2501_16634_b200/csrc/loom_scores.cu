@@ -202,17 +202,25 @@ __device__ __forceinline__ void est_put(const EstStreams& o, uint64_t i, const E
 }
 
 // Lane-parallel longest-path DP of one group (lane S < 2^K computes column
-// S; bit k of S = suffix node P + k).  f[x][S]: the longest path ending at x
+// S; bit k of S = suffix node P + k; a suffix node reads its predecessors'
+// column S minus its own bit, so lanes synchronise per node).  f[x][S]: the longest path ending at x
 // whose suffix nodes are exactly S, top walls only.  Leaves c[S] in cw.
 template <int K>
 __device__ __forceinline__ void est_warp_dp(const EstView& v, const int* dtop, int P, int64_t* fw, int64_t* cw) {
   constexpr int NS = 1 << K;
   const int S = threadIdx.x & 31;
+  const bool act = S < NS;
   const int n = v.h->n_nodes;
   int64_t cmax = kEstNeg;
-  if (S < NS) {
-    for (int t = 0; t < n; ++t) {
-      const int x = v.topo[t];
+  // every lane walks the nodes (lanes >= NS idle) so the barriers are
+  // full-warp ones
+  for (int t = 0; t < n; ++t) {
+    const int x = v.topo[t];
+    // a suffix node reads column S ^ bit of its predecessors, written by
+    // another lane: every lane's earlier rows must have landed (top nodes
+    // read only their own column)
+    if (x >= P) __syncwarp();
+    if (act) {
       const int pb = v.predoff[x], pe = v.predoff[x + 1];
       int64_t val = kEstNeg;
       if (x < P) {
@@ -228,11 +236,11 @@ __device__ __forceinline__ void est_warp_dp(const EstView& v, const int* dtop, i
           val = b;
         }
       }
-      fw[x * NS + S] = val;  // column S is private to lane S: no cross-lane hazard
+      fw[x * NS + S] = val;
       cmax = max(cmax, val);
     }
-    cw[S] = S == 0 ? max(cmax, int64_t(0)) : cmax;  // latency starts at 0 (estimator.hpp:27)
   }
+  if (act) cw[S] = S == 0 ? max(cmax, int64_t(0)) : cmax;  // latency starts at 0 (estimator.hpp:27)
   __syncwarp();
 }
 
@@ -295,8 +303,14 @@ __global__ void __launch_bounds__(kEstBlock) estimate_range_kernel(const uint8_t
     const uint64_t lo = begin > g0 ? begin : g0;
     const uint32_t ga = static_cast<uint32_t>(lo - g0);
     const uint32_t gb = static_cast<uint32_t>((end < g0 + G ? end : g0 + G) - g0);
-    uint32_t o = ga + lane;
-    if (o >= gb) continue;
+    // Lane l takes the elements e == l (mod 32) of the output, so each store
+    // instruction fills one aligned 32-element window (whole sectors; a
+    // window straddling sectors costs L2 partial-sector merges).
+    // In the group's first window the lanes before ga sit out one step.
+    const int mis = static_cast<int>(static_cast<uint32_t>(lo - begin) & 31u);  // element of ga within its window
+    int o = static_cast<int>(ga) - mis + lane;  // this lane's plan offset at the current window
+    const int o_first = o < static_cast<int>(ga) ? o + 32 : o;
+    if (o_first >= static_cast<int>(gb)) continue;
     // this group's slice of every stream; element o - ga of the slice is plan g0 + o
     const uint64_t base = lo - begin;
     int64_t* p_lat = out.lat ? out.lat + base : nullptr;
@@ -307,14 +321,17 @@ __global__ void __launch_bounds__(kEstBlock) estimate_range_kernel(const uint8_t
     int32_t* p_q = out.q ? out.q + base : nullptr;
     int ds[K];
     {
-      uint32_t x = o;
+      uint32_t x = static_cast<uint32_t>(o_first);
 #pragma unroll
       for (int k = K - 1; k >= 0; --k) {
         ds[k] = static_cast<int>(x % static_cast<uint32_t>(rs[k]));
         x /= static_cast<uint32_t>(rs[k]);
       }
     }
+    // lockstep over windows: a lane whose first window starts before ga sits
+    // that step out (its digits already point at its next plan)
     for (;;) {
+      const bool act = o >= static_cast<int>(ga);  // false only in a lane's first window
       double eg = sa, ec = sc, ed = sd;
       int32_t eq = q;
       Lat cur[NS];
@@ -331,21 +348,24 @@ __global__ void __launch_bounds__(kEstBlock) estimate_range_kernel(const uint8_t
 #pragma unroll
         for (int t = 0; t < (NS >> (k + 1)); ++t) cur[t] = max(cur[2 * t], cur[2 * t + 1] + w);
       }
-      const uint32_t i = o - ga;
-      if (p_lat) p_lat[i] = cur[0];
-      if (p_gpu) p_gpu[i] = eg;
-      if (p_cpu) p_cpu[i] = ec;
-      if (p_tot) p_tot[i] = __dadd_rn(eg, ec);  // total_wh = gpu_wh + cpu_wh (estimator.hpp:67)
-      if (p_dol) p_dol[i] = ed;
-      if (p_q) p_q[i] = eq;
+      // predicated, not branched: the warp stays converged, so every store
+      // instruction fills its window at once
+      const uint32_t i = static_cast<uint32_t>(o) - ga;
+      if (p_lat && act) p_lat[i] = cur[0];
+      if (p_gpu && act) p_gpu[i] = eg;
+      if (p_cpu && act) p_cpu[i] = ec;
+      if (p_tot && act) p_tot[i] = __dadd_rn(eg, ec);  // total_wh = gpu_wh + cpu_wh (estimator.hpp:67)
+      if (p_dol && act) p_dol[i] = ed;
+      if (p_q && act) p_q[i] = eq;
       o += 32;
-      if (o >= gb) break;
-      int carry = 0;  // suffix digits += digits of 32
+      if (o >= static_cast<int>(gb)) break;
+      int carry = 0;  // suffix digits += digits of 32 (a sat-out lane already points at its next plan)
 #pragma unroll
       for (int k = K - 1; k >= 0; --k) {
         const int x = ds[k] + step[k] + carry;
         carry = x >= rs[k];
-        ds[k] = carry ? x - rs[k] : x;
+        ds[k] = act ? (carry ? x - rs[k] : x) : ds[k];
+        carry = act ? carry : 0;
       }
     }
   }

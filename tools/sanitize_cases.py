@@ -1,7 +1,8 @@
 """Small invocations of every kernel family for compute-sanitizer
 (tools/sanitize.sh): hierarchical argmin (K = 2..4, energy / latency /
 quality primaries, register and shared-memory innermost tables), the
-one-plan-per-thread path, the batch kernel, Pareto and greedy."""
+one-plan-per-thread path, the batch kernel, Pareto, greedy, shard searches
+and the estimate-stream kernels."""
 import sys
 from pathlib import Path
 
@@ -34,4 +35,20 @@ f = loom.search_pareto_points(ctx, lw5.problem)
 loom.pareto_filter_points(ctx, f)
 w3 = W.config3(slo_us=None)
 loom.greedy_search(w3.dag, w3.library, {"constraint": "MIN_COST"}, w3.bounds, ctx=ctx)
+# shard searches with a common incumbent, and a range search that seeds itself
+w3s = W.config3()
+lw3 = loom.Lowered(w3s.dag, w3s.library, w3s.bounds)
+o3 = loom.objective(w3s.objective)
+for b in (0, 1 << 22, 5 << 30):
+    try:
+        loom.search_argmin_shard(ctx, lw3.problem, o3, b, b + (1 << 22))
+        loom.search_argmin(ctx, lw3.problem, o3, b, b + (1 << 22))
+    except loom.NoFeasibleConfigError:
+        pass
+# estimate streams: range (aligned and ragged) and gather
+import numpy as np  # noqa: E402
+loom.estimate_range(ctx, lw3.problem, 12345, 12345 + 70_000)
+loom.estimate_plans(ctx, lw3.problem, np.arange(0, 1 << 20, 997, dtype=np.uint64))
+lw1 = loom.Lowered(W.config1().dag, W.config1().library, W.config1().bounds)
+loom.estimate_range(ctx, lw1.problem, 0, lw1.total)
 print("sanitize cases done", len(f))
