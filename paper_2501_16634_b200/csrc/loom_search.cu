@@ -771,7 +771,10 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
         uint32_t hits = 0;
 #pragma unroll
         for (int st = 0; st < NV / 2; ++st) {
-          const double eu0 = __dadd_rn(ea, H.ga[off + 2 * st]), eu1 = __dadd_rn(ea, H.ga[off + 2 * st + 1]);
+          // kernel-parameter launches read the node's terms from the constant bank
+          const double gu0 = PT ? ip.gu[2 * st] : H.ga[off + 2 * st];
+          const double gu1 = PT ? ip.gu[2 * st + 1] : H.ga[off + 2 * st + 1];
+          const double eu0 = __dadd_rn(ea, gu0), eu1 = __dadd_rn(ea, gu1);
           hits |= static_cast<uint32_t>(in.any_energy2(ip, ctx_bound(H, eu0), ctx_bound(H, eu1))) << st;
         }
         LOOM_COUNT(3, NV / 2);
@@ -1908,6 +1911,8 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   b.full_only = full_only;
   b.nv = nv;
   for (int j = 0; j < 16; ++j) {
+    const int un = n - 2;  // node above the innermost
+    b.ip.gu[j] = (un >= 0 && j < p->radix[un]) ? ga[optoff[un] + j] : 0.0;
     b.ip.g[j] = j < inner_pad ? inner[j].g : INFINITY;
     b.ip.w[j] = j < inner_pad ? inner[j].w : INT_MAX;
     int64_t bits;

@@ -94,6 +94,7 @@ struct InnerParams {
   int32_t w[16];
   int32_t gh[16];  // high word of g: g <= t  =>  gh <= hi(t) for g >= 0 (ALU-pipe form of the energy test)
   float gf[16];    // g rounded down to binary32: g <= t  =>  gf <= round_up_f32(t) (FP32 form)
+  double gu[16];   // FP_A terms of the node above the innermost (its radix <= 16), for the unrolled sweep
 };
 
 // One plan's Pareto coordinates (40 bytes; same layout as loom_point).
