@@ -81,7 +81,7 @@ __device__ unsigned long long g_stats[8];
     if (LOOM_STATS) atomicAdd(&g_stats[i], (unsigned long long)(n)); \
   } while (0)
 #ifndef LOOM_PT_CTAS
-#define LOOM_PT_CTAS 2  // resident CTAs per SM of single-problem launches (register cap 128)
+#define LOOM_PT_CTAS 6  // resident CTAs per SM of single-problem launches (128 threads: register cap 80, 24 warps)
 #endif
 #ifndef LOOM_SWEEP_SYNC
 #define LOOM_SWEEP_SYNC 1  // reconverge after every innermost sweep (else once per subrow step)
@@ -1048,7 +1048,7 @@ __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
 }
 
 template <int K, int PRIM, int NV, bool PT>
-__global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 2)
+__global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
     search_kernel(const uint8_t* __restrict__ arena, const JobDesc* __restrict__ jobs, int ctas_per_job,
                   Rec* __restrict__ scratch, JobSync* __restrict__ sync, Rec* __restrict__ out,
                   const InnerParams ip) {

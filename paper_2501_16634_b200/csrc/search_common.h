@@ -13,7 +13,10 @@ constexpr int kMaxNodes = 32;
 constexpr int kMaxEdges = 512;
 constexpr int kMaxOptions = 6144;
 constexpr int kMaxBlobBytes = 200 * 1024;
-constexpr int kBlock = 256;
+#ifndef LOOM_BLOCK
+#define LOOM_BLOCK 128
+#endif
+constexpr int kBlock = LOOM_BLOCK;  // threads per CTA of the search / Pareto kernels
 
 // Criterion slots inside the kernels.  FP_A / FP_B are the (at most two)
 // floating-point sums the objective ranks on (gpu_wh and/or dollars); they
