@@ -79,11 +79,14 @@ struct DevBuf {
     }
     {
       std::lock_guard<std::mutex> g(c->pool_mu);
-      auto it = c->pool_free.find(k);
-      if (it != c->pool_free.end()) {
+      // best fit among free buffers up to twice the request: sizes that vary a
+      // little from call to call (Pareto candidate sets) reuse one buffer
+      // instead of a fresh cudaMalloc (which synchronises the device)
+      auto it = c->pool_free.lower_bound(k);
+      if (it != c->pool_free.end() && it->first <= 2 * k) {
         p = static_cast<T*>(it->second);
+        cls = it->first;
         c->pool_free.erase(it);
-        cls = k;
         return cudaSuccess;
       }
     }

@@ -1205,6 +1205,9 @@ size_t smem_bytes(size_t blob, int n_nodes) {
 }
 
 // ---------------------------------------------------------------------------
+// Threads per CTA of the Pareto kernels (independent of the search kernel's).
+constexpr int kPBlock = 256;
+
 // Pareto frontier (pareto_filter, optimizer.hpp:153-171, over estimate(p) for
 // every plan p in ConfigEnumerator order).  Dominance: a <= b on dollars,
 // gpu_wh (raw doubles) and latency, a.quality >= b.quality, one strict.
@@ -1331,7 +1334,7 @@ __device__ __forceinline__ bool guarded_warp(const GuardView& g, double d, doubl
 
 // Per-warp shared scratch of the Pareto evaluation: warp_dp's f[n][32] and
 // c[32] (int64).
-__host__ __device__ constexpr size_t pareto_dp_bytes(int n) { return dp_bytes_per_warp(n) * (kBlock / 32); }
+__host__ __device__ constexpr size_t pareto_dp_bytes(int n) { return dp_bytes_per_warp(n) * (kPBlock / 32); }
 
 // Phase 1 over [begin, end).  For n >= 3 the space is cut into groups that
 // fix every digit but the last three (x = n-3, u = n-2, w = n-1); groups are
@@ -1345,7 +1348,7 @@ __host__ __device__ constexpr size_t pareto_dp_bytes(int n) { return dp_bytes_pe
 // row (x fixed) -> plan; the plans of live rows are evaluated exactly and the
 // ones no guard point dominates are appended with warp-ballot compaction.
 // Range edges (partial groups) and n < 3 take the one-plan-per-thread path.
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kPBlock)
     pareto_eval_kernel(const uint8_t* __restrict__ blob_g, uint32_t blob_bytes, uint64_t begin, uint64_t end,
                        const ParetoPoint* __restrict__ guard, int n_guard, ParetoPoint* __restrict__ out,
                        uint64_t cap, unsigned long long* __restrict__ count, unsigned long long* __restrict__ stats,
@@ -1513,7 +1516,7 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // Points of an explicit list of plan indices (the guard sample).
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kPBlock)
     pareto_points_kernel(const uint8_t* __restrict__ blob_g, uint32_t blob_bytes, const uint64_t* __restrict__ idx,
                          uint64_t n, ParetoPoint* __restrict__ out) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1530,7 +1533,7 @@ __global__ void __launch_bounds__(kBlock)
 
 // Candidate refinement: keep the candidates no guard point dominates
 // (guard points are real plans, so this never drops a frontier point).
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kPBlock)
     pareto_prefilter_kernel(const ParetoPoint* __restrict__ in, uint64_t n, const ParetoPoint* __restrict__ guard,
                             int n_guard, ParetoPoint* __restrict__ out, unsigned long long* __restrict__ count) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1552,7 +1555,7 @@ __global__ void __launch_bounds__(kBlock)
 // span > 0: point i is compared only with the points of its own span-sized
 // block (a multiple of the CTA size) -- the first stage of a blocked filter,
 // exact because frontier(A u B) = frontier(frontier(A) u frontier(B)).
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kPBlock)
     pareto_filter_kernel(const ParetoPoint* __restrict__ pts, uint64_t n, uint8_t* __restrict__ keep,
                          uint64_t span) {
   constexpr int T = 512;
@@ -2581,9 +2584,9 @@ int filter_device(loom_ctx* c, const ParetoPoint* d_pts, uint64_t n, std::vector
   constexpr uint64_t kSpan = 8192;
   DevBuf<uint8_t> keep(c);
   LOOM_CUDA(keep.alloc(n));
-  const uint64_t blocks = (n + kBlock - 1) / kBlock;
+  const uint64_t blocks = (n + kPBlock - 1) / kPBlock;
   const uint64_t span = n > 2 * kSpan ? kSpan : 0;
-  pareto_filter_kernel<<<static_cast<unsigned>(blocks), kBlock, 0, c->stream>>>(d_pts, n, keep.p, span);
+  pareto_filter_kernel<<<static_cast<unsigned>(blocks), kPBlock, 0, c->stream>>>(d_pts, n, keep.p, span);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   std::vector<uint8_t> hk(n);
@@ -2645,8 +2648,8 @@ int refine_and_filter(loom_ctx* c, ParetoPoint* d_in, uint64_t n, std::vector<Pa
     LOOM_CUDA(cudaMemcpyAsync(d_g.p, guard.data(), guard.size() * sizeof(ParetoPoint), cudaMemcpyHostToDevice,
                               c->stream));
     LOOM_CUDA(cudaMemsetAsync(d_cnt.p, 0, sizeof(unsigned long long), c->stream));
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + kBlock - 1) / kBlock, uint64_t(c->sms) * 8));
-    pareto_prefilter_kernel<<<grid, kBlock, gsmem, c->stream>>>(cur, n, d_g.p, static_cast<int>(guard.size()), nxt,
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + kPBlock - 1) / kPBlock, uint64_t(c->sms) * 8));
+    pareto_prefilter_kernel<<<grid, kPBlock, gsmem, c->stream>>>(cur, n, d_g.p, static_cast<int>(guard.size()), nxt,
                                                                 d_cnt.p);
     LOOM_CUDA(cudaGetLastError());
     ++c->launches;
@@ -2698,7 +2701,7 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
     LOOM_CUDA(d_idx.alloc(kSample));
     LOOM_CUDA(d_s.alloc(kSample));
     LOOM_CUDA(cudaMemcpyAsync(d_idx.p, idx.data(), kSample * 8, cudaMemcpyHostToDevice, c->stream));
-    pareto_points_kernel<<<static_cast<unsigned>(kSample / kBlock), kBlock, bytes + 128, c->stream>>>(
+    pareto_points_kernel<<<static_cast<unsigned>(kSample / kPBlock), kPBlock, bytes + 128, c->stream>>>(
         d_blob.p, bytes, d_idx.p, kSample, d_s.p);
     LOOM_CUDA(cudaGetLastError());
     ++c->launches;
@@ -2715,12 +2718,12 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
   LOOM_CUDA(d_guard.alloc(kGuardMax));
   LOOM_CUDA(d_count.alloc(1));
   int resident = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, reinterpret_cast<const void*>(pareto_eval_kernel), kBlock,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, reinterpret_cast<const void*>(pareto_eval_kernel), kPBlock,
                                                 smem);
   const uint64_t units = n / 64 + 1;
   const unsigned grid =
       static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(c->sms) * std::max(1, resident),
-                                                                     (units + kBlock - 1) / kBlock)));
+                                                                     (units + kPBlock - 1) / kPBlock)));
   for (int attempt = 0; attempt < 6; ++attempt) {
     const auto t0 = std::chrono::steady_clock::now();
     unsigned long long count = 0;
@@ -2735,7 +2738,7 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
       LOOM_CUDA(cudaMemsetAsync(d_stats.p, 0, 32, c->stream));
     }
     LOOM_CUDA(cudaMemsetAsync(d_next.p, 0, sizeof(unsigned long long), c->stream));
-    pareto_eval_kernel<<<grid, kBlock, smem, c->stream>>>(d_blob.p, bytes, begin, end, d_guard.p,
+    pareto_eval_kernel<<<grid, kPBlock, smem, c->stream>>>(d_blob.p, bytes, begin, end, d_guard.p,
                                                           static_cast<int>(guard.size()), d_cand.p, cap, d_count.p,
                                                           d_stats.p, d_next.p);
     if (dbg) {
@@ -2816,7 +2819,7 @@ extern "C" int loom_pareto_filter_points(loom_ctx* c, const loom_point* pts, uin
   LOOM_CUDA(d.alloc(n));
   LOOM_CUDA(k.alloc(n));
   LOOM_CUDA(cudaMemcpyAsync(d.p, pts, n * sizeof(loom_point), cudaMemcpyHostToDevice, c->stream));
-  pareto_filter_kernel<<<static_cast<unsigned>((n + kBlock - 1) / kBlock), kBlock, 0, c->stream>>>(d.p, n, k.p, 0);
+  pareto_filter_kernel<<<static_cast<unsigned>((n + kPBlock - 1) / kPBlock), kPBlock, 0, c->stream>>>(d.p, n, k.p, 0);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(keep, k.p, n, cudaMemcpyDeviceToHost, c->stream));
