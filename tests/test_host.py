@@ -6,6 +6,7 @@ error behaviour mirror the reference."""
 import ctypes as C
 import random
 import subprocess
+from pathlib import Path
 
 import pytest
 
@@ -185,3 +186,25 @@ def test_dag_fast_reader_equals_dom_reader(loomlib):
                 '[1, 2]', '{"nodes": [], "edges": []} trailing'):
         with pytest.raises(loom.LoomError):
             loom.Lowered(bad, w.library, w.bounds)
+
+
+def test_bench_fast_path_matches_compiled_sass(loomlib):
+    """bench.py's roofline divides by the compiled fast path's instruction
+    counts; they must be the ones in the object file that was built (the
+    fully unrolled energy-first sweep of search_kernel<4, kPrimFp, 16, true>)."""
+    import shutil
+    import subprocess
+    import sys
+    if not (shutil.which("cuobjdump") or Path("/usr/local/cuda/bin/cuobjdump").exists()):
+        pytest.skip("no cuobjdump")
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "tools" / "sass_blocks.py"), "4", "0", "16", "1", "200"],
+                         capture_output=True, text=True, check=True).stdout
+    import re
+    rows = [tuple(int(x) for x in re.search(r"issue\s+(\d+)\s+alu\s+(\d+)\s+fp64\s+(\d+)", l).groups())
+            for l in out.splitlines() if "issue" in l]
+    assert rows, out
+    sys.path.insert(0, str(root))
+    import bench
+    fp = bench.FAST_PATH
+    assert (fp["issue"], fp["alu"], fp["fp64"]) in rows, (fp, rows)
