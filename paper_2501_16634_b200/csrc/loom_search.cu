@@ -650,13 +650,17 @@ struct Inner {
 __device__ __forceinline__ double ctx_bound(const Hot& H, double eu) { return __dadd_ru(H.hi_up, -eu); }
 
 template <int K>
-__device__ __forceinline__ int64_t* coef_col(uint8_t* coef_base, int J) {
+__device__ __forceinline__ int64_t* coef_col(uint8_t* coef_base, int J, bool lazy = false) {
   int off = 0;
-  for (int j = 1; j < J; ++j) off += 1 << (K - j);
+  if (!lazy)  // lazy sweeps keep only the innermost pair's column, at offset 0
+    for (int j = 1; j < J; ++j) off += 1 << (K - j);
   return reinterpret_cast<int64_t*>(coef_base) + off * kBlock + threadIdx.x;
 }
 
 constexpr int kCoefEntries = 8 + 4;  // K = 4: levels 1 and 2
+// Coefficient entries per thread: every suffix level's column, or only the
+// innermost pair's (4) when the sweep folds latency lazily.
+__host__ __device__ constexpr int coef_entries(bool lazy) { return lazy ? 4 : kCoefEntries; }
 
 // The suffix-level-J input coefficient vector (entries 0..3 are all the
 // innermost pair needs), folded from the row's level-0 vector through the
@@ -692,7 +696,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
   // level 0 reads the thread's local vector (stride 1), deeper levels their
   // shared-memory column (stride kBlock)
   constexpr int SI = J == 0 ? 1 : kBlock;
-  const int64_t* cin = J == 0 ? H.c0 : coef_col<K>(H.coef_base, J);
+  const int64_t* cin = J == 0 ? H.c0 : coef_col<K>(H.coef_base, J, kLazyCoef<PRIM, NV>);
   if constexpr (J == K - 2) {
     const int n_in = H.radix[node + 1];
     const int64_t wmin = H.h->inner_wmin, wu_max = H.h->pre_wmax;
@@ -861,7 +865,7 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
     }
   } else {
     constexpr int NS = 1 << (K - J - 1);
-    int64_t* cout = coef_col<K>(H.coef_base, J + 1);
+    int64_t* cout = coef_col<K>(H.coef_base, J + 1, kLazyCoef<PRIM, NV>);
     for (int o = o_lo; o < o_hi; ++o) {
       if constexpr (!kLazyCoef<PRIM, NV>) {
         const int64_t w = H.wall[off + o];
@@ -1097,7 +1101,7 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
     const uint64_t g_first = jd.sub_lo / G, g_end = (jd.sub_hi - 1) / G + 1;
     const uint64_t lane = threadIdx.x & 31;
     uint8_t* coef_base = slot_base + kSlotBytes * kBlock;
-    uint8_t* dp_base = coef_base + sizeof(int64_t) * kCoefEntries * kBlock;
+    uint8_t* dp_base = coef_base + sizeof(int64_t) * coef_entries(kLazyCoef<PRIM, NV>) * kBlock;
     int64_t* fw = reinterpret_cast<int64_t*>(dp_base + dp_bytes_per_warp(h->n_nodes) * (threadIdx.x >> 5));
     int64_t* cw = fw + 32 * h->n_nodes;
     const int P = h->n_nodes - K;
@@ -1199,9 +1203,9 @@ KernelFn pick_kernel(int K, int prim, int nv, bool pt) {
 // Dynamic shared memory of a launch: problem image + per-thread slots.
 // (coefficient columns sized for K = 4: 8 + 4 entries per thread)
 // + per-warp DP scratch
-size_t smem_bytes(size_t blob, int n_nodes) {
-  return ((blob + 127) & ~size_t(127)) + static_cast<size_t>(kSlotBytes) * kBlock + sizeof(int64_t) * kCoefEntries * kBlock +
-         dp_bytes_per_warp(n_nodes) * (kBlock / 32);
+size_t smem_bytes(size_t blob, int n_nodes, bool lazy) {
+  return ((blob + 127) & ~size_t(127)) + static_cast<size_t>(kSlotBytes) * kBlock +
+         sizeof(int64_t) * coef_entries(lazy) * kBlock + dp_bytes_per_warp(n_nodes) * (kBlock / 32);
 }
 
 // ---------------------------------------------------------------------------
@@ -1685,6 +1689,9 @@ struct Built {
 };
 
 int align16(int x) { return (x + 15) & ~15; }
+
+// The kernel instantiation a Built picks folds latency lazily (kLazyCoef).
+bool lazy_of(const Built& b) { return b.prim == kPrimFp && b.nv > 0 && LOOM_ENERGY_FIRST; }
 
 int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_threads, Built& b) {
   uint64_t total = 0;
@@ -2300,18 +2307,18 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
   KernelFn fn = pick_kernel(b.K, b.prim, b.nv, true);
-  if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes))) return rc;
-  const int ctas = ctas_for(c, units, fn, smem_bytes(b.blob.size(), p->n_nodes));
+  if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
+  const int ctas = ctas_for(c, units, fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)));
   if (int rc = ensure(c->d_arena, c->arena_cap, b.blob.size())) return rc;
   if (int rc = ensure(c->d_jobs, c->jobs_cap, 1)) return rc;
   if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(ctas))) return rc;
   if (int rc = ensure_tickets(c, 1)) return rc;
   if (int rc = ensure(c->d_out, c->out_cap, 1)) return rc;
   if (int rc = ensure_host(c, 1)) return rc;
-  if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes))) return rc;
+  if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  fn<<<ctas, kBlock, smem_bytes(b.blob.size(), p->n_nodes), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch,
+  fn<<<ctas, kBlock, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch,
                                                                    c->d_tickets, c->d_out, b.ip);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
@@ -2366,7 +2373,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
       g = &groups.back();
     }
     g->jobs.push_back(j);
-    g->smem = std::max(g->smem, smem_bytes(built[j].blob.size(), problems[j].n_nodes));
+    g->smem = std::max(g->smem, smem_bytes(built[j].blob.size(), problems[j].n_nodes, lazy_of(built[j])));
   }
   // One arena for all images; one launch per group, one CTA per job.
   std::vector<uint64_t> off(n_jobs, 0);
@@ -2469,11 +2476,11 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   dp->host.edge_to = dp->eto.data();
   dp->objective = *o;
   dp->fn = pick_kernel(dp->built.K, dp->built.prim, dp->built.nv, true);
-  if (set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)) != LOOM_OK) {
+  if (set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built))) != LOOM_OK) {
     delete dp;
     return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: cannot size shared memory");
   }
-  const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes));
+  const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)));
   dp->ctas = ctas;
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
@@ -2484,7 +2491,7 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
              cudaMemcpy(dp->d_blob, dp->built.blob.data(), dp->built.blob.size(), cudaMemcpyHostToDevice) ==
                  cudaSuccess &&
              cudaMemset(dp->d_ticket, 0, sizeof(JobSync)) == cudaSuccess;
-  if (!okk || set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)) != LOOM_OK) {
+  if (!okk || set_smem(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built))) != LOOM_OK) {
     loom_problem_release(dp);
     return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: upload failed");
   }
@@ -2519,9 +2526,9 @@ int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint
   d.blob_off = 0;
   if (d.begin >= d.end) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: empty range");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
-  const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes)));
+  const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built))));
   LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  dp->fn<<<ctas, kBlock, smem_bytes(dp->built.blob.size(), dp->host.n_nodes), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
+  dp->fn<<<ctas, kBlock, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
                                                              dp->d_ticket, dp->d_out, dp->built.ip);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
