@@ -29,6 +29,7 @@
 #include "loom_b200/loom.hpp"
 
 #include <algorithm>
+#include <charconv>
 #include <climits>
 #include <cmath>
 #include <numeric>
@@ -372,13 +373,32 @@ int NodeAssignment::fan_out() const {
 }
 
 std::string assignment_token(const std::string& node_id, const NodeAssignment& a) {
-  std::string s = node_id + "=" + a.implementation + "[";
+  // "<node_id>=<impl>[<sku>:<units>x<workers>(+...)]p<paths>;" (config.hpp:49-61),
+  // built in one buffer
+  std::size_t n = node_id.size() + a.implementation.size() + 16;
+  for (const Placement& p : a.placements) n += p.sku.size() + 24;
+  std::string s;
+  s.reserve(n);
+  char num[16];
+  auto put_int = [&](int v) {
+    const auto r = std::to_chars(num, num + sizeof num, v);
+    s.append(num, r.ptr);
+  };
+  s += node_id;
+  s += '=';
+  s += a.implementation;
+  s += '[';
   for (std::size_t i = 0; i < a.placements.size(); ++i) {
-    if (i) s += "+";
-    s += a.placements[i].sku + ":" + std::to_string(a.placements[i].units) + "x" +
-         std::to_string(a.placements[i].workers);
+    if (i) s += '+';
+    s += a.placements[i].sku;
+    s += ':';
+    put_int(a.placements[i].units);
+    s += 'x';
+    put_int(a.placements[i].workers);
   }
-  s += "]p" + std::to_string(a.path_count) + ";";
+  s += "]p";
+  put_int(a.path_count);
+  s += ';';
   return s;
 }
 
@@ -423,16 +443,6 @@ int chunk_capacity(double work, double min_chunk) {
   return std::max(1, static_cast<int>(std::floor(work / min_chunk)));
 }
 
-namespace {
-// Equal split: count = clamp(min(fan_out, floor(work / min_chunk)), 1, ..).
-std::vector<double> equal_split(double work, int fan_out, double min_chunk) {
-  int count = 1;
-  if (fan_out > 1 && min_chunk > 0)
-    count = std::max(1, std::min(fan_out, static_cast<int>(std::floor(work / min_chunk))));
-  return std::vector<double>(static_cast<std::size_t>(count), work / count);
-}
-}  // namespace
-
 std::vector<double> water_fill_split(double work, double min_chunk, const std::vector<double>& speeds) {
   // Quanta of work/quanta each go to the worker that would finish it first;
   // strict '<' keeps ties on the lower worker index.
@@ -476,14 +486,20 @@ struct Worker {
 NodePlan plan_workers(const DagNode& node, const Worker* workers, std::size_t n_workers, std::size_t n_placements,
                       int fan) {
   const auto where = [&] { return "node '" + node.id + "'"; };
+  // One worker, or equal chunks (split_task, chunking.hpp:17-24): every
+  // worker's chunk is the same value, no vector needed (this runs once per
+  // option during lowering).  Hybrids water-fill (chunking.hpp:35-58).
   std::vector<double> chunk;
+  double equal = node.work_units;
   if (n_workers == 1) {
-    chunk = {node.work_units};
   } else if (n_placements <= 1) {
-    chunk = equal_split(node.work_units, fan, node.min_chunk);
-    if (static_cast<int>(chunk.size()) != fan)
+    int count = 1;
+    if (fan > 1 && node.min_chunk > 0)
+      count = std::max(1, std::min(fan, static_cast<int>(std::floor(node.work_units / node.min_chunk))));
+    if (count != fan)
       throw InvalidConfigError(where() + ": fan-out " + std::to_string(fan) + " exceeds the chunk capacity of " +
                                std::to_string(chunk_capacity(node.work_units, node.min_chunk)));
+    equal = node.work_units / count;  // equal_split's value
   } else {
     std::vector<double> speeds;
     for (std::size_t w = 0; w < n_workers; ++w) speeds.push_back(workers[w].profile->throughput);
@@ -496,7 +512,7 @@ NodePlan plan_workers(const DagNode& node, const Worker* workers, std::size_t n_
   for (std::size_t w = 0; w < n_workers; ++w) {
     const Worker& r = workers[w];
     const Micros setup = to_micros(r.profile->setup_seconds);
-    const Micros run = to_micros(chunk[w] / r.profile->throughput);
+    const Micros run = to_micros((chunk.empty() ? equal : chunk[w]) / r.profile->throughput);
     const Micros dur = setup + run;
     plan.wall_us = std::max(plan.wall_us, dur);
     const double hours = to_seconds(dur) / 3600.0;
@@ -795,12 +811,23 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
   };
 
   L.total = n ? 1 : 0;
+  // per-node scratch reused across nodes; the tables grow by whole nodes
+  std::vector<NodePlan> plans;
+  std::vector<const Implementation*> impls;
+  std::vector<std::string> tokens;
+  std::vector<int> order;
+  std::vector<int32_t> rank;
+  plans.reserve(32);
+  impls.reserve(32);
+  L.radix.reserve(n);
+  L.options.reserve(n);
   for (int i = 0; i < n; ++i) {
     const DagNode& node = dag.nodes[i];
     check_name(node.id);
     std::vector<NodeAssignment> opts;
-    std::vector<NodePlan> plans;
-    std::vector<const Implementation*> impls;
+    opts.reserve(32);
+    plans.clear();
+    impls.clear();
     enumerate_options(node, library, bounds, opts, &plans, &impls);
     const int r = static_cast<int>(opts.size());
     L.radix.push_back(r);
@@ -809,7 +836,13 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
       throw InvalidConfigError("plan space exceeds 2^64 plans");
     else L.total *= static_cast<uint64_t>(r);
 
-    std::vector<std::string> tokens;
+    tokens.clear();
+    tokens.reserve(r);
+    const std::size_t base = L.wall_us.size();
+    for (auto* v : {&L.gpu_wh, &L.cpu_wh, &L.dollars}) v->reserve(base + r);
+    L.wall_us.reserve(base + r);
+    L.quality.reserve(base + r);
+    L.lexrank.reserve(base + r);
     for (int o = 0; o < r; ++o) {
       const NodeAssignment& a = opts[o];
       check_name(a.implementation);
@@ -823,10 +856,10 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
       L.quality.push_back(node_quality(node, *impls[o], a.path_count));
       tokens.push_back(assignment_token(node.id, a));
     }
-    std::vector<int> order(r);
+    order.resize(r);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tokens[a] < tokens[b]; });
-    std::vector<int32_t> rank(r);
+    rank.resize(r);
     for (int k = 0; k < r; ++k) rank[order[k]] = k;
     L.lexrank.insert(L.lexrank.end(), rank.begin(), rank.end());
     L.options.push_back(std::move(opts));
