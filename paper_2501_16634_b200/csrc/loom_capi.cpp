@@ -3,6 +3,9 @@
 // winner records (multi-rank combine), reference-format JSON lowering, and the
 // drop-in entry points loom::exhaustive_search / loom_exhaustive_search_json.
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -542,15 +545,39 @@ int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const 
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   loom_objective obj;
   if (int rc = loom_objective_parse(objective_json, &obj)) return rc;
+  const bool trace = std::getenv("LOOM_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[loom trace] search_batch %s %.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  };
   std::vector<loom_lowered*> lw(n, nullptr);
   std::vector<int32_t> lst(n, LOOM_OK);
   int rc = loom_lower_batch(library_json, bounds_json, dag_jsons, n, threads, lw.data(), lst.data());
+  mark("lower");
   if (rc == LOOM_OK) {
     rc = loom_search_argmin_lowered(ctx, lw.data(), n, &obj, out, status);
     for (int i = 0; i < n; ++i)
       if (lst[i] != LOOM_OK) status[i] = lst[i];
   }
-  for (loom_lowered* h : lw) loom_lowered_destroy(h);
+  mark("search");
+  // the lowered problems hold ~100 small allocations each: free them on the
+  // same host threads that made them
+  const int t = std::max(1, std::min<int>(n, threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()))));
+  if (t > 1 && n >= 256) {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < t; ++w)
+      pool.emplace_back([&, w] {
+        for (int i = w; i < n; i += t) loom_lowered_destroy(lw[i]);
+      });
+    for (auto& th : pool) th.join();
+  } else {
+    for (loom_lowered* h : lw) loom_lowered_destroy(h);
+  }
+  mark("free");
   return rc;
 }
 
