@@ -294,3 +294,31 @@ def test_shard_search_with_incumbent_combines_to_argmin(ctx, cfg, ranks):
 def _feasible(est: dict, w) -> bool:
     slo = w.objective.get("latency_slo_us") if isinstance(w.objective, dict) else None
     return slo is None or est["latency_us"] <= slo
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_energy_first_under_binding_slos_vs_oracle(ctx, seed):
+    """The energy-first sweep flags every context whose best option beats the
+    running bound; with a tight latency SLO the low-energy plans are mostly
+    infeasible, so the flagged path (two-criteria re-test, lazy latency
+    coefficients, exact scan) carries the search.  C3-shaped problems with
+    SLOs at the 1st / 10th / 50th latency percentile of a sample, MIN_COST and
+    MIN_DOLLARS, 2^22-plan slices, against the CPU oracle."""
+    w0 = W.config3(seed=seed, slo_us=None)
+    lw = loom.Lowered(w0.dag, w0.library, w0.bounds)
+    p = O.problem(w0.dag, w0.library, w0.bounds)
+    rng = random.Random(seed)
+    sample = sorted(lw.evaluate(rng.randrange(lw.total))["latency_us"] for _ in range(400))
+    for pct in (0.01, 0.10, 0.50):
+        slo = sample[int(pct * (len(sample) - 1))]
+        for token in ("MIN_COST", "MIN_DOLLARS"):
+            obj = {"constraint": token, "latency_slo_us": slo}
+            b = rng.randrange(lw.total - (1 << 22))
+            e = b + (1 << 22)
+            ref = O.argmin(p, obj, b, e, threads=cpu_threads())  # None: nothing feasible
+            if ref is None:
+                with pytest.raises(loom.NoFeasibleConfigError):
+                    loom.search_argmin(ctx, lw.problem, loom.objective(obj), b, e)
+                continue
+            got = loom.search_argmin(ctx, lw.problem, loom.objective(obj), b, e)
+            _check_oracle(got, ref)
