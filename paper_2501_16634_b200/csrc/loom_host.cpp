@@ -595,7 +595,8 @@ void enumerate_options(const DagNode& node, const AgentLibrary& library, const S
 
   auto emit = [&](const Implementation* impl, std::vector<Placement> placements, const NodePlan* plan) {
     for (int k = 1; k <= paths_max; ++k) {
-      out.push_back({impl->name, placements, k});
+      if (k < paths_max) out.push_back({impl->name, placements, k});
+      else out.push_back({impl->name, std::move(placements), k});  // the last path takes the vector
       if (plans) plans->push_back(*plan);
       if (impls) impls->push_back(impl);
     }
