@@ -1238,22 +1238,35 @@ struct GuardView {
   int n;
 };
 
+// Four guard points per step: independent compare chains and one branch per
+// four points (most points do not dominate, so the scan usually runs to the
+// end; one point per step was latency-bound on the compare -> branch chain).
+__device__ __forceinline__ int guard_scan(const GuardView& g, int k0, double d, double e, int64_t l, int32_t q) {
+  int k = k0;
+  for (; k + 4 <= g.n; k += 4) {
+    const bool a0 = dominates(g.d[k], g.e[k], g.l[k], g.q[k], d, e, l, q);
+    const bool a1 = dominates(g.d[k + 1], g.e[k + 1], g.l[k + 1], g.q[k + 1], d, e, l, q);
+    const bool a2 = dominates(g.d[k + 2], g.e[k + 2], g.l[k + 2], g.q[k + 2], d, e, l, q);
+    const bool a3 = dominates(g.d[k + 3], g.e[k + 3], g.l[k + 3], g.q[k + 3], d, e, l, q);
+    if (a0 | a1 | a2 | a3) return a0 ? k : a1 ? k + 1 : a2 ? k + 2 : k + 3;
+  }
+  for (; k < g.n; ++k)
+    if (dominates(g.d[k], g.e[k], g.l[k], g.q[k], d, e, l, q)) return k;
+  return -1;
+}
+
 __device__ __forceinline__ bool guarded(const GuardView& g, double d, double e, int64_t l, int32_t q) {
-  for (int k = 0; k < g.n; ++k)
-    if (dominates(g.d[k], g.e[k], g.l[k], g.q[k], d, e, l, q)) return true;
-  return false;
+  return guard_scan(g, 0, d, e, l, q) >= 0;
 }
 
 // Same, trying the previous plan's dominator first (consecutive plans of a
 // thread differ in one digit, so the same guard point usually dominates).
 __device__ __forceinline__ bool guarded_hint(const GuardView& g, int& hint, double d, double e, int64_t l, int32_t q) {
   if (hint < g.n && dominates(g.d[hint], g.e[hint], g.l[hint], g.q[hint], d, e, l, q)) return true;
-  for (int k = 0; k < g.n; ++k)
-    if (dominates(g.d[k], g.e[k], g.l[k], g.q[k], d, e, l, q)) {
-      hint = k;
-      return true;
-    }
-  return false;
+  const int k = guard_scan(g, 0, d, e, l, q);
+  if (k < 0) return false;
+  hint = k;
+  return true;
 }
 
 // One plan's point from its digits (estimate restated; slot A = gpu_wh,
