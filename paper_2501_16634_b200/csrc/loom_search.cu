@@ -2710,6 +2710,7 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes + 128)));
 
   // guard: exact frontier of an evenly strided sample of the range
+  const auto t_guard = std::chrono::steady_clock::now();
   std::vector<ParetoPoint> guard;
   const uint64_t kSample = 1 << 16;
   if (n > kSample) {
@@ -2728,6 +2729,9 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
     std::vector<ParetoPoint> f0;
     if (int rc = filter_device(c, d_s.p, kSample, f0)) return rc;
     guard = guard_of(f0);
+    if (std::getenv("LOOM_DEBUG"))
+      std::fprintf(stderr, "[loom pareto] guard build %.3fs (sample frontier %zu)\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t_guard).count(), f0.size());
   }
 
   const uint64_t cap = std::min<uint64_t>(uint64_t(1) << 22, n);
