@@ -338,14 +338,15 @@ def b200_arm(args) -> None:
 
 
 # Compiled fast path of the innermost contexts of search_kernel<4, kPrimFp,
-# 16, true> (tools/sass_blocks.py 4 0 16 1): one fully unrolled sweep over
-# the 16 options of the node above the innermost = 256 plans per lane in 338
-# SASS instructions -- 128 DSETP.LE.OR and 128 ISETP.LE.OR (one compare per
-# plan on its primary criterion: half the options on the FP64 pipe, half on
-# the ALU pipe with high words), 32 DADD, 24 LDCU (tables from the constant
-# bank), step flags -- of which 149 run on the ALU pipe and 160 on the FP64
-# pipe: issue-bound.  DESIGN.md §5.
-FAST_PATH = {"issue": 338, "alu": 149, "fp64": 160, "plans_per_lane": 256}
+# 16, true> (tools/sass_blocks.py 4 0 16 1): one fully unrolled block sweeps
+# two options of the node two above the innermost x the 16 options of the
+# node above it = 512 plans per lane in 675 SASS instructions -- 256
+# DSETP.LE.OR and 256 ISETP.LE.OR (one compare per plan on its primary
+# criterion: half the options on the FP64 pipe, half on the ALU pipe with
+# high words), 66 DADD, 24 LDCU (tables from the constant bank), step flags
+# -- of which 301 run on the ALU pipe and 322 on the FP64 pipe: issue-bound.
+# DESIGN.md §5.
+FAST_PATH = {"issue": 675, "alu": 301, "fp64": 322, "plans_per_lane": 512}
 
 
 def other_configs(ctx, loom, W) -> dict:

@@ -89,6 +89,9 @@ __device__ unsigned long long g_stats[8];
 #ifndef LOOM_F32_SPLIT
 #define LOOM_F32_SPLIT 0  // energy-first sweep: also use the FP32 pipe (experiment)
 #endif
+#ifndef LOOM_SWEEP_PAIRS
+#define LOOM_SWEEP_PAIRS 1  // energy-first: two sweeps per unrolled block (level K-3)
+#endif
 #ifndef LOOM_JOB_BOUND
 #define LOOM_JOB_BOUND 1
 #endif
@@ -671,6 +674,10 @@ __host__ __device__ constexpr int coef_entries(bool lazy) { return lazy ? 4 : kC
 template <int PRIM, int NV>
 constexpr bool kLazyCoef = PRIM == kPrimFp && NV > 0 && LOOM_ENERGY_FIRST;
 
+// level(): sweep normally, or (paired sweeps, see level K-3) only handle the
+// given flagged steps of an already swept node -- no sweep, no warp sync.
+constexpr uint32_t kNoPreHits = 0xffffffffu;
+
 template <int K>
 __device__ __noinline__ void lazy_coef(const int64_t* c0, const int64_t* wall, const int32_t* optoff, int P, int J,
                                        int o0, int o1, int64_t* out) {
@@ -689,7 +696,7 @@ __device__ __noinline__ void lazy_coef(const int64_t* c0, const int64_t* wall, c
 template <int K, int PRIM, int NV, bool PT, int J>
 __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, const InnerParams& ip, double ea,
                                       int32_t qv, uint64_t lex,
-                                      int o_lo, int o_hi, uint64_t ibase) {
+                                      int o_lo, int o_hi, uint64_t ibase, uint32_t pre_hits = kNoPreHits) {
   const int node = H.P + J;
   const int off = H.optoff[node];
   const int n = H.radix[node];
@@ -769,6 +776,10 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
           }
         }
       };
+      if (pre_hits != kNoPreHits) {  // flagged steps of a paired sweep (level K-3)
+        flagged(pre_hits, 0, NV);
+        return;
+      }
       if (ef && n == NV && o_lo == 0 && o_hi == NV) {
         // The whole node above the innermost, radix == NV: one fully
         // unrolled sweep of NV/2 steps, branch-free step flags.
@@ -866,6 +877,43 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
   } else {
     constexpr int NS = 1 << (K - J - 1);
     int64_t* cout = coef_col<K>(H.coef_base, J + 1, kLazyCoef<PRIM, NV>);
+    if constexpr (J == K - 3 && kLazyCoef<PRIM, NV> && PT && LOOM_SWEEP_PAIRS) {
+      // Paired sweeps: two options of this node per unrolled block (512
+      // plans per lane), sharing the per-sweep setup; flagged steps are
+      // handed to the child level afterwards, then the warp reconverges once.
+      if (H.radix[node + 1] == NV && ((o_hi - o_lo) & 1) == 0) {
+        for (int o = o_lo; o < o_hi; o += 2) {
+          const double e2a = __dadd_rn(ea, H.ga[off + o]), e2b = __dadd_rn(ea, H.ga[off + o + 1]);
+          uint32_t ha = 0, hb = 0;
+#pragma unroll
+          for (int st = 0; st < NV / 2; ++st) {
+            ha |= static_cast<uint32_t>(in.any_energy2(ip, ctx_bound(H, __dadd_rn(e2a, ip.gu[2 * st])),
+                                                       ctx_bound(H, __dadd_rn(e2a, ip.gu[2 * st + 1]))))
+                  << st;
+            hb |= static_cast<uint32_t>(in.any_energy2(ip, ctx_bound(H, __dadd_rn(e2b, ip.gu[2 * st])),
+                                                       ctx_bound(H, __dadd_rn(e2b, ip.gu[2 * st + 1]))))
+                  << st;
+          }
+          LOOM_COUNT(3, NV);
+          LOOM_COUNT(0, __popc(ha) + __popc(hb));
+          if (__builtin_expect(ha != 0, 0)) {
+            H.od[J] = o;
+            const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o);
+            level<K, PRIM, NV, PT, J + 1>(H, in, ip, e2a, INT_MAX, lex + H.lexw[off + o], 0, NV, ib, ha);
+          }
+          if (__builtin_expect(hb != 0, 0)) {
+            H.od[J] = o + 1;
+            const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o + 1);
+            level<K, PRIM, NV, PT, J + 1>(H, in, ip, e2b, INT_MAX, lex + H.lexw[off + o + 1], 0, NV, ib, hb);
+          }
+          if (LOOM_SWEEP_SYNC) {
+            if (H.sync_mask == 0xffffffffu) __syncwarp();
+            else __syncwarp(H.sync_mask);
+          }
+        }
+        return;
+      }
+    }
     for (int o = o_lo; o < o_hi; ++o) {
       if constexpr (!kLazyCoef<PRIM, NV>) {
         const int64_t w = H.wall[off + o];
