@@ -90,7 +90,10 @@ __device__ unsigned long long g_stats[8];
 #define LOOM_F32_SPLIT 0  // energy-first sweep: also use the FP32 pipe (experiment)
 #endif
 #ifndef LOOM_SWEEP_PAIRS
-#define LOOM_SWEEP_PAIRS 1  // energy-first: two sweeps per unrolled block (level K-3)
+#define LOOM_SWEEP_PAIRS 1  // energy-first: several sweeps per unrolled block (level K-3)
+#endif
+#ifndef LOOM_SWEEP_GROUP
+#define LOOM_SWEEP_GROUP 2  // sweeps per block
 #endif
 #ifndef LOOM_JOB_BOUND
 #define LOOM_JOB_BOUND 1
@@ -881,30 +884,32 @@ __device__ __forceinline__ void level(Hot& H, const Inner<K, PRIM, NV, PT>& in, 
       // Paired sweeps: two options of this node per unrolled block (512
       // plans per lane), sharing the per-sweep setup; flagged steps are
       // handed to the child level afterwards, then the warp reconverges once.
-      if (H.radix[node + 1] == NV && ((o_hi - o_lo) & 1) == 0) {
-        for (int o = o_lo; o < o_hi; o += 2) {
-          const double e2a = __dadd_rn(ea, H.ga[off + o]), e2b = __dadd_rn(ea, H.ga[off + o + 1]);
-          uint32_t ha = 0, hb = 0;
+      constexpr int GS = LOOM_SWEEP_GROUP;  // options of this node per block
+      if (H.radix[node + 1] == NV && (o_hi - o_lo) % GS == 0) {
+        for (int o = o_lo; o < o_hi; o += GS) {
+          double e2[GS];
+          uint32_t hs[GS];
 #pragma unroll
-          for (int st = 0; st < NV / 2; ++st) {
-            ha |= static_cast<uint32_t>(in.any_energy2(ip, ctx_bound(H, __dadd_rn(e2a, ip.gu[2 * st])),
-                                                       ctx_bound(H, __dadd_rn(e2a, ip.gu[2 * st + 1]))))
-                  << st;
-            hb |= static_cast<uint32_t>(in.any_energy2(ip, ctx_bound(H, __dadd_rn(e2b, ip.gu[2 * st])),
-                                                       ctx_bound(H, __dadd_rn(e2b, ip.gu[2 * st + 1]))))
-                  << st;
+          for (int g = 0; g < GS; ++g) {
+            e2[g] = __dadd_rn(ea, H.ga[off + o + g]);
+            hs[g] = 0;
           }
-          LOOM_COUNT(3, NV);
-          LOOM_COUNT(0, __popc(ha) + __popc(hb));
-          if (__builtin_expect(ha != 0, 0)) {
-            H.od[J] = o;
-            const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o);
-            level<K, PRIM, NV, PT, J + 1>(H, in, ip, e2a, INT_MAX, lex + H.lexw[off + o], 0, NV, ib, ha);
-          }
-          if (__builtin_expect(hb != 0, 0)) {
-            H.od[J] = o + 1;
-            const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o + 1);
-            level<K, PRIM, NV, PT, J + 1>(H, in, ip, e2b, INT_MAX, lex + H.lexw[off + o + 1], 0, NV, ib, hb);
+#pragma unroll
+          for (int st = 0; st < NV / 2; ++st)
+#pragma unroll
+            for (int g = 0; g < GS; ++g)
+              hs[g] |= static_cast<uint32_t>(in.any_energy2(ip, ctx_bound(H, __dadd_rn(e2[g], ip.gu[2 * st])),
+                                                           ctx_bound(H, __dadd_rn(e2[g], ip.gu[2 * st + 1]))))
+                       << st;
+          LOOM_COUNT(3, GS * NV / 2);
+#pragma unroll
+          for (int g = 0; g < GS; ++g) {
+            LOOM_COUNT(0, __popc(hs[g]));
+            if (__builtin_expect(hs[g] != 0, 0)) {
+              H.od[J] = o + g;
+              const uint64_t ib = J == 0 ? 0 : ibase * static_cast<uint64_t>(n) + static_cast<uint64_t>(o + g);
+              level<K, PRIM, NV, PT, J + 1>(H, in, ip, e2[g], INT_MAX, lex + H.lexw[off + o + g], 0, NV, ib, hs[g]);
+            }
           }
           if (LOOM_SWEEP_SYNC) {
             if (H.sync_mask == 0xffffffffu) __syncwarp();
