@@ -322,3 +322,88 @@ def test_energy_first_under_binding_slos_vs_oracle(ctx, seed):
                 continue
             got = loom.search_argmin(ctx, lw.problem, loom.objective(obj), b, e)
             _check_oracle(got, ref)
+
+
+def _subset_problem(lw, keep: dict):
+    """A copy of a lowered problem keeping only the listed options of some
+    nodes ({node: [option, ...]}); other nodes keep all theirs."""
+    import ctypes as C
+    pr = lw.problem
+    n = pr.n_nodes
+    keep_all = []
+    off = 0
+    radix = []
+    for i in range(n):
+        opts = keep.get(i, list(range(pr.radix[i])))
+        keep_all += [off + o for o in opts]
+        radix.append(len(opts))
+        off += pr.radix[i]
+    held = []
+
+    def arr(ct, vals):
+        a = (ct * max(1, len(vals)))(*vals)
+        held.append(a)
+        return C.cast(a, C.POINTER(ct))
+
+    q = loom.Problem()
+    q.n_nodes, q.n_edges = n, pr.n_edges
+    q.radix = arr(C.c_int32, radix)
+    for f, ct in (("wall_us", C.c_int64), ("gpu_wh", C.c_double), ("cpu_wh", C.c_double),
+                  ("dollars", C.c_double), ("quality", C.c_int32)):
+        setattr(q, f, arr(ct, [getattr(pr, f)[k] for k in keep_all]))
+    # identifier ranks re-ranked within each node (order preserved)
+    lex = []
+    off = 0
+    for i in range(n):
+        opts = keep.get(i, list(range(pr.radix[i])))
+        ranks = [pr.lexrank[off + o] for o in opts]
+        order = sorted(range(len(opts)), key=lambda k: ranks[k])
+        rr = [0] * len(opts)
+        for r, k in enumerate(order):
+            rr[k] = r
+        lex += rr
+        off += pr.radix[i]
+    q.lexrank = arr(C.c_int32, lex)
+    # mixed-radix identifier weights in sorted node-id order, recomputed for the new radices
+    w = [0] * n
+    order = sorted(range(n), key=lambda i: pr.lex_weight[i])  # ascending weight = least significant first
+    acc = 1
+    for i in order:
+        w[i] = acc
+        acc *= radix[i]
+    q.lex_weight = arr(C.c_uint64, w)
+    q.edge_from = arr(C.c_int32, [pr.edge_from[e] for e in range(pr.n_edges)])
+    q.edge_to = arr(C.c_int32, [pr.edge_to[e] for e in range(pr.n_edges)])
+    q._held = held
+    return q
+
+
+@pytest.mark.parametrize("keep", [{7: list(range(15))}, {8: list(range(12))}, {7: [0, 3, 5], 9: list(range(11))}])
+def test_sweep_shapes_hierarchical_equals_full_eval(ctx, keep):
+    """C3 with some suffix nodes cut to odd / narrower radices, so the sweep
+    takes its unpaired and non-unrolled forms: the hierarchical search equals
+    the one-plan-per-thread re-evaluation on 2^24-plan slices."""
+    w = W.config3()
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    q = _subset_problem(lw, keep)
+    obj = loom.objective(w.objective)
+    total = C_total(q)
+    rng = random.Random(11)
+    for _ in range(4):
+        b = rng.randrange(total - (1 << 24))
+        res = []
+        for algo in (0, 1):
+            try:
+                res.append(loom.search_argmin(ctx, q, obj, b, b + (1 << 24), algo))
+            except loom.NoFeasibleConfigError:
+                res.append(None)
+        assert res[0] == res[1]
+    full = [loom.search_argmin(ctx, q, loom.objective("MIN_COST"), 0, 1 << 24, a) for a in (0, 1)]
+    assert full[0] == full[1]
+
+
+def C_total(q) -> int:
+    import ctypes as C
+    t = C.c_uint64()
+    assert loom.lib().loom_problem_total(C.byref(q), C.byref(t)) == 0
+    return t.value
