@@ -322,7 +322,9 @@ def b200_arm(args) -> None:
                          "note": "peak = SMs x 4 SMSPs x 32 lanes x measured SM clock / SMSP cycles per plan of "
                                  f"the compiled fast path ({fp['issue']} instructions, {fp['alu']} ALU-pipe, "
                                  f"{fp['fp64']} FP64-pipe per {fp['plans_per_lane']} plans per lane; both pipes take "
-                                 "2 cycles per warp instruction); traffic = DRAM bytes per launch (ncu)"},
+                                 "2 cycles per warp instruction); traffic = DRAM bytes per launch (ncu): the 7 KB problem image plus "
+                                 "local-memory spills of loop state at the 80-register cap -- the search has no "
+                                 "data stream"},
             "gpu_launches": launches,
             "clocks": clk,
         }
