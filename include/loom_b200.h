@@ -175,8 +175,19 @@ uint64_t loom_ctx_launch_count(const loom_ctx* ctx);
 int loom_search_argmin(loom_ctx* ctx, const loom_problem* problem, const loom_objective* objective,
                        uint64_t begin, uint64_t end, loom_winner* out);
 
-/* Same, selecting the evaluation algorithm: 0 = hierarchical (default),
- * 1 = one-plan-per-thread full re-evaluation (independent cross-check). */
+/* Same, selecting the evaluation algorithm:
+ *   LOOM_ALGO_AUTO  (default) branch and bound over the ConfigEnumerator tree
+ *                   -- subtrees whose criteria lower bound is infeasible or
+ *                   strictly worse than a plan already found are dropped --
+ *                   with the exhaustive sweep as its fallback when the bound
+ *                   prunes too little;
+ *   LOOM_ALGO_FULL  one plan per thread, re-evaluated from scratch
+ *                   (independent cross-check);
+ *   LOOM_ALGO_SWEEP the hierarchical sweep alone: every plan of the range is
+ *                   tested in the fast path. */
+#define LOOM_ALGO_AUTO 0
+#define LOOM_ALGO_FULL 1
+#define LOOM_ALGO_SWEEP 2
 int loom_search_argmin_algo(loom_ctx* ctx, const loom_problem* problem,
                             const loom_objective* objective, uint64_t begin, uint64_t end,
                             int32_t algo, loom_winner* out);
@@ -222,6 +233,16 @@ int loom_search_argmin_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t be
 /* loom_search_argmin_shard on a resident problem, enqueued without synchronising. */
 int loom_search_argmin_shard_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t begin, uint64_t end,
                                    uint64_t incumbent);
+/* loom_search_argmin_async with a chosen LOOM_ALGO_* and incumbent
+ * (LOOM_NO_INCUMBENT, LOOM_INCUMBENT_GREEDY or a plan index). */
+#define LOOM_NO_INCUMBENT (UINT64_MAX - 1)
+int loom_search_argmin_algo_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t begin, uint64_t end,
+                                  uint64_t incumbent, int32_t algo);
+/* Evidence of the last branch-and-bound launch (its job 0): out[0] = child
+ * evaluations (subtree bounds + leaves), out[1] = 1 if it exhausted its
+ * budget and the sweep finished the search, out[2] = DFS steps of the longest
+ * work unit, out[3] = work units that survived their root bound (4 entries). */
+int loom_bnb_last_stats(uint64_t* out);
 /* Wait for the last enqueued search of dp and decode its result. */
 int loom_search_argmin_result(loom_ctx* ctx, loom_device_problem* dp, loom_winner* out);
 

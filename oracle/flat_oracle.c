@@ -362,3 +362,285 @@ int oracle_pareto(const or_problem* p, uint64_t begin, uint64_t end, int threads
   free(c);
   return 0;
 }
+
+/* ---- exact branch-and-bound argmin over the WHOLE plan space --------------
+ *
+ * For plan spaces the flat loop cannot finish (C3: 1.1e12 plans).  A DFS over
+ * the nodes in enumeration order; every subtree (the first i digits fixed) is
+ * bounded by a componentwise lower bound of its plans' criteria:
+ *   energy / dollars  the dag-order left fold with every free node at its
+ *                     minimum (FP addition rounds monotonically, so the fold is
+ *                     monotone in every term; llround is monotone too),
+ *   latency           the finish-time recursion with free nodes at their
+ *                     minimum wall (max-plus is monotone),
+ *   quality           min(prefix quality, max over free nodes) (upper bound).
+ * A subtree is dropped when its bound is infeasible (latency > SLO) or
+ * lexicographically STRICTLY worse than the incumbent under the criteria
+ * list: then every plan in it is strictly worse on some criterion with all
+ * earlier ones equal or worse, so none can be the argmin.  Ties on every
+ * criterion are never pruned (the identifier decides).  Options failing the
+ * quality floor are never taken (a plan's quality is the min over nodes).
+ * Leaves are evaluated with evaluate() + feasible() + objective_less() above,
+ * so the result is the restated reference argmin.  Threads take top-level
+ * subtrees from a shared counter and share the incumbent through a mutex;
+ * the order is strict and total, so the answer does not depend on timing. */
+
+typedef struct {
+  const or_ctx* c;
+  const or_objective* o;
+  int n;
+  int topo_pos[OR_MAX_NODES];
+  double min_gpu[OR_MAX_NODES], min_dol[OR_MAX_NODES];
+  int64_t min_wall[OR_MAX_NODES];
+  int max_q[OR_MAX_NODES];
+  int n_ok[OR_MAX_NODES];
+  int* order; /* per node: allowed options in exploration order (node-major, off[]) */
+  int split;  /* nodes fixed per top-level task */
+  uint64_t n_tasks;
+  uint64_t next_task;
+  pthread_mutex_t mu;
+  or_estimate best;
+  int bd[OR_MAX_NODES];
+  uint64_t visited;
+} bnb_shared;
+
+typedef struct {
+  bnb_shared* s;
+  or_estimate best;
+  int bd[OR_MAX_NODES];
+  int d[OR_MAX_NODES];
+  double fg[OR_MAX_NODES + 1], fd[OR_MAX_NODES + 1]; /* prefix folds */
+  int fq[OR_MAX_NODES + 1];
+  uint64_t visited;
+} bnb_worker;
+
+static int opt_passes_floor(const bnb_shared* s, int o) {
+  return !s->o->has_floor || s->c->p->quality[o] >= s->o->floor;
+}
+
+/* Lower bound of every plan whose first `depth` digits are w->d[0..depth). */
+static void bnb_bound(const bnb_worker* w, int depth, or_estimate* lb) {
+  const bnb_shared* s = w->s;
+  const or_problem* p = s->c->p;
+  double g = w->fg[depth], dl = w->fd[depth];
+  int q = w->fq[depth];
+  for (int i = depth; i < s->n; ++i) {
+    g += s->min_gpu[i];
+    dl += s->min_dol[i];
+    if (s->max_q[i] < q) q = s->max_q[i];
+  }
+  int64_t fin[OR_MAX_NODES];
+  int64_t lat = 0;
+  for (int t = 0; t < s->n; ++t) {
+    const int v = p->topo[t];
+    int64_t st = 0;
+    for (int k = 0; k < s->c->npred[v]; ++k)
+      if (fin[s->c->pred[v][k]] > st) st = fin[s->c->pred[v][k]];
+    fin[v] = st + (v < depth ? p->wall[s->c->off[v] + w->d[v]] : s->min_wall[v]);
+    if (fin[v] > lat) lat = fin[v];
+  }
+  lb->latency_us = lat;
+  lb->gpu_wh = g;
+  lb->dollars = dl;
+  lb->quality = s->n == 0 ? 0 : q;
+}
+
+/* 1 iff every plan bounded by lb is infeasible or strictly worse than best. */
+static int bnb_prune(const bnb_shared* s, const or_estimate* lb, const or_estimate* best) {
+  const or_objective* o = s->o;
+  if (o->has_slo && lb->latency_us > o->slo) return 1;
+  if (o->has_floor && lb->quality < o->floor) return 1;
+  if (!best->found) return 0;
+  for (int i = 0; i < o->n_criteria; ++i) {
+    int64_t a, b;
+    switch (o->criteria[i]) {
+      case 0: a = quantize(lb->dollars); b = quantize(best->dollars); break;
+      case 1: a = quantize(lb->gpu_wh); b = quantize(best->gpu_wh); break;
+      case 2: a = lb->latency_us; b = best->latency_us; break;
+      default: a = -(int64_t)lb->quality; b = -(int64_t)best->quality; break;
+    }
+    if (a > b) return 1;
+    if (a < b) return 0;
+  }
+  return 0;
+}
+
+static void bnb_offer(bnb_worker* w, const or_estimate* e, const int* d) {
+  const bnb_shared* s = w->s;
+  if (!feasible(s->o, e)) return;
+  if (w->best.found && !objective_less(s->c, s->o, e, d, &w->best, w->bd)) return;
+  w->best = *e;
+  memcpy(w->bd, d, sizeof(int) * (size_t)s->n);
+}
+
+static void bnb_dfs(bnb_worker* w, int depth) {
+  const bnb_shared* s = w->s;
+  const or_problem* p = s->c->p;
+  const int off = s->c->off[depth];
+  for (int k = 0; k < s->n_ok[depth]; ++k) {
+    const int opt = s->order[off + k];
+    const int o = off + opt;
+    w->d[depth] = opt;
+    const double pc = (double)p->path_count[o];
+    w->fg[depth + 1] = w->fg[depth] + p->gpu[o] * pc;
+    w->fd[depth + 1] = w->fd[depth] + p->dol[o] * pc;
+    w->fq[depth + 1] = p->quality[o] < w->fq[depth] ? p->quality[o] : w->fq[depth];
+    ++w->visited;
+    if (depth + 1 == s->n) {
+      or_estimate e;
+      evaluate(s->c, w->d, &e);
+      uint64_t idx = 0;
+      for (int i = 0; i < s->n; ++i) idx = idx * (uint64_t)p->radix[i] + (uint64_t)w->d[i];
+      e.index = idx;
+      bnb_offer(w, &e, w->d);
+      continue;
+    }
+    or_estimate lb;
+    bnb_bound(w, depth + 1, &lb);
+    if (bnb_prune(s, &lb, &w->best)) continue;
+    bnb_dfs(w, depth + 1);
+  }
+}
+
+static void* bnb_thread(void* arg) {
+  bnb_worker* w = (bnb_worker*)arg;
+  bnb_shared* s = w->s;
+  const or_problem* p = s->c->p;
+  for (;;) {
+    pthread_mutex_lock(&s->mu);
+    const uint64_t t = s->next_task++;
+    if (s->best.found && (!w->best.found || objective_less(s->c, s->o, &s->best, s->bd, &w->best, w->bd))) {
+      w->best = s->best;
+      memcpy(w->bd, s->bd, sizeof(int) * (size_t)s->n);
+    }
+    pthread_mutex_unlock(&s->mu);
+    if (t >= s->n_tasks) break;
+    /* task t: the split top nodes take the t-th combination of their allowed options */
+    uint64_t x = t;
+    int ok = 1;
+    w->fg[0] = 0.0;
+    w->fd[0] = 0.0;
+    w->fq[0] = INT32_MAX;
+    int rank[OR_MAX_NODES];
+    for (int i = s->split - 1; i >= 0; --i) {
+      rank[i] = (int)(x % (uint64_t)s->n_ok[i]);
+      x /= (uint64_t)s->n_ok[i];
+    }
+    for (int i = 0; i < s->split; ++i) {
+      const int opt = s->order[s->c->off[i] + rank[i]];
+      const int o = s->c->off[i] + opt;
+      w->d[i] = opt;
+      const double pc = (double)p->path_count[o];
+      w->fg[i + 1] = w->fg[i] + p->gpu[o] * pc;
+      w->fd[i + 1] = w->fd[i] + p->dol[o] * pc;
+      w->fq[i + 1] = p->quality[o] < w->fq[i] ? p->quality[o] : w->fq[i];
+    }
+    if (s->split == s->n) {
+      or_estimate e;
+      evaluate(s->c, w->d, &e);
+      uint64_t idx = 0;
+      for (int i = 0; i < s->n; ++i) idx = idx * (uint64_t)p->radix[i] + (uint64_t)w->d[i];
+      e.index = idx;
+      bnb_offer(w, &e, w->d);
+    } else {
+      or_estimate lb;
+      bnb_bound(w, s->split, &lb);
+      if (!bnb_prune(s, &lb, &w->best)) bnb_dfs(w, s->split);
+    }
+    (void)ok;
+    pthread_mutex_lock(&s->mu);
+    if (w->best.found && (!s->best.found || objective_less(s->c, s->o, &w->best, w->bd, &s->best, s->bd))) {
+      s->best = w->best;
+      memcpy(s->bd, w->bd, sizeof(int) * (size_t)s->n);
+    }
+    pthread_mutex_unlock(&s->mu);
+  }
+  return NULL;
+}
+
+static const bnb_shared* g_sort_s;
+static int g_sort_node;
+static int bnb_cmp(const void* a, const void* b) {
+  /* exploration order: the primary criterion's own value, then the option index */
+  const bnb_shared* s = g_sort_s;
+  const or_problem* p = s->c->p;
+  const int oa = s->c->off[g_sort_node] + *(const int*)a, ob = s->c->off[g_sort_node] + *(const int*)b;
+  double va = 0, vb = 0;
+  const int prim = s->o->n_criteria ? s->o->criteria[0] : 2;
+  switch (prim) {
+    case 0: va = p->dol[oa] * p->path_count[oa]; vb = p->dol[ob] * p->path_count[ob]; break;
+    case 1: va = p->gpu[oa] * p->path_count[oa]; vb = p->gpu[ob] * p->path_count[ob]; break;
+    case 2: va = (double)p->wall[oa]; vb = (double)p->wall[ob]; break;
+    default: va = -(double)p->quality[oa]; vb = -(double)p->quality[ob]; break;
+  }
+  if (va != vb) return va < vb ? -1 : 1;
+  return oa < ob ? -1 : oa > ob;
+}
+
+/* Exact argmin over the whole space; *visited = subtrees + leaves expanded. */
+int oracle_argmin_bnb(const or_problem* p, const or_objective* o, int threads, or_estimate* out,
+                      uint64_t* visited) {
+  or_ctx* c = (or_ctx*)malloc(sizeof(or_ctx));
+  if (!c || ctx_init(c, p)) {
+    free(c);
+    return -1;
+  }
+  if (threads < 1) threads = 1;
+  bnb_shared* s = (bnb_shared*)calloc(1, sizeof(bnb_shared));
+  s->c = c;
+  s->o = o;
+  s->n = p->n_nodes;
+  s->order = (int*)malloc(sizeof(int) * (size_t)(c->off[p->n_nodes] + 1));
+  memset(out, 0, sizeof *out);
+  int empty = p->n_nodes == 0;
+  for (int i = 0; i < p->n_nodes; ++i) {
+    int k = 0;
+    s->min_gpu[i] = INFINITY;
+    s->min_dol[i] = INFINITY;
+    s->min_wall[i] = INT64_MAX;
+    s->max_q[i] = INT32_MIN;
+    for (int j = 0; j < p->radix[i]; ++j) {
+      const int oi = c->off[i] + j;
+      if (!opt_passes_floor(s, oi)) continue;
+      s->order[c->off[i] + k++] = j;
+      const double pc = (double)p->path_count[oi];
+      if (p->gpu[oi] * pc < s->min_gpu[i]) s->min_gpu[i] = p->gpu[oi] * pc;
+      if (p->dol[oi] * pc < s->min_dol[i]) s->min_dol[i] = p->dol[oi] * pc;
+      if (p->wall[oi] < s->min_wall[i]) s->min_wall[i] = p->wall[oi];
+      if (p->quality[oi] > s->max_q[i]) s->max_q[i] = p->quality[oi];
+    }
+    s->n_ok[i] = k;
+    if (k == 0) empty = 1;
+    g_sort_s = s;
+    g_sort_node = i;
+    qsort(s->order + c->off[i], (size_t)k, sizeof(int), bnb_cmp);
+  }
+  if (!empty) {
+    s->split = 0;
+    s->n_tasks = 1;
+    while (s->split < p->n_nodes && s->n_tasks < 64u * (uint64_t)threads) s->n_tasks *= (uint64_t)s->n_ok[s->split++];
+    pthread_mutex_init(&s->mu, NULL);
+    bnb_worker* w = (bnb_worker*)calloc((size_t)threads, sizeof(bnb_worker));
+    pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 0; t < threads; ++t) {
+      w[t].s = s;
+      pthread_create(&tid[t], NULL, bnb_thread, &w[t]);
+    }
+    uint64_t vis = 0;
+    for (int t = 0; t < threads; ++t) {
+      pthread_join(tid[t], NULL);
+      vis += w[t].visited;
+    }
+    if (visited) *visited = vis;
+    if (s->best.found) *out = s->best;
+    pthread_mutex_destroy(&s->mu);
+    free(w);
+    free(tid);
+  } else if (visited) {
+    *visited = 0;
+  }
+  free(s->order);
+  free(s);
+  free(c);
+  return 0;
+}

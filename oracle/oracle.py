@@ -62,6 +62,8 @@ def _lib():
         _flat.oracle_argmin.argtypes = [C.POINTER(OrProblem), C.POINTER(OrObjective), C.c_uint64, C.c_uint64,
                                         C.c_int, C.POINTER(OrEstimate)]
         _flat.oracle_estimates.argtypes = [C.POINTER(OrProblem), C.c_uint64, C.c_uint64, C.POINTER(OrEstimate)]
+        _flat.oracle_argmin_bnb.argtypes = [C.POINTER(OrProblem), C.POINTER(OrObjective), C.c_int,
+                                            C.POINTER(OrEstimate), C.POINTER(C.c_uint64)]
         _flat.oracle_pareto.argtypes = [C.POINTER(OrProblem), C.c_uint64, C.c_uint64, C.c_int,
                                         C.POINTER(OrEstimate), C.c_uint64, C.POINTER(C.c_uint64)]
     return _flat
@@ -129,6 +131,19 @@ def argmin(p: OracleProblem, objective: dict, begin: int = 0, end: int | None = 
     if rc != 0:
         raise RuntimeError("oracle_argmin failed")
     return out.as_dict() if out.found else None
+
+
+def argmin_bnb(p: OracleProblem, objective: dict, threads: int | None = None) -> tuple[dict | None, int]:
+    """Exact argmin over the WHOLE space by branch and bound (flat_oracle.c:
+    oracle_argmin_bnb); returns (winner or None, subtrees + leaves visited)."""
+    threads = threads or os.cpu_count() or 1
+    out = OrEstimate()
+    vis = C.c_uint64(0)
+    o = objective_struct(objective)
+    rc = _lib().oracle_argmin_bnb(C.byref(p.struct), C.byref(o), threads, C.byref(out), C.byref(vis))
+    if rc != 0:
+        raise RuntimeError("oracle_argmin_bnb failed")
+    return (out.as_dict() if out.found else None), vis.value
 
 
 def estimates(p: OracleProblem, begin: int, end: int) -> list[dict]:

@@ -32,6 +32,8 @@ struct loom_ctx {
   size_t tickets_cap = 0;
   loomk::Rec* d_out = nullptr;
   size_t out_cap = 0;
+  loomk::BnbSync* d_bsync = nullptr;  // branch-and-bound per-job state (zero between launches)
+  size_t bsync_cap = 0;
   loomk::Rec* h_out = nullptr;  // pinned
   size_t h_out_cap = 0;
   uint8_t* h_arena = nullptr;  // pinned staging of batch problem images

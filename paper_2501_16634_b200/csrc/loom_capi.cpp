@@ -52,6 +52,16 @@ int check_problem(const loom_problem* p, uint64_t* total) {
   if (n_opts && (!p->wall_us || !p->gpu_wh || !p->cpu_wh || !p->dollars || !p->quality || !p->lexrank))
     return fail(LOOM_INVALID, "InvalidConfigError: null option table");
   if (!p->lex_weight) return fail(LOOM_INVALID, "InvalidConfigError: null lex_weight");
+  // The reference's library rejects negative watts, rates and throughputs, so
+  // lowered values are finite and >= 0; the kernels' bounds rely on it (raw
+  // C-ABI callers are held to the same contract).
+  for (int64_t k = 0; k < n_opts; ++k) {
+    const double v[3] = {p->gpu_wh[k], p->cpu_wh[k], p->dollars[k]};
+    for (double x : v)
+      if (!(x >= 0.0) || x == HUGE_VAL)
+        return fail(LOOM_INVALID, "InvalidConfigError: option energy / dollars must be finite and >= 0");
+    if (p->wall_us[k] < 0) return fail(LOOM_INVALID, "InvalidConfigError: negative wall");
+  }
   if (p->n_edges && (!p->edge_from || !p->edge_to)) return fail(LOOM_INVALID, "InvalidConfigError: null edges");
   for (int e = 0; e < p->n_edges; ++e)
     if (p->edge_from[e] < 0 || p->edge_from[e] >= p->n_nodes || p->edge_to[e] < 0 || p->edge_to[e] >= p->n_nodes)

@@ -64,6 +64,8 @@ using loomi::cuda_fail;
 namespace {
 
 constexpr int64_t kNeg = -(int64_t(1) << 62);
+constexpr unsigned kBnbDone = 1;     // JobSync.pad after a branch-and-bound launch (bnb.cuh)
+constexpr unsigned kBnbAborted = 2;
 
 #ifndef LOOM_PAIR_UNROLL
 #define LOOM_PAIR_UNROLL 4
@@ -1116,6 +1118,17 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
 
   const int job = blockIdx.x / ctas_per_job;
   const int part = blockIdx.x % ctas_per_job;
+  // After a branch-and-bound launch (bnb.cuh) on the same job: kBnbDone ->
+  // its result stands and this launch only retires; kBnbAborted -> search
+  // exhaustively, starting from its best plan.
+  const unsigned bnb_state = __ldcg(&sync[job].pad);
+  if (bnb_state == kBnbDone) {
+    if (threadIdx.x == 0 && atomicAdd(&sync[job].ticket, 1u) == static_cast<unsigned>(ctas_per_job - 1)) {
+      sync[job].ticket = 0;
+      sync[job].pad = 0;
+    }
+    return;
+  }
   const JobDesc jd = jobs[job];
   if (threadIdx.x == 0) s_gbest = LOOM_JOB_BOUND ? &sync[job].best_neg : nullptr;
   load_blob(smem, arena + jd.blob_off, jd.blob_bytes, &mbar);  // (its __syncthreads publishes s_gbest)
@@ -1129,6 +1142,7 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
     full_eval(v, jd.seed, c);
     slot_offer(sl, threadIdx.x, h, c);
   }
+  if (bnb_state == kBnbAborted) slot_offer(sl, threadIdx.x, h, load_rec_cg(&out[job]));
 
   const uint64_t gt = static_cast<uint64_t>(part) * kBlock + threadIdx.x;
   const uint64_t nt = static_cast<uint64_t>(ctas_per_job) * kBlock;
@@ -1224,6 +1238,7 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
     if (threadIdx.x == 0) {
       out[job] = acc;
       sync[job].ticket = 0;
+      sync[job].pad = 0;
       sync[job].next_group = 0;
       sync[job].best_neg = 0;
     }
@@ -1231,6 +1246,9 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
 }
 
 using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, JobSync*, Rec*, InnerParams);
+
+#include "bnb.cuh"
+
 
 // pt: the innermost table comes from the kernel parameter (single-problem
 // launches); batch launches read it per job from shared memory.
@@ -1896,6 +1914,32 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   const int inner_pad = std::max(nv, (inner_radix + 7) & ~7);
   hd.off_inner = take(static_cast<int>(sizeof(InnerEntry)) * inner_pad);
   hd.off_w32 = take(4 * n_opts);
+  hd.off_perm = take(4 * n_opts);
+  hd.off_nok = take(4 * n);
+  hd.off_bmin = take(static_cast<int>(sizeof(BnbMin)) * n);
+  hd.off_rk = take(8 * (n + 1));
+  // settled-node lists (bnb.cuh): anc[x] = x and its ancestors
+  std::vector<std::vector<int32_t>> uns(n), nset(n);
+  {
+    std::vector<uint64_t> anc(n, 0);  // n <= 32 nodes: bit sets
+    for (int x : topo) {
+      anc[x] |= uint64_t(1) << x;
+      for (int e = predoff[x]; e < predoff[x + 1]; ++e) anc[x] |= anc[pred[e]];
+    }
+    auto settled = [&](int x, int k) { return (anc[x] >> k) == 0; };  // every ancestor-or-self < k
+    for (int k = 0; k < n; ++k)
+      for (int x : topo) {
+        if (!settled(x, k)) uns[k].push_back(x);
+        if (settled(x, k + 1) && !settled(x, k)) nset[k].push_back(x);
+      }
+  }
+  auto csr_bytes = [&](const std::vector<std::vector<int32_t>>& v) {
+    std::size_t m = n + 1;
+    for (auto& x : v) m += x.size();
+    return static_cast<int>(4 * m);
+  };
+  hd.off_uns = take(csr_bytes(uns));
+  hd.off_nsettle = take(csr_bytes(nset));
   if (off > kMaxBlobBytes) return loomi::fail(LOOM_INVALID, "InvalidConfigError: problem image exceeds shared memory");
   hd.n_nodes = n;
   hd.n_edges = p->n_edges;
@@ -1965,6 +2009,53 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
       lexw[k] = static_cast<uint64_t>(p->lexrank[k]) * p->lex_weight[i];
       qq[k] = p->quality[k];
       w32[k] = floor_ok(k) ? static_cast<int32_t>(std::min<int64_t>(p->wall_us[k], int64_t(1) << 30)) : (1 << 30);
+    }
+  }
+  {  // branch-and-bound tables (bnb.cuh)
+    int32_t* perm = reinterpret_cast<int32_t*>(base + hd.off_perm);
+    int32_t* nok = reinterpret_cast<int32_t*>(base + hd.off_nok);
+    BnbMin* bm = reinterpret_cast<BnbMin*>(base + hd.off_bmin);
+    uint64_t* rk = reinterpret_cast<uint64_t*>(base + hd.off_rk);
+    rk[n] = 1;
+    for (int i = n - 1; i >= 0; --i) rk[i] = rk[i + 1] * static_cast<uint64_t>(p->radix[i]);
+    auto put_csr = [&](int at, const std::vector<std::vector<int32_t>>& v) {
+      int32_t* o = reinterpret_cast<int32_t*>(base + at);
+      int32_t m = n + 1;
+      for (int k = 0; k < n; ++k) {
+        o[k] = m;
+        for (int32_t x : v[k]) o[m++] = x;
+      }
+      o[n] = m;
+    };
+    put_csr(hd.off_uns, uns);
+    put_csr(hd.off_nsettle, nset);
+    for (int i = 0; i < n; ++i) {
+      std::vector<int32_t> ord;
+      BnbMin m{INFINITY, INFINITY, INT64_MAX, UINT64_MAX, INT_MIN, {0, 0, 0}};
+      for (int k = optoff[i]; k < optoff[i + 1]; ++k) {
+        if (!floor_ok(k)) continue;
+        ord.push_back(k - optoff[i]);
+        m.a = std::min(m.a, ga[k]);
+        m.b = std::min(m.b, gb[k]);
+        m.w = std::min(m.w, wall[k]);
+        m.lex = std::min(m.lex, lexw[k]);
+        m.q = std::max(m.q, qq[k]);
+      }
+      // exploration order: best on the primary criterion first (ties: index)
+      auto key = [&](int32_t j) -> double {
+        const int k = optoff[i] + j;
+        if (o->n_criteria == 0) return static_cast<double>(lexw[k]);
+        switch (crit[0]) {
+          case kFpA: return ga[k];
+          case kFpB: return gb[k];
+          case kLat: return static_cast<double>(wall[k]);
+          default: return -static_cast<double>(qq[k]);
+        }
+      };
+      std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return key(x) < key(y); });
+      for (std::size_t j = 0; j < ord.size(); ++j) perm[optoff[i] + j] = ord[j];
+      nok[i] = static_cast<int32_t>(ord.size());
+      bm[i] = m;
     }
   }
   InnerEntry* inner = reinterpret_cast<InnerEntry*>(base + hd.off_inner);
@@ -2071,6 +2162,13 @@ void range_seed(const loom_problem* p, const loom_objective* o, const Built& b, 
   }
 }
 
+// Search algorithms (loom_search_argmin_algo): branch and bound with the
+// sweep as its fallback (default), one plan per thread re-evaluated from
+// scratch (cross-check), the hierarchical sweep alone (every plan tested).
+constexpr int kAlgoAuto = 0;
+constexpr int kAlgoFull = 1;
+constexpr int kAlgoSweep = 2;
+
 // incumbent: kNoIncumbent (a plain range search: the start is range_seed's
 // in-range plan), LOOM_INCUMBENT_GREEDY (the greedy seed, wherever it lies)
 // or a plan index of the space.  An out-of-range incumbent takes part in the
@@ -2139,6 +2237,8 @@ struct loom_device_problem {
   int ctas = 0;
   KernelFn fn = nullptr;
   cudaEvent_t done = nullptr;
+  BnbSync* d_bsync = nullptr;
+  int bnb_ctas = 0;  // 0: the image does not fit the branch-and-bound kernel
 };
 
 namespace {
@@ -2164,6 +2264,36 @@ int ensure_tickets(loom_ctx* c, size_t need) {
   LOOM_CUDA(cudaMemset(c->d_tickets, 0, std::max<size_t>(need, 1) * sizeof(JobSync)));
   c->tickets_cap = need;
   return LOOM_OK;
+}
+
+int ensure_bsync(loom_ctx* c, size_t need) {
+  if (need <= c->bsync_cap && c->d_bsync) return LOOM_OK;
+  if (c->d_bsync) cudaFree(c->d_bsync);
+  c->d_bsync = nullptr;
+  c->bsync_cap = 0;
+  LOOM_CUDA(cudaMalloc(&c->d_bsync, std::max<size_t>(need, 1) * sizeof(BnbSync)));
+  LOOM_CUDA(cudaMemset(c->d_bsync, 0, std::max<size_t>(need, 1) * sizeof(BnbSync)));
+  c->bsync_cap = need;
+  return LOOM_OK;
+}
+
+// CTAs of one full wave of the branch-and-bound kernel at this image size
+// (0 when its shared memory does not fit: the sweep alone then searches).
+int bnb_ctas_for(const loom_ctx* c, size_t blob, int n) {
+  const size_t smem = bnb_smem_bytes(blob, n);
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(bnb_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(bnb_kernel), kBlock, smem) !=
+          cudaSuccess ||
+      nb < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c->sms * nb;
 }
 
 int ensure_host(loom_ctx* c, size_t need) {
@@ -2318,6 +2448,7 @@ int loom_ctx_destroy(loom_ctx* c) {
   cudaFree(c->d_jobs);
   cudaFree(c->d_scratch);
   cudaFree(c->d_tickets);
+  cudaFree(c->d_bsync);
   cudaFree(c->d_out);
   for (void* q : c->pool_all) cudaFree(q);
   if (c->h_out) cudaFreeHost(c->h_out);
@@ -2332,7 +2463,8 @@ uint64_t loom_ctx_launch_count(const loom_ctx* c) { return c ? c->launches : 0; 
 namespace {
 int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin, uint64_t end,
                        int32_t algo, uint64_t incumbent, loom_winner* out);
-int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end, uint64_t incumbent);
+int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end, uint64_t incumbent,
+                      int32_t algo = kAlgoAuto);
 }  // namespace
 
 int loom_search_argmin_algo(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin,
@@ -2354,6 +2486,18 @@ int loom_search_argmin_shard_async(loom_ctx* c, loom_device_problem* dp, uint64_
   return search_async_impl(c, dp, begin, end, incumbent);
 }
 
+int loom_search_argmin_algo_async(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end,
+                                  uint64_t incumbent, int32_t algo) {
+  if (algo < kAlgoAuto || algo > kAlgoSweep) return loomi::fail(LOOM_INVALID, "InvalidConfigError: unknown algo");
+  return search_async_impl(c, dp, begin, end, incumbent == UINT64_MAX - 1 ? kNoIncumbent : incumbent, algo);
+}
+
+int loom_bnb_last_stats(uint64_t* out) {
+  if (!out) return LOOM_INVALID;
+  if (cudaMemcpyFromSymbol(out, g_bnb_last, sizeof(uint64_t) * 4) != cudaSuccess) return LOOM_DEVICE_ERROR;
+  return LOOM_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -2368,22 +2512,30 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   if (int rc = build_image(p, o, target, b)) return rc;
   if (b.total == 0)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
-  const JobDesc d = make_desc(b, begin, end, algo == 1, p, o, incumbent);
+  const JobDesc d = make_desc(b, begin, end, algo == kAlgoFull, p, o, incumbent);
   if (d.begin >= d.end)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
   KernelFn fn = pick_kernel(b.K, b.prim, b.nv, true);
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
   const int ctas = ctas_for(c, units, fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)));
+  const int bctas = algo == kAlgoAuto ? bnb_ctas_for(c, b.blob.size(), p->n_nodes) : 0;
   if (int rc = ensure(c->d_arena, c->arena_cap, b.blob.size())) return rc;
   if (int rc = ensure(c->d_jobs, c->jobs_cap, 1)) return rc;
-  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(ctas))) return rc;
+  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(std::max(ctas, bctas)))) return rc;
   if (int rc = ensure_tickets(c, 1)) return rc;
+  if (int rc = ensure_bsync(c, 1)) return rc;
   if (int rc = ensure(c->d_out, c->out_cap, 1)) return rc;
   if (int rc = ensure_host(c, 1)) return rc;
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  if (bctas) {
+    bnb_kernel<<<bctas, kBlock, bnb_smem_bytes(b.blob.size(), p->n_nodes), c->stream>>>(
+        c->d_arena, c->d_jobs, bctas, c->d_scratch, c->d_tickets, c->d_bsync, c->d_out);
+    LOOM_CUDA(cudaGetLastError());
+    ++c->launches;
+  }
   fn<<<ctas, kBlock, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)), c->stream>>>(c->d_arena, c->d_jobs, ctas, c->d_scratch,
                                                                    c->d_tickets, c->d_out, b.ip);
   LOOM_CUDA(cudaGetLastError());
@@ -2478,6 +2630,28 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
     }
   }
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, all.data(), all.size() * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
+  // Branch and bound over every job (one CTA per job, `all` order); each
+  // group's sweep launch below then retires the jobs it settled.
+  if (!all.empty()) {
+    size_t bsmem = 0;
+    int nmax = 0;
+    for (auto& g : groups)
+      for (int j : g.jobs) {
+        bsmem = std::max(bsmem, bnb_smem_bytes(built[j].blob.size(), problems[j].n_nodes));
+        nmax = std::max(nmax, problems[j].n_nodes);
+      }
+    if (int rc = ensure_bsync(c, all.size())) return rc;
+    if (cudaFuncSetAttribute(reinterpret_cast<const void*>(bnb_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bsmem)) == cudaSuccess) {
+      bnb_kernel<<<static_cast<int>(all.size()), kBlock, bsmem, c->stream>>>(c->d_arena, c->d_jobs, 1, c->d_scratch,
+                                                                          c->d_tickets, c->d_bsync, c->d_out);
+      LOOM_CUDA(cudaGetLastError());
+      ++c->launches;
+    } else {
+      cudaGetLastError();
+    }
+    (void)nmax;
+  }
   size_t first = 0;
   for (auto& g : groups) {
     if (int rc = set_smem(g.fn, g.smem)) return rc;
@@ -2548,9 +2722,12 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   }
   const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)));
   dp->ctas = ctas;
+  dp->bnb_ctas = dp->built.blob.empty() ? 0 : bnb_ctas_for(c, dp->built.blob.size(), dp->host.n_nodes);
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
-             cudaMalloc(&dp->d_scratch, sizeof(Rec) * ctas) == cudaSuccess &&
+             cudaMalloc(&dp->d_scratch, sizeof(Rec) * std::max(ctas, dp->bnb_ctas)) == cudaSuccess &&
+             cudaMalloc(&dp->d_bsync, sizeof(BnbSync)) == cudaSuccess &&
+             cudaMemset(dp->d_bsync, 0, sizeof(BnbSync)) == cudaSuccess &&
              cudaMalloc(&dp->d_ticket, sizeof(JobSync)) == cudaSuccess &&
              cudaMalloc(&dp->d_out, sizeof(Rec)) == cudaSuccess && cudaMallocHost(&dp->h_out, sizeof(Rec)) == cudaSuccess &&
              cudaEventCreateWithFlags(&dp->done, cudaEventDisableTiming) == cudaSuccess &&
@@ -2571,6 +2748,7 @@ int loom_problem_release(loom_device_problem* dp) {
   cudaFree(dp->d_job);
   cudaFree(dp->d_scratch);
   cudaFree(dp->d_ticket);
+  cudaFree(dp->d_bsync);
   cudaFree(dp->d_out);
   if (dp->h_out) cudaFreeHost(dp->h_out);
   if (dp->done) cudaEventDestroy(dp->done);
@@ -2586,14 +2764,21 @@ uint64_t loom_device_problem_bytes(const loom_device_problem* dp) {
 
 namespace {
 
-int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end, uint64_t incumbent) {
+int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end, uint64_t incumbent,
+                      int32_t algo) {
   if (!c || !dp) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
-  JobDesc d = make_desc(dp->built, begin, end, false, &dp->host, &dp->objective, incumbent);
+  JobDesc d = make_desc(dp->built, begin, end, algo == kAlgoFull, &dp->host, &dp->objective, incumbent);
   d.blob_off = 0;
   if (d.begin >= d.end) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: empty range");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
   const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built))));
   LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  if (algo == kAlgoAuto && dp->bnb_ctas) {
+    bnb_kernel<<<dp->bnb_ctas, kBlock, bnb_smem_bytes(dp->built.blob.size(), dp->host.n_nodes), c->stream>>>(
+        dp->d_blob, dp->d_job, dp->bnb_ctas, dp->d_scratch, dp->d_ticket, dp->d_bsync, dp->d_out);
+    LOOM_CUDA(cudaGetLastError());
+    ++c->launches;
+  }
   dp->fn<<<ctas, kBlock, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)), c->stream>>>(dp->d_blob, dp->d_job, ctas, dp->d_scratch,
                                                              dp->d_ticket, dp->d_out, dp->built.ip);
   LOOM_CUDA(cudaGetLastError());

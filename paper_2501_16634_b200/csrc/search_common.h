@@ -75,7 +75,34 @@ struct alignas(16) BlobHeader {
   int32_t tie_lat;
   uint64_t seed_index;
   int64_t qa_floor;
-  int64_t pad_;
+  // Branch and bound (bnb.cuh): per node the options that pass the quality
+  // floor in exploration order (best primary value first; int32 at optoff),
+  // their count, per-node bounds over those options, and the plans below a
+  // prefix of length k (uint64[n+1], rk[n] = 1).
+  int32_t off_perm;
+  int32_t off_nok;
+  int32_t off_bmin;
+  int32_t off_rk;
+  // Latency bound caching: with the first k digits fixed, a node is
+  // "settled" when it and all its ancestors are among them (its finish time
+  // is then the same for every plan below).  uns: per depth k the nodes NOT
+  // settled, in topological order; nsettle: per depth k the nodes that become
+  // settled when node k is fixed.  Both are int32 CSR: [n+1] offsets, entries.
+  int32_t off_uns;
+  int32_t off_nsettle;
+  int32_t pad_bnb[2];
+};
+
+// Per-node bounds over the options that pass the quality floor: the smallest
+// FP_A / FP_B term and wall, the largest quality and identifier-rank term
+// (smallest lexw), for subtree lower bounds.
+struct alignas(16) BnbMin {
+  double a;
+  double b;
+  int64_t w;
+  uint64_t lex;
+  int32_t q;
+  int32_t pad[3];
 };
 
 // A candidate / winner inside the kernels: the quantized criteria, exact
@@ -121,6 +148,24 @@ struct alignas(16) JobSync {
   // found by any thread of the job so far); 0 = none.  atomicMax only.
   unsigned long long best_neg;
   unsigned long long pad2;
+};
+
+// Per-job state of the branch-and-bound search (bnb.cuh), zero between
+// launches (the last CTA resets it).  The task counter, the work counter and
+// the published best sit on separate 128-byte lines: warps hammer the first
+// and read the last at every DFS step.
+struct alignas(128) BnbSync {
+  unsigned long long next_task;
+  unsigned char pad0[120];
+  unsigned long long work;  // child evaluations so far (flushed per warp)
+  unsigned abort;           // evaluation budget exhausted
+  unsigned ticket;          // CTA arrivals of the final reduction
+  unsigned char pad1[112];
+  unsigned lock;
+  unsigned seq;             // even: best is stable; odd: a writer is updating it
+  unsigned pad2[2];
+  Rec best;
+  unsigned char pad3[64];
 };
 
 // Per-job launch descriptor (global memory).

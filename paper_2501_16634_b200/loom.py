@@ -176,6 +176,8 @@ def lib() -> C.CDLL:
         "loom_search_argmin_async": ([vp, vp, C.c_uint64, C.c_uint64], C.c_int),
         "loom_search_argmin_shard": ([vp, P, O, C.c_uint64, C.c_uint64, C.c_uint64, W], C.c_int),
         "loom_search_argmin_shard_async": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64], C.c_int),
+        "loom_search_argmin_algo_async": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32], C.c_int),
+        "loom_bnb_last_stats": ([C.POINTER(C.c_uint64)], C.c_int),
         "loom_device_problem_bytes": ([vp], C.c_uint64),
         "loom_search_argmin_result": ([vp, vp, W], C.c_int),
         "loom_search_pareto": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64,
@@ -440,6 +442,15 @@ def search_argmin(ctx: Context, problem: Problem, obj: Objective, begin: int = 0
 
 
 INCUMBENT_GREEDY = (1 << 64) - 1
+NO_INCUMBENT = (1 << 64) - 2
+ALGO_AUTO, ALGO_FULL, ALGO_SWEEP = 0, 1, 2
+
+
+def bnb_last_stats() -> dict:
+    """Child evaluations and abort flag of the last branch-and-bound launch's job 0."""
+    buf = (C.c_uint64 * 4)()
+    _check(lib().loom_bnb_last_stats(buf))
+    return {"child_evaluations": buf[0], "aborted": bool(buf[1]), "max_task_steps": buf[2], "live_tasks": buf[3]}
 
 
 def search_argmin_shard(ctx: Context, problem: Problem, obj: Objective, begin: int, end: int,
@@ -489,6 +500,13 @@ class DeviceProblem:
     def search_async(self, begin: int = 0, end: int | None = None) -> None:
         end = (1 << 64) - 1 if end is None else end
         _check(lib().loom_search_argmin_async(self.ctx.handle, self._h, begin, end))
+
+    def search_algo_async(self, begin: int = 0, end: int | None = None, algo: int = ALGO_AUTO,
+                          incumbent: int = NO_INCUMBENT) -> None:
+        """Enqueue a search with a chosen algorithm (ALGO_AUTO: branch and bound
+        with the sweep as fallback; ALGO_FULL; ALGO_SWEEP: every plan tested)."""
+        end = (1 << 64) - 1 if end is None else end
+        _check(lib().loom_search_argmin_algo_async(self.ctx.handle, self._h, begin, end, incumbent, algo))
 
     def search_shard_async(self, begin: int, end: int, incumbent: int = INCUMBENT_GREEDY) -> None:
         """Enqueue loom_search_argmin_shard_async (argmin of [begin, end) u {incumbent})."""
