@@ -101,6 +101,10 @@ inline Lowered lower(const loom::WorkflowDag& dag, const loom::AgentLibrary& lib
       L.dol.push_back(plan.dollars * a.path_count);
       L.quality.push_back(loom::node_quality(node, *library.implementation(a.implementation), a.path_count));
       toks.push_back(token(node.id, a));
+      // the identifier tie-break by per-node rank is exact only when the ';'
+      // that ends a node's substring is its only one (as loom::lower checks)
+      if (toks.back().find(';') + 1 != toks.back().size())
+        throw loom::InvalidConfigError("name in '" + toks.back() + "' contains ';', which breaks identifier ordering");
     }
     std::vector<int> order(opts.size());
     std::iota(order.begin(), order.end(), 0);
@@ -125,9 +129,14 @@ inline Lowered lower(const loom::WorkflowDag& dag, const loom::AgentLibrary& lib
 
 inline loom_objective objective_of(const loom::ObjectiveHierarchy& h) {
   loom_objective o{};
-  o.n_criteria = static_cast<int32_t>(h.criteria.size());
-  for (std::size_t i = 0; i < h.criteria.size() && i < 4; ++i)
-    o.criteria[i] = static_cast<int32_t>(h.criteria[i]);  // same enumerator order (workflow.hpp:67)
+  // a repeated criterion never changes objective_less (estimator.hpp:93-116):
+  // keep each criterion's first occurrence, which leaves at most four
+  int n = 0;
+  for (const loom::Criterion c : h.criteria) {
+    const int32_t v = static_cast<int32_t>(c);  // same enumerator order (workflow.hpp:67)
+    if (std::find(o.criteria, o.criteria + n, v) == o.criteria + n) o.criteria[n++] = v;
+  }
+  o.n_criteria = n;
   if (h.quality_floor) {
     o.has_quality_floor = 1;
     o.quality_floor = *h.quality_floor;
@@ -139,9 +148,13 @@ inline loom_objective objective_of(const loom::ObjectiveHierarchy& h) {
 inline loom::ConfigEstimate exhaustive_search(const loom::WorkflowDag& dag, const loom::AgentLibrary& library,
                                               const loom::ObjectiveHierarchy& objective,
                                               const loom::SearchBounds& bounds, loom_ctx* ctx = nullptr) {
-  static loom_ctx* shared = nullptr;
   if (!ctx) {
-    if (!shared && loom_ctx_create(0, nullptr, &shared) != LOOM_OK) throw std::runtime_error(loom_last_error());
+    // created once, thread-safely (function-local static initialisation)
+    static loom_ctx* const shared = [] {
+      loom_ctx* c = nullptr;
+      if (loom_ctx_create(0, nullptr, &c) != LOOM_OK) throw std::runtime_error(loom_last_error());
+      return c;
+    }();
     ctx = shared;
   }
   const Lowered L = lower(dag, library, bounds);

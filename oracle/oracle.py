@@ -11,6 +11,7 @@ from /root/reference by oracle/Makefile) when it is present.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import json
 import os
 import subprocess
@@ -85,7 +86,20 @@ class OracleProblem:
 
 
 def problem(dag: dict, bundle: dict, bounds: dict) -> OracleProblem:
-    low = L.lower(dag, bundle, bounds)
+    return _from_lowered(L.lower(dag, bundle, bounds))
+
+
+def subproblem(p: OracleProblem, keep: list[list[int]]) -> OracleProblem:
+    """The plan space restricted to options keep[i] (ascending) of each node:
+    the same DAG and option values, fewer options, so the flat per-plan loop
+    can check the branch and bound on spaces the full loop cannot finish."""
+    low = p.lowered
+    pick = lambda per_node: [[lst[k] for k in ks] for lst, ks in zip(per_node, keep)]  # noqa: E731
+    return _from_lowered(dataclasses.replace(low, options=pick(low.options), plans=pick(low.plans),
+                                             quality=pick(low.quality), tokens=pick(low.tokens)))
+
+
+def _from_lowered(low) -> OracleProblem:
     flat = [(p, o, q, t) for pl, op, ql, tl in zip(low.plans, low.options, low.quality, low.tokens)
             for p, o, q, t in zip(pl, op, ql, tl)]
     keep = []

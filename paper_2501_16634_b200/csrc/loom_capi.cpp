@@ -151,16 +151,22 @@ int status_of(const loom::Error& e) {
 loom_objective to_objective(const loom::ObjectiveHierarchy& h, std::optional<loom::Micros> slo) {
   loom_objective o;
   std::memset(&o, 0, sizeof o);
-  if (h.criteria.size() > 4) throw loom::InvalidConfigError("more than 4 criteria");
-  o.n_criteria = static_cast<int32_t>(h.criteria.size());
-  for (std::size_t i = 0; i < h.criteria.size(); ++i) {
-    switch (h.criteria[i]) {
-      case loom::Criterion::min_cost_dollars: o.criteria[i] = LOOM_MIN_COST_DOLLARS; break;
-      case loom::Criterion::min_energy: o.criteria[i] = LOOM_MIN_ENERGY; break;
-      case loom::Criterion::min_latency: o.criteria[i] = LOOM_MIN_LATENCY; break;
-      case loom::Criterion::max_quality: o.criteria[i] = LOOM_MAX_QUALITY; break;
+  // objective_less (estimator.hpp:93-116) accepts any criteria list; a repeat
+  // of an earlier criterion compares values already found equal, so dropping
+  // it (keeping the first occurrence) leaves the order unchanged and at most
+  // the four distinct criteria remain
+  int n = 0;
+  for (const loom::Criterion c : h.criteria) {
+    int32_t v = 0;
+    switch (c) {
+      case loom::Criterion::min_cost_dollars: v = LOOM_MIN_COST_DOLLARS; break;
+      case loom::Criterion::min_energy: v = LOOM_MIN_ENERGY; break;
+      case loom::Criterion::min_latency: v = LOOM_MIN_LATENCY; break;
+      case loom::Criterion::max_quality: v = LOOM_MAX_QUALITY; break;
     }
+    if (std::find(o.criteria, o.criteria + n, v) == o.criteria + n) o.criteria[n++] = v;
   }
+  o.n_criteria = n;
   if (h.quality_floor) {
     o.has_quality_floor = 1;
     o.quality_floor = *h.quality_floor;

@@ -222,7 +222,11 @@ __device__ __forceinline__ Rec slot_load(const Slots& s, int t) {
 __device__ __forceinline__ void slot_thresholds(const Slots& s, int t, const BlobHeader* h) {
   const bool f = s.found[t];
   s.hi[t] = f ? hi_of(s.qa[t]) : INFINITY;
-  const bool tight = f && (h->prim == kPrimLat || (h->tie_lat && s.qa[t] <= h->qa_floor));
+  // latency-first objectives only: an empty hierarchy also runs the kPrimLat
+  // kernel, but there the identifier alone orders plans, so a slower plan can
+  // still win and the SLO is the only latency bound
+  const bool lat_first = h->prim == kPrimLat && h->n_crit > 0;
+  const bool tight = f && (lat_first || (h->tie_lat && s.qa[t] <= h->qa_floor));
   s.lat_s[t] = tight ? min(h->slo_eff, s.lat[t]) : h->slo_eff;
   s.bq[t] = f ? s.qual[t] : INT_MIN;
 }

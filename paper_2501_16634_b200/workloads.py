@@ -171,8 +171,14 @@ def config2() -> Workload:
 # ---------------------------------------------------------------------------
 C3_SEED = 20250316
 # 10th percentile of the latencies of 200,000 uniformly sampled plans of the
-# C3 space (derived once with the oracle; tests/test_workloads.py re-derives it).
+# C3 space (derived once with the oracle).  It does NOT bind at the MIN_COST
+# optimum: the best all-CPU plan takes 47,258,723 us and has gpu_wh = 0, so the
+# argmin is the node-local greedy seed (tests/golden/c3/full_space.json).
 C3_SLO_US = 72043534
+# The bench's headline SLO: below the all-CPU optimum, so every feasible plan
+# puts work on GPUs, MIN_COST trades GPU energy against the critical path, and
+# the argmin is not the greedy seed (checked by bench.py and the tests).
+C3_BINDING_SLO_US = 40_000_000
 
 
 def _two_class_library(rng: random.Random, caps: list[str], cpu_units: tuple[int, int],

@@ -1,0 +1,132 @@
+"""Full-space goldens for the large configurations (TEST INFRASTRUCTURE).
+
+    python tests/golden/make_fullspace.py [c3] [c4] [c5]
+
+Runs the CPU oracle (oracle/flat_oracle.c, a plain-C restatement of the
+reference's per-plan algorithm, itself pinned to the compiled reference by
+tests/test_oracle.py) over the WHOLE plan space of each configuration and
+writes the answers the GPU tests compare against:
+
+  c3/full_space.json  C3 (1.1e12 plans) argmin under MIN_COST with binding and
+                      non-binding latency SLOs, MIN_LATENCY, MIN_DOLLARS under an
+                      SLO and MAX_QUALITY, by the oracle's exact branch and
+                      bound (oracle_argmin_bnb; validated against the flat
+                      per-plan loop by tests/test_oracle.py on restricted C3
+                      spaces and against the reference's goldens), plus the
+                      MIN_COST answer re-derived by the flat loop over the
+                      8^10-plan all-CPU subspace (see test_c3_all_cpu_subspace).
+  c4/all_jobs.json    every one of the 10,000 C4 jobs (262,144 plans each),
+                      MIN_COST and MIN_LATENCY, by the flat per-plan loop.
+  c5/frontier.json    the exact pareto_filter of all 1e9 C5 plans by the flat
+                      streaming skyline (oracle_pareto).
+
+Nothing here reads the product library.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle import oracle as O  # noqa: E402
+from paper_2501_16634_b200 import workloads as W  # noqa: E402
+
+THREADS = os.cpu_count() or 1
+
+# C3 objectives: C3_SLO_US (72.0 s) does not bind -- the all-CPU optimum takes
+# 47.26 s -- so the others sit below it and force GPU nodes into the argmin.
+C3_OBJECTIVES = (
+    [{"constraint": "MIN_COST"}, {"constraint": "MIN_COST", "latency_slo_us": W.C3_SLO_US}]
+    + [{"constraint": "MIN_COST", "latency_slo_us": s}
+       for s in (46_000_000, 44_000_000, 42_000_000, W.C3_BINDING_SLO_US, 38_000_000, 36_000_000, 34_000_000)]
+    + [{"constraint": "MIN_LATENCY"}, {"constraint": "MIN_DOLLARS", "latency_slo_us": W.C3_BINDING_SLO_US},
+       {"constraint": "MIN_DOLLARS"}, {"constraint": "MAX_QUALITY"},
+       {"constraint": "MAX_QUALITY", "latency_slo_us": 60_000_000},
+       {"constraint": "MIN_COST", "latency_slo_us": 20_000_000}]  # infeasible
+)
+
+
+def row(r: dict | None) -> dict | None:
+    if r is None:
+        return None
+    return {k: r[k] for k in ("index", "latency_us", "gpu_wh", "cpu_wh", "total_wh", "dollars", "quality")}
+
+
+def c3() -> None:
+    w = W.config3(slo_us=None)
+    p = O.problem(w.dag, w.library, w.bounds)
+    out = {"workload": "C3 (workloads.config3, seed %d), 16^10 plans" % W.C3_SEED, "cases": []}
+    for o in C3_OBJECTIVES:
+        t0 = time.time()
+        r, visited = O.argmin_bnb(p, o, THREADS)
+        out["cases"].append({"objective": o, "winner": row(r),
+                             "identifier": O.identifier(p, r["index"]) if r else None,
+                             "oracle_subtrees_visited": visited})
+        print("c3", o, row(r), f"{time.time() - t0:.2f}s", flush=True)
+    # MIN_COST re-derived by the flat loop over the all-CPU subspace
+    t0 = time.time()
+    sub, full_index = all_cpu_subspace(p)
+    r = O.argmin(sub, {"constraint": "MIN_COST"}, threads=THREADS)
+    out["all_cpu_subspace"] = {"plans": sub.total, "sub_index": r["index"],
+                               "full_index": full_index(r["index"]), "winner": row(r)}
+    print("c3 all-cpu subspace", out["all_cpu_subspace"], f"{time.time() - t0:.1f}s", flush=True)
+    (HERE / "c3" / "full_space.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
+def all_cpu_subspace(p):
+    """The options with gpu_wh == 0 (CPU-only lowering) of every node, as a
+    sub-problem, and the map from its plan index to the full space's."""
+    low = p.lowered
+    keep = [[k for k, pl in enumerate(plans) if pl["gpu_wh"] == 0.0] for plans in low.plans]
+    sub = O.subproblem(p, keep)
+
+    def full_index(i: int) -> int:
+        digits = []
+        for ks in reversed(keep):
+            digits.append(ks[i % len(ks)])
+            i //= len(ks)
+        idx = 0
+        for d, r in zip(reversed(digits), low.radix):
+            idx = idx * r + d
+        return idx
+    return sub, full_index
+
+
+def c4() -> None:
+    jobs = W.config4(10_000)
+    out = {"workload": "C4 (workloads.config4, seed %d): 10,000 jobs x 8^6 plans" % W.C4_SEED,
+           "fields": ["index", "latency_us", "gpu_wh", "dollars"], "objectives": {}}
+    probs = [O.problem(j.dag, j.library, j.bounds) for j in jobs]
+    for token in ("MIN_COST", "MIN_LATENCY"):
+        t0 = time.time()
+        rows = []
+        for p in probs:
+            r = O.argmin(p, {"constraint": token}, threads=THREADS)
+            rows.append(None if r is None else [r["index"], r["latency_us"], r["gpu_wh"], r["dollars"]])
+        out["objectives"][token] = rows
+        print("c4", token, f"{time.time() - t0:.1f}s", flush=True)
+    (HERE / "c4" / "all_jobs.json").write_text(json.dumps(out, separators=(",", ":")) + "\n")
+
+
+def c5() -> None:
+    w = W.config5()
+    p = O.problem(w.dag, w.library, w.bounds)
+    t0 = time.time()
+    front = O.pareto(p, 0, p.total, threads=THREADS)
+    out = {"workload": "C5 (workloads.config5, seed %d): 10^9 plans" % W.C5_SEED, "plans": p.total,
+           "fields": ["index", "latency_us", "gpu_wh", "dollars", "quality"],
+           "frontier": [[f["index"], f["latency_us"], f["gpu_wh"], f["dollars"], f["quality"]] for f in front]}
+    print("c5", len(front), f"{time.time() - t0:.1f}s", flush=True)
+    (HERE / "c5" / "frontier.json").write_text(json.dumps(out, separators=(",", ":")) + "\n")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c3", "c4", "c5"]
+    for name in which:
+        globals()[name]()

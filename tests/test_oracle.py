@@ -2,6 +2,8 @@
 golden vectors produced by the compiled reference (tests/golden/make_golden.py)
 and, where they are published, against the reference's own known answers
 (test_fixture.cpp, test_cli.cpp)."""
+from pathlib import Path
+
 import pytest
 
 from conftest import cpu_threads
@@ -148,3 +150,151 @@ def test_c3_slices_match_reference(golden):
     s = gold["slice_no_slo"]
     got = O.argmin(p, {"constraint": "MIN_COST"}, s["begin"], s["end"], threads=cpu_threads())
     _same(got, s["result"]["winner"], p)
+
+
+# ---------------------------------------------------------------------------
+# The oracle's exact branch and bound (flat_oracle.c: oracle_argmin_bnb), which
+# produces the full-space C3 goldens, pinned to the reference's goldens and to
+# the flat per-plan loop.
+def test_bnb_matches_reference_c1(c1, golden):
+    w, p = c1
+    res = golden("c1/results.json")
+    for token in TOKENS:
+        got, _ = O.argmin_bnb(p, {"constraint": token}, threads=3)
+        _same(got, res["tokens"][token]["exhaustive"], p)
+    for floor, ref in res["floors"].items():
+        got, _ = O.argmin_bnb(p, {"constraint": "MIN_COST", "quality_floor": int(floor)})
+        if ref.get("error"):
+            assert got is None
+        else:
+            _same(got, ref, p)
+
+
+def test_bnb_matches_reference_random_and_c2(golden):
+    gold = golden("random/results.json")
+    checked = 0
+    for seed, entry in gold.items():
+        w = W.random_scenario(int(seed), max_nodes=4)
+        p = O.problem(w.dag, w.library, w.bounds)
+        for token, ref in entry.get("search", {}).items():
+            got, _ = O.argmin_bnb(p, {"constraint": token}, threads=2)
+            if ref.get("error"):
+                assert got is None
+            else:
+                _same(got, ref, p)
+                checked += 1
+    assert checked > 200
+    w = W.config2()
+    p = O.problem(w.dag, w.library, w.bounds)
+    for o in (w.objective, {"constraint": "MIN_COST"}, {"constraint": "MAX_QUALITY"},
+              {"constraint": "MIN_DOLLARS", "latency_slo_us": 300_000_000}):
+        got, _ = O.argmin_bnb(p, o)
+        ref = O.argmin(p, o, threads=cpu_threads())
+        assert got == ref, o
+    ref = golden("c2/results.json")
+    assert ref  # c2 goldens pin O.argmin (test_c2_* above); bnb == argmin here
+
+
+C3_RESTRICTIONS = [
+    [0, 3, 8, 11, 14],          # 5^10 plans: CPU and GPU options of both sizes
+    [1, 6, 9, 15],              # 4^10
+    [2, 5, 7, 10, 12, 13],      # 6^10 (~6e7)
+]
+
+
+@pytest.mark.parametrize("keep", C3_RESTRICTIONS)
+def test_bnb_matches_flat_loop_on_restricted_c3(keep):
+    """Restricted C3 spaces the flat per-plan loop finishes: the branch and
+    bound equals it under binding / non-binding SLOs and every token."""
+    w = W.config3(slo_us=None)
+    full = O.problem(w.dag, w.library, w.bounds)
+    p = O.subproblem(full, [keep] * 10)
+    objs = [{"constraint": "MIN_COST"}, {"constraint": "MIN_LATENCY"}, {"constraint": "MAX_QUALITY"},
+            {"constraint": "MIN_DOLLARS", "latency_slo_us": 45_000_000}]
+    lat = O.argmin(p, {"constraint": "MIN_LATENCY"}, threads=cpu_threads())["latency_us"]
+    cpu = O.argmin(p, {"constraint": "MIN_COST"}, threads=cpu_threads())["latency_us"]
+    for f in (0.2, 0.5, 0.8, 0.97):  # SLOs between the fastest plan and the cheapest
+        objs.append({"constraint": "MIN_COST", "latency_slo_us": int(lat + f * (cpu - lat))})
+    objs.append({"constraint": "MIN_COST", "latency_slo_us": lat - 1})  # infeasible
+    for o in objs:
+        got, _ = O.argmin_bnb(p, o)
+        ref = O.argmin(p, o, threads=cpu_threads())
+        assert got == ref, o
+
+
+def test_c3_full_space_goldens(golden):
+    """The committed full-space C3 answers (make_fullspace.py) are what the
+    oracle's branch and bound returns; the binding SLOs do bind."""
+    gold = golden("c3/full_space.json")
+    w = W.config3(slo_us=None)
+    p = O.problem(w.dag, w.library, w.bounds)
+    seed = gold["cases"][0]["winner"]["index"]  # MIN_COST: the all-CPU greedy seed
+    for case in gold["cases"]:
+        got, _ = O.argmin_bnb(p, case["objective"])
+        if case["winner"] is None:
+            assert got is None
+            continue
+        assert {k: got[k] for k in case["winner"]} == case["winner"]
+        assert O.identifier(p, got["index"]) == case["identifier"]
+        slo = case["objective"].get("latency_slo_us")
+        if case["objective"]["constraint"] == "MIN_COST" and slo is not None and slo < 47_258_723:
+            assert got["index"] != seed and got["gpu_wh"] > 0 and got["latency_us"] <= slo
+
+
+def test_c3_all_cpu_subspace(golden):
+    """MIN_COST ranks on quantize(gpu_wh) first; every C3 option
+    lowered onto a GPU has quantize(gpu_wh) >= 1 and every CPU option 0, so the
+    full-space argmin lies in the 8^10-plan all-CPU subspace, which the flat
+    per-plan loop searches exhaustively (~10 s on 8 threads)."""
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+    from make_fullspace import all_cpu_subspace
+
+    w = W.config3(slo_us=None)
+    p = O.problem(w.dag, w.library, w.bounds)
+    for plans, opts in zip(p.lowered.plans, p.lowered.options):
+        assert sum(pl["gpu_wh"] == 0.0 for pl in plans) == 8
+        for pl, op in zip(plans, opts):
+            assert pl["gpu_wh"] == 0.0 or pl["gpu_wh"] * op["path_count"] * 1e9 >= 0.5  # llround >= 1
+    sub, full_index = all_cpu_subspace(p)
+    assert sub.total == 8 ** 10
+    r = O.argmin(sub, {"constraint": "MIN_COST"}, threads=cpu_threads())
+    gold = golden("c3/full_space.json")
+    assert full_index(r["index"]) == gold["all_cpu_subspace"]["full_index"] == gold["cases"][0]["winner"]["index"]
+    assert r["latency_us"] == gold["cases"][0]["winner"]["latency_us"] == 47_258_723
+
+
+def test_c4_all_jobs_golden_pinned_to_reference(golden):
+    """The flat oracle's 10,000-job C4 golden agrees with every job the
+    compiled reference answered (c4/jobs.json), and re-derives on a sample."""
+    allj = golden("c4/all_jobs.json")["objectives"]["MIN_COST"]
+    ref = golden("c4/jobs.json")["jobs"]
+    jobs = W.config4(10_000)
+    for k, r in ref.items():
+        p = O.problem(jobs[int(k)].dag, jobs[int(k)].library, jobs[int(k)].bounds)
+        assert O.identifier(p, allj[int(k)][0]) == r["result"]["identifier"]
+        assert allj[int(k)][1:] == [r["result"]["latency_us"], r["result"]["gpu_wh"], r["result"]["dollars"]]
+    lat = golden("c4/all_jobs.json")["objectives"]["MIN_LATENCY"]
+    for k in (17, 4321, 9999):
+        p = O.problem(jobs[k].dag, jobs[k].library, jobs[k].bounds)
+        for token, g in (("MIN_COST", allj[k]), ("MIN_LATENCY", lat[k])):
+            r = O.argmin(p, {"constraint": token}, threads=cpu_threads())
+            assert [r["index"], r["latency_us"], r["gpu_wh"], r["dollars"]] == g
+
+
+def test_c5_frontier_golden_properties(golden):
+    """The committed 1e9-plan C5 frontier: ascending plan indices, each point
+    the oracle's estimate of its plan, no point dominated by another."""
+    import numpy as np
+    g = golden("c5/frontier.json")["frontier"]
+    w = W.config5()
+    p = O.problem(w.dag, w.library, w.bounds)
+    idx = [r[0] for r in g]
+    assert idx == sorted(idx) and len(g) == 2322
+    for r in g[::97]:
+        e = O.estimates(p, r[0], r[0] + 1)[0]
+        assert [e["latency_us"], e["gpu_wh"], e["dollars"], e["quality"]] == r[1:]
+    F = np.array([[r[3], r[2], r[1], -r[4]] for r in g], dtype=np.float64)
+    for i in range(len(F)):
+        le = (F <= F[i]).all(axis=1) & (F < F[i]).any(axis=1)
+        assert not le.any(), i
