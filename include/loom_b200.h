@@ -133,6 +133,10 @@ int loom_problem_total(const loom_problem* problem, uint64_t* total);
 /* Exact reference estimate of one plan (estimator.hpp:43-78) into a winner record. */
 int loom_evaluate_plan(const loom_problem* problem, uint64_t plan_index, loom_winner* out);
 /* objective_less over winner records; found==0 records lose.  Deterministic. */
+/* The smallest latency_us of any plan whose options meet the objective's
+ * quality floor (objective may be NULL): the critical path (estimator.hpp:69-76)
+ * with every node at its fastest option.  A latency SLO below it is infeasible. */
+int loom_latency_floor(const loom_problem* problem, const loom_objective* objective, int64_t* out);
 int loom_winner_less(const loom_winner* a, const loom_winner* b, const loom_objective* objective);
 int loom_winner_reduce(const loom_winner* winners, int32_t n, const loom_objective* objective,
                        loom_winner* out);
@@ -167,6 +171,50 @@ int loom_ctx_create(int32_t device, void* cuda_stream, loom_ctx** out);
 int loom_ctx_destroy(loom_ctx* ctx);
 /* Kernel launches issued by this ctx since creation (evidence for benches). */
 uint64_t loom_ctx_launch_count(const loom_ctx* ctx);
+/* The cudaStream_t the ctx launches on. */
+void* loom_ctx_stream(const loom_ctx* ctx);
+
+/* ---- multi-GPU groups ----------------------------------- */
+/* A group owns one device context per local GPU and one NCCL communicator
+ * (NCCL over NVLink/NVSwitch).  The plan space shards by contiguous index
+ * ranges (loom_shard_range), every rank starts from the same incumbent (the
+ * greedy seed), and one ncclAllGather of the per-rank results plus the
+ * deterministic objective_less reduce gives every rank the same winner --
+ * the caller of exhaustive_search (loom_main.cpp:140-146) sees one call.
+ *   loom_group_create(mask):   this process drives every device in the mask
+ *                              (bit d = device d; ncclCommInitAll; one host
+ *                              thread per device per call);
+ *   loom_group_create_rank():  one process per GPU (torchrun-style): rank 0
+ *                              makes an id with loom_nccl_unique_id, the
+ *                              caller distributes it, every rank joins. */
+#define LOOM_NCCL_ID_BYTES 128
+typedef struct loom_group loom_group;
+int loom_nccl_unique_id(uint8_t* out /* LOOM_NCCL_ID_BYTES */);
+int loom_group_create(uint64_t device_mask, loom_group** out);
+int loom_group_create_rank(int32_t device, void* cuda_stream, const uint8_t* nccl_id, int32_t rank,
+                           int32_t world, loom_group** out);
+int loom_group_destroy(loom_group* group);
+int32_t loom_group_world(const loom_group* group);  /* GPUs in the whole group    */
+int32_t loom_group_local(const loom_group* group);  /* GPUs driven by this process */
+int32_t loom_group_rank(const loom_group* group);   /* group rank of local GPU 0   */
+loom_ctx* loom_group_ctx(loom_group* group, int32_t local_index);
+/* Contiguous shard [*b, *e) of [begin, end) for rank of world (host only). */
+int loom_shard_range(uint64_t begin, uint64_t end, int32_t rank, int32_t world, uint64_t* b, uint64_t* e);
+/* loom_search_argmin over the group: every rank returns the same winner. */
+int loom_group_search_argmin(loom_group* group, const loom_problem* problem, const loom_objective* objective,
+                             uint64_t begin, uint64_t end, loom_winner* out);
+/* loom_search_pareto_points over the group (per-rank frontiers, all-gathered,
+ * filtered on the device, ascending plan index). */
+int loom_group_search_pareto_points(loom_group* group, const loom_problem* problem, uint64_t begin, uint64_t end,
+                                    loom_point* out, uint64_t capacity, uint64_t* count);
+/* loom_search_argmin_batch over the group (contiguous job ranges per rank). */
+int loom_group_search_argmin_batch(loom_group* group, const loom_problem* problems,
+                                   const loom_objective* objectives, int32_t n_jobs, loom_winner* out,
+                                   int32_t* status);
+/* loom_exhaustive_search_json over the group. */
+int loom_group_exhaustive_search_json(loom_group* group, const char* dag_json, const char* library_json,
+                                      const char* objective_json, const char* bounds_json, char* out_json,
+                                      size_t cap, size_t* needed);
 
 /* ---- search (device) ---------------------------------------------------- */
 /* Argmin over plan indices [begin, end) (end clamped to the total).  Fills
@@ -203,10 +251,16 @@ int loom_search_argmin_batch(loom_ctx* ctx, const loom_problem* problems,
 int loom_search_argmin_lowered(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n,
                                const loom_objective* objective, loom_winner* out, int32_t* status);
 
+/* Same with one objective per job (objectives[i] for lowered[i]). */
+int loom_search_argmin_lowered_each(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n,
+                                    const loom_objective* objectives, loom_winner* out, int32_t* status);
+
 /* The whole multi-tenant call on reference-format JSON: n DAGs against one
  * library bundle, bounds and objective -> n winners (a loop of
  * exhaustive_search, optimizer.hpp:173-188, with lowering on `threads` host
  * threads and one batched device search).  status[i] is the job's status. */
+/* objective_json is one objective for every job, or a JSON array of n
+ * per-job objectives (e.g. per-tenant latency SLOs). */
 int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const char* bounds_json,
                                  const char* const* dag_jsons, int32_t n, const char* objective_json,
                                  int32_t threads, loom_winner* out, int32_t* status);
@@ -238,10 +292,15 @@ int loom_search_argmin_shard_async(loom_ctx* ctx, loom_device_problem* dp, uint6
 #define LOOM_NO_INCUMBENT (UINT64_MAX - 1)
 int loom_search_argmin_algo_async(loom_ctx* ctx, loom_device_problem* dp, uint64_t begin, uint64_t end,
                                   uint64_t incumbent, int32_t algo);
-/* Evidence of the last branch-and-bound launch (its job 0): out[0] = child
- * evaluations (subtree bounds + leaves), out[1] = 1 if it exhausted its
- * budget and the sweep finished the search, out[2] = DFS steps of the longest
- * work unit, out[3] = work units that survived their root bound (4 entries). */
+/* Evidence of the last default (LOOM_ALGO_AUTO) search, job 0 (6 entries):
+ * out[0] = children evaluated (subtree bounds + leaves, all stages),
+ * out[1] = bit 0: the depth-first search ran (the frontier search overflowed
+ *          its buffers or did not apply); bit 1: its budget ran out and the
+ *          every-plan sweep finished the search,
+ * out[2] = largest frontier (frontier search) or longest work unit (depth first),
+ * out[3] = CTAs of the frontier launch (or work units alive at the root),
+ * out[4] = complete plans evaluated exactly (leaves),
+ * out[5] = children evaluated by the depth-first search. */
 int loom_bnb_last_stats(uint64_t* out);
 /* Wait for the last enqueued search of dp and decode its result. */
 int loom_search_argmin_result(loom_ctx* ctx, loom_device_problem* dp, loom_winner* out);

@@ -231,14 +231,23 @@ ConfigEstimate estimate(const ConfigPoint& config, const WorkflowDag& dag,
 bool objective_less(const ConfigEstimate& a, const ConfigEstimate& b,
                     const ObjectiveHierarchy& objective);
 bool meets_quality_floor(const ConfigEstimate& e, const ObjectiveHierarchy& objective);
-std::vector<ConfigEstimate> pareto_filter(const std::vector<ConfigEstimate>& estimates);
 
-// GPU-backed; ctx == nullptr uses a process-wide context on device 0.
+// GPU-backed.  The overloads without a context use this thread's own context
+// on device 0 (created on first use; concurrent callers do not serialise).
+// pareto_filter: stable input order, duplicates all kept (optimizer.hpp:153-171),
+// evaluated on the device (loom_pareto_filter_points).
+std::vector<ConfigEstimate> pareto_filter(const std::vector<ConfigEstimate>& estimates);
+std::vector<ConfigEstimate> pareto_filter(const std::vector<ConfigEstimate>& estimates, loom_ctx* ctx);
 ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
                                  const ObjectiveHierarchy& objective, const SearchBounds& bounds);
 ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
                                  const ObjectiveHierarchy& objective, const SearchBounds& bounds,
                                  loom_ctx* ctx, std::optional<Micros> latency_slo_us = std::nullopt);
+// Multi-GPU: the plan space sharded over the group's GPUs (loom_group_create /
+// loom_group_create_rank); every rank of the group returns the same estimate.
+ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
+                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds,
+                                 loom_group* group, std::optional<Micros> latency_slo_us = std::nullopt);
 
 // greedy_search (optimizer.hpp:227-291) on the GPU: node-local seeds on the
 // host, every sweep's per-node argmin on the device (one CTA).

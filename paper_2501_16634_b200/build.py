@@ -30,7 +30,7 @@ CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
              "-Wno-unused-parameter", *INCLUDES, "-I", "/usr/local/cuda/include"]
 
 CU_SOURCES = ["loom_search.cu", "loom_scores.cu"]
-CXX_SOURCES = ["loom_capi.cpp", "loom_host.cpp", "json.cpp"]
+CXX_SOURCES = ["loom_capi.cpp", "loom_host.cpp", "json.cpp", "loom_group.cpp"]
 
 
 def _run(cmd: list[str], log: list[str]) -> None:
@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
             _run(["g++", *CXX_FLAGS, "-c", str(CSRC / src), "-o", str(o)], log)
         objs.append(o)
     if force or _stale(lib, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lpthread"], log)
+        _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lpthread", "-lnccl"], log)
     if verbose:
         print("\n".join(log))
     (cu_obj / "build.log").write_text("\n".join(log))

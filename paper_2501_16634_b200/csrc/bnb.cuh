@@ -42,7 +42,7 @@
 constexpr int kBnbTasksPerWarp = 64;
 // Evidence of the last launch's job 0: child evaluations and the abort flag
 // (loom_bnb_last_stats).
-__device__ unsigned long long g_bnb_last[4];
+__device__ unsigned long long g_bnb_last[6];
 __device__ unsigned long long g_bnb_acc[2];  // running: max expansions of one task, tasks alive at the root
 
 // Bounds of the free nodes below a child of node k (nodes k+1 .. n-1), per
@@ -215,6 +215,10 @@ __global__ void __launch_bounds__(kBlock)
   __shared__ int am_last;
 
   const int job = blockIdx.x / ctas_per_job;
+  // after a frontier search (bfs.cuh) of this job: done -> retire at once;
+  // overflow -> continue depth first from its best plan
+  const unsigned prior = __ldcg(&sync[job].pad);
+  if (prior == kBnbDone) return;
   const JobDesc jd = jobs[job];
   BnbSync* bs = &bsync[job];
   load_blob(smem, arena + jd.blob_off, jd.blob_bytes, &mbar);
@@ -253,6 +257,11 @@ __global__ void __launch_bounds__(kBlock)
       if (best.found) W.bound = best;
       else best.found = 0;
     }
+    if (prior == kBfsOverflow) {
+      const Rec r = load_rec_cg(&out[job]);
+      if (rec_better(r, best, h)) best = r;
+      if (rec_better(best, W.bound, h)) W.bound = best;
+    }
   }
   __syncwarp();
 
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(kBlock)
   if (empty) n_tasks = 0;
   const bool ranged = jd.begin > 0 || jd.end < h->total;
   const uint64_t budget = max(h->total / 64, static_cast<uint64_t>(1) << 16);
-  uint64_t work_local = 0;
+  uint64_t work_local = 0, leaf_local = 0;
   unsigned steps = 0;
   bool aborted = false;
 
@@ -323,7 +332,9 @@ __global__ void __launch_bounds__(kBlock)
     int64_t lat;
     const int c = eval_child(k, slot, a, bb, q, lx, lat, lo);
     bool keep = false, improved = false;
-    if (c >= 0 && (!ranged || (lo < jd.end && lo + B.rk[k + 1] > jd.begin))) {
+    const bool live = c >= 0 && (!ranged || (lo < jd.end && lo + B.rk[k + 1] > jd.begin));
+    if (k == n - 1) leaf_local += __popc(__ballot_sync(0xffffffffu, live));
+    if (live) {
       const bool feas = lat <= h->slo_eff;
       if (k == n - 1) {
         if (feas) {
@@ -537,6 +548,7 @@ __global__ void __launch_bounds__(kBlock)
     }  // roots
   }
   if (lane == 0 && work_local) atomicAdd(&bs->work, work_local);
+  if (lane == 0 && leaf_local) atomicAdd(&bs->leaves, leaf_local);
 
   // lane bests -> CTA -> job (last CTA to arrive)
   Rec b = block_best(best, h, warp_slot);
@@ -565,6 +577,7 @@ __global__ void __launch_bounds__(kBlock)
         g_bnb_last[1] = bs->abort;
         g_bnb_last[2] = g_bnb_acc[0];
         g_bnb_last[3] = g_bnb_acc[1];
+        g_bnb_last[4] = bs->leaves;
         g_bnb_acc[0] = 0;
         g_bnb_acc[1] = 0;
       }
@@ -574,6 +587,7 @@ __global__ void __launch_bounds__(kBlock)
       bs->abort = 0;
       bs->next_task = 0;
       bs->work = 0;
+      bs->leaves = 0;
       bs->best = Rec{0, 0, 0, 0, 0, 0, 0};
     }
   }

@@ -34,6 +34,11 @@ struct loom_ctx {
   size_t out_cap = 0;
   loomk::BnbSync* d_bsync = nullptr;  // branch-and-bound per-job state (zero between launches)
   size_t bsync_cap = 0;
+  // frontier branch and bound (bfs.cuh): two frontier buffers of front_cap
+  // entries each (allocated on first use) and the job state
+  loomk::FrontierEntry* d_front = nullptr;
+  size_t front_cap = 0;
+  loomk::BfsSync* d_bfs = nullptr;
   loomk::Rec* h_out = nullptr;  // pinned
   size_t h_out_cap = 0;
   uint8_t* h_arena = nullptr;  // pinned staging of batch problem images

@@ -3,6 +3,7 @@
 // winner records (multi-rank combine), reference-format JSON lowering, and the
 // drop-in entry points loom::exhaustive_search / loom_exhaustive_search_json.
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <cstdio>
 #include <chrono>
@@ -183,14 +184,44 @@ struct ParsedObjective {
   std::optional<loom::Micros> slo;
 };
 
+ParsedObjective parse_objective_value(const loomjson::Value& j);
+
 ParsedObjective parse_objective_json(const std::string& text) {
-  ParsedObjective out;
   loomjson::Value j;
   try {
     j = loomjson::parse(text);
   } catch (const loomjson::ParseError& e) {
     throw loom::SchemaError(std::string("malformed objective: ") + e.what());
   }
+  return parse_objective_value(j);
+}
+
+// One objective, or (batch calls) a JSON array of per-job objectives.
+std::vector<loom_objective> parse_objectives_json(const std::string& text, int32_t n) {
+  loomjson::Value j;
+  try {
+    j = loomjson::parse(text);
+  } catch (const loomjson::ParseError& e) {
+    throw loom::SchemaError(std::string("malformed objective: ") + e.what());
+  }
+  std::vector<loom_objective> out;
+  if (!j.is_array()) {
+    const ParsedObjective p = parse_objective_value(j);
+    out.assign(static_cast<size_t>(std::max(n, 1)), to_objective(p.hierarchy, p.slo));
+    return out;
+  }
+  if (static_cast<int64_t>(j.size()) != n)
+    throw loom::SchemaError("objective array has " + std::to_string(j.size()) + " entries for " +
+                            std::to_string(n) + " jobs");
+  for (const auto& v : j.items()) {
+    const ParsedObjective p = parse_objective_value(v);
+    out.push_back(to_objective(p.hierarchy, p.slo));
+  }
+  return out;
+}
+
+ParsedObjective parse_objective_value(const loomjson::Value& j) {
+  ParsedObjective out;
   try {
     if (const loomjson::Value* c = j.find("criteria")) {
       for (const auto& v : c->items()) {
@@ -259,29 +290,29 @@ struct loom_lowered {
 
 namespace loom {
 
-// Process-wide context for the 4-argument overload (device 0, own stream).
+// This thread's context for the overloads without one (device 0, own
+// stream): a loom_ctx is re-entrant per thread, so callers on different
+// threads run concurrently instead of queueing on one shared context.
 namespace {
-std::mutex g_ctx_mu;
-loom_ctx* g_ctx = nullptr;
-}  // namespace
-
-ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
-                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds) {
-  std::lock_guard<std::mutex> lock(g_ctx_mu);
-  if (!g_ctx && loom_ctx_create(0, nullptr, &g_ctx) != LOOM_OK)
-    throw std::runtime_error(loom_last_error());
-  return exhaustive_search(dag, library, objective, bounds, g_ctx);
+loom_ctx* thread_ctx() {
+  struct Holder {
+    loom_ctx* c = nullptr;
+    ~Holder() {
+      if (c) loom_ctx_destroy(c);
+    }
+  };
+  thread_local Holder h;
+  if (!h.c && loom_ctx_create(0, nullptr, &h.c) != LOOM_OK) throw std::runtime_error(loom_last_error());
+  return h.c;
 }
 
-ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
-                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds, loom_ctx* ctx,
-                                 std::optional<Micros> latency_slo_us) {
-  const LoweredProblem L = lower(dag, library, bounds);
+ConfigEstimate search_lowered_one(const LoweredProblem& L, const WorkflowDag& dag, const AgentLibrary& library,
+                                  const loom_objective& obj,
+                                  const std::function<int(const loom_problem*, loom_winner*)>& search) {
   if (L.total == 0) throw NoFeasibleConfigError("no configuration satisfies the quality floor and bounds");
   const loom_problem view = L.view();
-  const loom_objective obj = to_objective(objective, latency_slo_us);
   loom_winner w;
-  const int rc = loom_search_argmin(ctx, &view, &obj, 0, L.total, &w);
+  const int rc = search(&view, &w);
   if (rc == LOOM_INFEASIBLE) throw NoFeasibleConfigError("no configuration satisfies the quality floor and bounds");
   if (rc != LOOM_OK) throw std::runtime_error(loom_last_error());
   // The selected plan is re-estimated with the reference arithmetic on the
@@ -290,6 +321,51 @@ ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& lib
   if (e.latency_us != w.latency_us || e.gpu_wh != w.gpu_wh || e.dollars != w.dollars)
     throw std::runtime_error("DeviceError: GPU winner disagrees with host estimate");
   return e;
+}
+}  // namespace
+
+ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
+                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds) {
+  return exhaustive_search(dag, library, objective, bounds, thread_ctx());
+}
+
+ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
+                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds, loom_ctx* ctx,
+                                 std::optional<Micros> latency_slo_us) {
+  const LoweredProblem L = lower(dag, library, bounds);
+  const loom_objective obj = to_objective(objective, latency_slo_us);
+  return search_lowered_one(L, dag, library, obj, [&](const loom_problem* p, loom_winner* w) {
+    return loom_search_argmin(ctx, p, &obj, 0, L.total, w);
+  });
+}
+
+ConfigEstimate exhaustive_search(const WorkflowDag& dag, const AgentLibrary& library,
+                                 const ObjectiveHierarchy& objective, const SearchBounds& bounds, loom_group* group,
+                                 std::optional<Micros> latency_slo_us) {
+  const LoweredProblem L = lower(dag, library, bounds);
+  const loom_objective obj = to_objective(objective, latency_slo_us);
+  return search_lowered_one(L, dag, library, obj, [&](const loom_problem* p, loom_winner* w) {
+    return loom_group_search_argmin(group, p, &obj, 0, L.total, w);
+  });
+}
+
+std::vector<ConfigEstimate> pareto_filter(const std::vector<ConfigEstimate>& in) {
+  return pareto_filter(in, thread_ctx());
+}
+
+std::vector<ConfigEstimate> pareto_filter(const std::vector<ConfigEstimate>& in, loom_ctx* ctx) {
+  // the dominance axes only (optimizer.hpp:155-161), tagged with the input
+  // position; the device marks the points no other point dominates
+  std::vector<loom_point> pts(in.size());
+  for (std::size_t i = 0; i < in.size(); ++i)
+    pts[i] = loom_point{i, in[i].dollars, in[i].gpu_wh, in[i].latency_us, in[i].quality, 0};
+  std::vector<uint8_t> keep(in.size(), 0);
+  if (!in.empty() && loom_pareto_filter_points(ctx, pts.data(), pts.size(), keep.data()) != LOOM_OK)
+    throw std::runtime_error(loom_last_error());
+  std::vector<ConfigEstimate> kept;
+  for (std::size_t i = 0; i < in.size(); ++i)
+    if (keep[i]) kept.push_back(in[i]);
+  return kept;
 }
 
 namespace {
@@ -312,9 +388,7 @@ void greedy_prepare(const LoweredProblem& L, const WorkflowDag& dag, const loom_
 
 ConfigEstimate greedy_search(const WorkflowDag& dag, const AgentLibrary& library, const ObjectiveHierarchy& objective,
                              const SearchBounds& bounds, int max_sweeps) {
-  std::lock_guard<std::mutex> lock(g_ctx_mu);
-  if (!g_ctx && loom_ctx_create(0, nullptr, &g_ctx) != LOOM_OK) throw std::runtime_error(loom_last_error());
-  return greedy_search(dag, library, objective, bounds, max_sweeps, g_ctx);
+  return greedy_search(dag, library, objective, bounds, max_sweeps, thread_ctx());
 }
 
 ConfigEstimate greedy_search(const WorkflowDag& dag, const AgentLibrary& library, const ObjectiveHierarchy& objective,
@@ -425,6 +499,46 @@ int loom_evaluate_plan(const loom_problem* p, uint64_t plan_index, loom_winner* 
   return loomi::fill_winner(p, out);
 }
 
+int loom_latency_floor(const loom_problem* p, const loom_objective* o, int64_t* out) {
+  if (!p || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
+  uint64_t total = 0;
+  if (int rc = loomi::check_problem(p, &total)) return rc;
+  const int n = p->n_nodes;
+  // per node the smallest wall among options meeting the quality floor; the
+  // critical path is monotone in every wall (estimator.hpp:69-76), so these
+  // walls give the smallest latency of any plan
+  std::vector<int64_t> w(n, INT64_MAX);
+  for (int i = 0, k = 0; i < n; ++i)
+    for (int j = 0; j < p->radix[i]; ++j, ++k)
+      if (!o || !o->has_quality_floor || p->quality[k] >= o->quality_floor) w[i] = std::min(w[i], p->wall_us[k]);
+  for (int i = 0; i < n; ++i)
+    if (w[i] == INT64_MAX)
+      return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+  std::vector<int32_t> indeg(n, 0);
+  std::vector<std::vector<int32_t>> succ(n);
+  for (int e = 0; e < p->n_edges; ++e) {
+    succ[p->edge_from[e]].push_back(p->edge_to[e]);
+    ++indeg[p->edge_to[e]];
+  }
+  std::vector<int64_t> start(n, 0);
+  std::vector<int32_t> ready;
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) ready.push_back(i);
+  int64_t lat = 0;
+  for (std::size_t r = 0; r < ready.size(); ++r) {
+    const int v = ready[r];
+    const int64_t f = start[v] + w[v];
+    lat = std::max(lat, f);
+    for (int s2 : succ[v]) {
+      start[s2] = std::max(start[s2], f);
+      if (--indeg[s2] == 0) ready.push_back(s2);
+    }
+  }
+  if (static_cast<int>(ready.size()) != n) return loomi::fail(LOOM_INVALID, "CycleError: the dag has a cycle");
+  *out = n ? lat : 0;
+  return LOOM_OK;
+}
+
 int loom_winner_less(const loom_winner* a, const loom_winner* b, const loom_objective* o) {
   if (!a->found) return 0;
   if (!b->found) return 1;
@@ -527,8 +641,24 @@ int loom_lower_batch(const char* library_json, const char* bounds_json, const ch
 
 const loom_problem* loom_lowered_problem(const loom_lowered* lw) { return lw ? &lw->view : nullptr; }
 
+namespace {
+int search_lowered(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n, const loom_objective* objective,
+                   bool per_job, loom_winner* out, int32_t* status);
+}  // namespace
+
 int loom_search_argmin_lowered(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n,
                                const loom_objective* objective, loom_winner* out, int32_t* status) {
+  return search_lowered(ctx, lowered, n, objective, false, out, status);
+}
+
+int loom_search_argmin_lowered_each(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n,
+                                    const loom_objective* objectives, loom_winner* out, int32_t* status) {
+  return search_lowered(ctx, lowered, n, objectives, true, out, status);
+}
+
+namespace {
+int search_lowered(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n, const loom_objective* objective,
+                   bool per_job, loom_winner* out, int32_t* status) {
   if (!ctx || (n > 0 && (!lowered || !out || !status)) || !objective || n < 0)
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   // only the lowered jobs go to the device; the rest keep LOOM_INVALID
@@ -543,7 +673,8 @@ int loom_search_argmin_lowered(loom_ctx* ctx, const loom_lowered* const* lowered
     }
   }
   const int m = static_cast<int>(idx.size());
-  std::vector<loom_objective> objs(m, *objective);
+  std::vector<loom_objective> objs(m);
+  for (int k = 0; k < m; ++k) objs[k] = per_job ? objective[idx[k]] : *objective;
   std::vector<loom_winner> w(m);
   std::vector<int32_t> st(m, LOOM_OK);
   const int rc = loom_search_argmin_batch(ctx, probs.data(), objs.data(), m, w.data(), st.data());
@@ -553,14 +684,19 @@ int loom_search_argmin_lowered(loom_ctx* ctx, const loom_lowered* const* lowered
   }
   return rc;
 }
+}  // namespace
 
 int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const char* bounds_json,
                                  const char* const* dag_jsons, int32_t n, const char* objective_json,
                                  int32_t threads, loom_winner* out, int32_t* status) {
   if (!ctx || !objective_json || (n > 0 && (!out || !status)) || n < 0)
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
-  loom_objective obj;
-  if (int rc = loom_objective_parse(objective_json, &obj)) return rc;
+  std::vector<loom_objective> objs;
+  try {
+    objs = parse_objectives_json(objective_json, n);
+  } catch (const loom::Error& e) {
+    return loomi::fail(status_of(e), e.what());
+  }
   const bool trace = std::getenv("LOOM_TRACE") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
   auto mark = [&](const char* what) {
@@ -575,7 +711,7 @@ int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const 
   int rc = loom_lower_batch(library_json, bounds_json, dag_jsons, n, threads, lw.data(), lst.data());
   mark("lower");
   if (rc == LOOM_OK) {
-    rc = loom_search_argmin_lowered(ctx, lw.data(), n, &obj, out, status);
+    rc = search_lowered(ctx, lw.data(), n, objs.data(), objs.size() == static_cast<size_t>(n) && n > 1, out, status);
     for (int i = 0; i < n; ++i)
       if (lst[i] != LOOM_OK) status[i] = lst[i];
   }
@@ -621,9 +757,45 @@ int loom_lowered_option_json(const loom_lowered* lw, int32_t node, int32_t optio
 
 void loom_lowered_destroy(loom_lowered* lw) { delete lw; }
 
+}  // extern "C"
+
+namespace {
+// The drop-in call on JSON with the device search supplied by the caller (one
+// context, or a multi-GPU group).
+using SearchFn = std::function<int(const loom_problem*, const loom_objective*, uint64_t, loom_winner*)>;
+int exhaustive_json(const SearchFn& search, const char* dag_json, const char* library_json,
+                    const char* objective_json, const char* bounds_json, char* out_json, size_t cap,
+                    size_t* needed);
+}  // namespace
+
+extern "C" {
+
 int loom_exhaustive_search_json(loom_ctx* ctx, const char* dag_json, const char* library_json,
                                 const char* objective_json, const char* bounds_json, char* out_json, size_t cap,
                                 size_t* needed) {
+  return exhaustive_json(
+      [ctx](const loom_problem* p, const loom_objective* o, uint64_t total, loom_winner* w) {
+        return loom_search_argmin(ctx, p, o, 0, total, w);
+      },
+      dag_json, library_json, objective_json, bounds_json, out_json, cap, needed);
+}
+
+int loom_group_exhaustive_search_json(loom_group* g, const char* dag_json, const char* library_json,
+                                      const char* objective_json, const char* bounds_json, char* out_json,
+                                      size_t cap, size_t* needed) {
+  return exhaustive_json(
+      [g](const loom_problem* p, const loom_objective* o, uint64_t total, loom_winner* w) {
+        return loom_group_search_argmin(g, p, o, 0, total, w);
+      },
+      dag_json, library_json, objective_json, bounds_json, out_json, cap, needed);
+}
+
+}  // extern "C"
+
+namespace {
+int exhaustive_json(const SearchFn& search, const char* dag_json, const char* library_json,
+                    const char* objective_json, const char* bounds_json, char* out_json, size_t cap,
+                    size_t* needed) {
   int rc = LOOM_OK;
   std::string result;
   try {
@@ -636,7 +808,7 @@ int loom_exhaustive_search_json(loom_ctx* ctx, const char* dag_json, const char*
     const loom_problem view = L.view();
     const loom_objective o = to_objective(obj.hierarchy, obj.slo);
     loom_winner w;
-    rc = loom_search_argmin(ctx, &view, &o, 0, L.total, &w);
+    rc = search(&view, &o, L.total, &w);
     if (rc == LOOM_OK) {
       const loom::ConfigEstimate e = loom::estimate(L.config_of(w.plan_index), dag, lib);
       if (e.latency_us != w.latency_us || e.gpu_wh != w.gpu_wh || e.dollars != w.dollars)
@@ -658,5 +830,4 @@ int loom_exhaustive_search_json(loom_ctx* ctx, const char* dag_json, const char*
   loomi::set_error(err);
   return rc;
 }
-
-}  // extern "C"
+}  // namespace

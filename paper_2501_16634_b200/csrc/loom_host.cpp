@@ -18,7 +18,6 @@
 //   estimate                 estimator.hpp:43-78
 //   quantize/objective_less  estimator.hpp:85-116
 //   meets_quality_floor      estimator.hpp:118-121
-//   pareto_filter            optimizer.hpp:153-171
 //   identifier               config.hpp:49-61
 //   objective_from_token     workflow.hpp:91-106
 //   topological_order        workflow.hpp:467-498
@@ -745,22 +744,7 @@ bool meets_quality_floor(const ConfigEstimate& e, const ObjectiveHierarchy& obje
   return !objective.quality_floor || e.quality >= *objective.quality_floor;
 }
 
-std::vector<ConfigEstimate> pareto_filter(const std::vector<ConfigEstimate>& in) {
-  auto dominates = [](const ConfigEstimate& a, const ConfigEstimate& b) {
-    const bool le = a.dollars <= b.dollars && a.gpu_wh <= b.gpu_wh && a.latency_us <= b.latency_us &&
-                    a.quality >= b.quality;
-    const bool lt = a.dollars < b.dollars || a.gpu_wh < b.gpu_wh || a.latency_us < b.latency_us ||
-                    a.quality > b.quality;
-    return le && lt;
-  };
-  std::vector<ConfigEstimate> kept;
-  for (std::size_t i = 0; i < in.size(); ++i) {
-    bool beaten = false;
-    for (std::size_t j = 0; j < in.size() && !beaten; ++j) beaten = j != i && dominates(in[j], in[i]);
-    if (!beaten) kept.push_back(in[i]);
-  }
-  return kept;
-}
+// pareto_filter (optimizer.hpp:153-171) runs on the device: loom_capi.cpp.
 
 // ---------------------------------------------------------------------------
 // lowering

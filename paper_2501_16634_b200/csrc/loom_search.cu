@@ -66,6 +66,7 @@ namespace {
 constexpr int64_t kNeg = -(int64_t(1) << 62);
 constexpr unsigned kBnbDone = 1;     // JobSync.pad after a branch-and-bound launch (bnb.cuh)
 constexpr unsigned kBnbAborted = 2;
+constexpr unsigned kBfsOverflow = 3;  // after a frontier search (bfs.cuh) that overflowed: depth first takes over
 
 #ifndef LOOM_PAIR_UNROLL
 #define LOOM_PAIR_UNROLL 4
@@ -1146,7 +1147,7 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
     full_eval(v, jd.seed, c);
     slot_offer(sl, threadIdx.x, h, c);
   }
-  if (bnb_state == kBnbAborted) slot_offer(sl, threadIdx.x, h, load_rec_cg(&out[job]));
+  if (bnb_state == kBnbAborted || bnb_state == kBfsOverflow) slot_offer(sl, threadIdx.x, h, load_rec_cg(&out[job]));
 
   const uint64_t gt = static_cast<uint64_t>(part) * kBlock + threadIdx.x;
   const uint64_t nt = static_cast<uint64_t>(ctas_per_job) * kBlock;
@@ -1252,6 +1253,7 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
 using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, JobSync*, Rec*, InnerParams);
 
 #include "bnb.cuh"
+#include "bfs.cuh"
 
 
 // pt: the innermost table comes from the kernel parameter (single-problem
@@ -1774,6 +1776,7 @@ struct Built {
   uint64_t total = 0;
   uint64_t r_sub = 1;
   uint64_t n_sub = 0;
+  int bfs_bits = 0;  // bits of the packed digits of a frontier entry (the frontier search needs <= 64)
 };
 
 int align16(int x) { return (x + 15) & ~15; }
@@ -2035,9 +2038,11 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
     put_csr(hd.off_nsettle, nset);
     for (int i = 0; i < n; ++i) {
       std::vector<int32_t> ord;
-      BnbMin m{INFINITY, INFINITY, INT64_MAX, UINT64_MAX, INT_MIN, {0, 0, 0}};
+      BnbMin m{INFINITY, INFINITY, INT64_MAX, UINT64_MAX, INT_MIN, -1, {0, 0}};
       for (int k = optoff[i]; k < optoff[i + 1]; ++k) {
         if (!floor_ok(k)) continue;
+        if (m.o_wall < 0 || wall[k] < m.w || (wall[k] == m.w && ga[k] < ga[optoff[i] + m.o_wall]))
+          m.o_wall = k - optoff[i];
         ord.push_back(k - optoff[i]);
         m.a = std::min(m.a, ga[k]);
         m.b = std::min(m.b, gb[k]);
@@ -2096,6 +2101,12 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
     }
   }
   b.total = total;
+  b.bfs_bits = 0;
+  for (int i = 0; i < n; ++i) {
+    int bits = 1;
+    while ((int64_t(1) << bits) < p->radix[i]) ++bits;
+    b.bfs_bits += bits;
+  }
   b.r_sub = r_sub;
   b.n_sub = total / r_sub;
   return LOOM_OK;
@@ -2243,6 +2254,7 @@ struct loom_device_problem {
   cudaEvent_t done = nullptr;
   BnbSync* d_bsync = nullptr;
   int bnb_ctas = 0;  // 0: the image does not fit the branch-and-bound kernel
+  int bfs_ctas = 0;  // 0: no frontier search for this problem
 };
 
 namespace {
@@ -2298,6 +2310,71 @@ int bnb_ctas_for(const loom_ctx* c, size_t blob, int n) {
     return 0;
   }
   return c->sms * nb;
+}
+
+// Frontier search (bfs.cuh): shared memory = problem image + one column of
+// finish times per thread; one cooperative wave of CTAs.
+size_t bfs_smem_bytes(size_t blob, int n) { return ((blob + 127) & ~size_t(127)) + sizeof(int64_t) * kBlock * n; }
+
+bool bfs_usable(const Built& b, int n) { return n >= 1 && b.bfs_bits <= 64 && !b.blob.empty(); }
+
+size_t bfs_cap_entries() {
+  static const size_t cap = [] {
+    const char* e = std::getenv("LOOM_BFS_CAP");
+    return e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : (size_t(1) << 23);  // 8M entries x 32 B x 2
+  }();
+  return cap;
+}
+
+int ensure_bfs(loom_ctx* c) {
+  if (!c->d_front) {
+    LOOM_CUDA(cudaMalloc(&c->d_front, 2 * bfs_cap_entries() * sizeof(FrontierEntry)));
+    c->front_cap = bfs_cap_entries();
+  }
+  if (!c->d_bfs) {
+    LOOM_CUDA(cudaMalloc(&c->d_bfs, sizeof(BfsSync)));
+    LOOM_CUDA(cudaMemset(c->d_bfs, 0, sizeof(BfsSync)));
+  }
+  return LOOM_OK;
+}
+
+// CTAs of one co-resident wave of bfs_kernel (0: it does not fit).
+int bfs_ctas_for(const loom_ctx* c, size_t blob, int n) {
+  const size_t smem = bfs_smem_bytes(blob, n);
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(bfs_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(bfs_kernel), kBlock, smem) !=
+          cudaSuccess ||
+      nb < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+#ifdef LOOM_BFS_CTAS_PER_SM
+  nb = std::min(nb, LOOM_BFS_CTAS_PER_SM);
+#endif
+  return c->sms * nb;
+}
+
+// Which search the last default launch started with (loom_bnb_last_stats).
+std::atomic<int> g_last_default_bfs{0};
+
+int launch_bfs(loom_ctx* c, int ctas, const uint8_t* d_blob, size_t blob_bytes, int n, const JobDesc* d_job,
+               JobSync* d_ticket, Rec* d_out) {
+  if (int rc = ensure_bfs(c)) return rc;
+  FrontierEntry* b0 = c->d_front;
+  FrontierEntry* b1 = c->d_front + c->front_cap;
+  uint64_t cap = c->front_cap;
+  BfsSync* bs = c->d_bfs;
+  void* args[] = {&d_blob, &d_job, &bs, &b0, &b1, &cap, &d_ticket, &d_out};
+  LOOM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bfs_kernel), dim3(ctas), dim3(kBlock), args,
+                                        bfs_smem_bytes(blob_bytes, n), c->stream));
+  ++c->launches;
+  g_last_default_bfs = 1;
+  return LOOM_OK;
 }
 
 int ensure_host(loom_ctx* c, size_t need) {
@@ -2453,6 +2530,8 @@ int loom_ctx_destroy(loom_ctx* c) {
   cudaFree(c->d_scratch);
   cudaFree(c->d_tickets);
   cudaFree(c->d_bsync);
+  cudaFree(c->d_front);
+  cudaFree(c->d_bfs);
   cudaFree(c->d_out);
   for (void* q : c->pool_all) cudaFree(q);
   if (c->h_out) cudaFreeHost(c->h_out);
@@ -2463,6 +2542,8 @@ int loom_ctx_destroy(loom_ctx* c) {
 }
 
 uint64_t loom_ctx_launch_count(const loom_ctx* c) { return c ? c->launches : 0; }
+
+void* loom_ctx_stream(const loom_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
 namespace {
 int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin, uint64_t end,
@@ -2498,7 +2579,26 @@ int loom_search_argmin_algo_async(loom_ctx* c, loom_device_problem* dp, uint64_t
 
 int loom_bnb_last_stats(uint64_t* out) {
   if (!out) return LOOM_INVALID;
-  if (cudaMemcpyFromSymbol(out, g_bnb_last, sizeof(uint64_t) * 4) != cudaSuccess) return LOOM_DEVICE_ERROR;
+  uint64_t dfs[6] = {0, 0, 0, 0, 0, 0}, bfs[6] = {0, 0, 0, 0, 0, 0};
+  if (cudaMemcpyFromSymbol(dfs, g_bnb_last, sizeof dfs) != cudaSuccess ||
+      cudaMemcpyFromSymbol(bfs, g_bfs_last, sizeof bfs) != cudaSuccess)
+    return LOOM_DEVICE_ERROR;
+  if (g_last_default_bfs) {
+    const bool of = bfs[1] != 0;  // the depth-first search ran after the frontier search
+    out[0] = bfs[0] + (of ? dfs[0] : 0);
+    out[1] = (of ? 1u : 0u) | (of && dfs[1] ? 2u : 0u);
+    out[2] = bfs[2];
+    out[3] = bfs[3];
+    out[4] = bfs[4] + (of ? dfs[4] : 0);
+    out[5] = of ? dfs[0] : 0;
+  } else {
+    out[0] = dfs[0];
+    out[1] = 1u | (dfs[1] ? 2u : 0u);
+    out[2] = dfs[2];
+    out[3] = dfs[3];
+    out[4] = dfs[4];
+    out[5] = dfs[0];
+  }
   return LOOM_OK;
 }
 
@@ -2534,6 +2634,13 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  const int fctas = algo == kAlgoAuto && bfs_usable(b, p->n_nodes) ? bfs_ctas_for(c, b.blob.size(), p->n_nodes) : 0;
+  if (fctas) {
+    if (int rc = launch_bfs(c, fctas, c->d_arena, b.blob.size(), p->n_nodes, c->d_jobs, c->d_tickets, c->d_out))
+      return rc;
+  } else if (algo == kAlgoAuto) {
+    g_last_default_bfs = 0;
+  }
   if (bctas) {
     bnb_kernel<<<bctas, kBlock, bnb_smem_bytes(b.blob.size(), p->n_nodes), c->stream>>>(
         c->d_arena, c->d_jobs, bctas, c->d_scratch, c->d_tickets, c->d_bsync, c->d_out);
@@ -2727,6 +2834,7 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)));
   dp->ctas = ctas;
   dp->bnb_ctas = dp->built.blob.empty() ? 0 : bnb_ctas_for(c, dp->built.blob.size(), dp->host.n_nodes);
+  dp->bfs_ctas = bfs_usable(dp->built, dp->host.n_nodes) ? bfs_ctas_for(c, dp->built.blob.size(), dp->host.n_nodes) : 0;
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
              cudaMalloc(&dp->d_scratch, sizeof(Rec) * std::max(ctas, dp->bnb_ctas)) == cudaSuccess &&
@@ -2777,6 +2885,13 @@ int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
   const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built))));
   LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  if (algo == kAlgoAuto && dp->bfs_ctas) {
+    if (int rc = launch_bfs(c, dp->bfs_ctas, dp->d_blob, dp->built.blob.size(), dp->host.n_nodes, dp->d_job,
+                            dp->d_ticket, dp->d_out))
+      return rc;
+  } else if (algo == kAlgoAuto) {
+    g_last_default_bfs = 0;
+  }
   if (algo == kAlgoAuto && dp->bnb_ctas) {
     bnb_kernel<<<dp->bnb_ctas, kBlock, bnb_smem_bytes(dp->built.blob.size(), dp->host.n_nodes), c->stream>>>(
         dp->d_blob, dp->d_job, dp->bnb_ctas, dp->d_scratch, dp->d_ticket, dp->d_bsync, dp->d_out);

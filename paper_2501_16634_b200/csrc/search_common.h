@@ -102,7 +102,8 @@ struct alignas(16) BnbMin {
   int64_t w;
   uint64_t lex;
   int32_t q;
-  int32_t pad[3];
+  int32_t o_wall;  // option (index within the node) of the smallest wall, ties to the smaller FP_A term
+  int32_t pad[2];
 };
 
 // A candidate / winner inside the kernels: the quantized criteria, exact
@@ -160,12 +161,41 @@ struct alignas(128) BnbSync {
   unsigned long long work;  // child evaluations so far (flushed per warp)
   unsigned abort;           // evaluation budget exhausted
   unsigned ticket;          // CTA arrivals of the final reduction
-  unsigned char pad1[112];
+  unsigned long long leaves;  // complete plans evaluated exactly (flushed per warp)
+  unsigned char pad1[104];
   unsigned lock;
   unsigned seq;             // even: best is stable; odd: a writer is updating it
   unsigned pad2[2];
   Rec best;
   unsigned char pad3[64];
+};
+
+// Per-job state of the frontier (level-synchronous) branch and bound
+// (bfs.cuh), zero between launches: survivors per depth, the grid barrier,
+// the job's incumbent under a lock, and launch evidence.
+struct alignas(128) BfsSync {
+  unsigned long long count[kMaxNodes + 1];  // frontier entries per depth
+  unsigned bar_count;
+  unsigned bar_gen;
+  unsigned lock;
+  unsigned overflow;
+  unsigned long long evals;   // children evaluated (subtree bounds + leaves)
+  unsigned long long leaves;  // complete plans evaluated exactly
+  unsigned long long max_frontier;
+  unsigned long long pad;
+  Rec best;
+};
+
+// One surviving prefix of the frontier (48 bytes): its digits bit-packed
+// (node i at BfsShared.shift[i]), the exact dag-order folds of its FP terms,
+// its bound on the first criterion and the minimum quality of its nodes.
+struct alignas(16) FrontierEntry {
+  uint64_t dig;
+  double fa;
+  double fb;
+  int64_t key;  // the prefix's bound on the first criterion (larger = worse), re-checked before expanding
+  int32_t q;
+  int32_t pad[3];
 };
 
 // Per-job launch descriptor (global memory).

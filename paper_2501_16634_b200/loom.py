@@ -189,12 +189,32 @@ def lib() -> C.CDLL:
         "loom_estimate_range_device": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(EstimateStreams)], C.c_int),
         "loom_estimate_plans": ([vp, P, C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(EstimateStreams)], C.c_int),
         "loom_greedy_seed": ([P, O, C.POINTER(C.c_int32)], C.c_int),
+        "loom_latency_floor": ([P, vp, C.POINTER(C.c_int64)], C.c_int),
         "loom_search_greedy": ([vp, P, O, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, W], C.c_int),
         "loom_lowered_sweep_order": ([vp, C.POINTER(C.c_int32)], C.c_int),
         "loom_greedy_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32, C.c_char_p,
                                      C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
         "loom_exhaustive_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
                                          C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+        "loom_search_argmin_lowered_each": ([vp, C.POINTER(vp), C.c_int32, O, W, C.POINTER(C.c_int32)], C.c_int),
+        "loom_ctx_stream": ([vp], vp),
+        "loom_nccl_unique_id": ([C.POINTER(C.c_uint8)], C.c_int),
+        "loom_group_create": ([C.c_uint64, C.POINTER(vp)], C.c_int),
+        "loom_group_create_rank": ([C.c_int32, vp, C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.POINTER(vp)],
+                                   C.c_int),
+        "loom_group_destroy": ([vp], C.c_int),
+        "loom_group_world": ([vp], C.c_int32),
+        "loom_group_local": ([vp], C.c_int32),
+        "loom_group_rank": ([vp], C.c_int32),
+        "loom_group_ctx": ([vp, C.c_int32], vp),
+        "loom_shard_range": ([C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(C.c_uint64),
+                              C.POINTER(C.c_uint64)], C.c_int),
+        "loom_group_search_argmin": ([vp, P, O, C.c_uint64, C.c_uint64, W], C.c_int),
+        "loom_group_search_pareto_points": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(Point), C.c_uint64,
+                                             C.POINTER(C.c_uint64)], C.c_int),
+        "loom_group_search_argmin_batch": ([vp, P, O, C.c_int32, W, C.POINTER(C.c_int32)], C.c_int),
+        "loom_group_exhaustive_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                               C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -387,7 +407,8 @@ def exhaustive_search_batch(dags: Sequence[Any], library: Any, objective: Any, b
                             ctx: "Context", threads: int = 0) -> BatchResult:
     """The multi-tenant call on reference-format JSON: exhaustive_search
     (optimizer.hpp:173-188) for every DAG against one library, objective and
-    bounds, lowered on host threads and searched in one batched launch."""
+    bounds, lowered on host threads and searched in one batched launch.
+    `objective` may also be a list with one objective per DAG."""
     n = len(dags)
     arr = (C.c_char_p * max(1, n))(*[_text(d) for d in dags])
     res = BatchResult(n)
@@ -446,11 +467,23 @@ NO_INCUMBENT = (1 << 64) - 2
 ALGO_AUTO, ALGO_FULL, ALGO_SWEEP = 0, 1, 2
 
 
+def latency_floor(problem: Problem, obj: Objective | None = None) -> int:
+    """Smallest latency of any plan (loom_latency_floor): the critical path
+    with every node at its fastest option meeting the quality floor."""
+    out = C.c_int64()
+    _check(lib().loom_latency_floor(C.byref(problem), C.byref(obj) if obj is not None else None, C.byref(out)))
+    return out.value
+
+
 def bnb_last_stats() -> dict:
-    """Child evaluations and abort flag of the last branch-and-bound launch's job 0."""
-    buf = (C.c_uint64 * 4)()
+    """Evidence of the last default (branch-and-bound) search: subtree bounds +
+    leaves evaluated, whether the depth-first search had to take over from the
+    frontier search and whether the every-plan sweep finished it ("aborted"),
+    the largest frontier, and the leaves (plans evaluated exactly)."""
+    buf = (C.c_uint64 * 6)()
     _check(lib().loom_bnb_last_stats(buf))
-    return {"child_evaluations": buf[0], "aborted": bool(buf[1]), "max_task_steps": buf[2], "live_tasks": buf[3]}
+    return {"child_evaluations": buf[0], "depth_first": bool(buf[1] & 1), "aborted": bool(buf[1] & 2),
+            "max_frontier": buf[2], "ctas": buf[3], "leaves": buf[4], "depth_first_evaluations": buf[5]}
 
 
 def search_argmin_shard(ctx: Context, problem: Problem, obj: Objective, begin: int, end: int,
@@ -621,6 +654,111 @@ def default_context() -> Context:
     if _default_ctx is None:
         _default_ctx = Context(0)
     return _default_ctx
+
+
+# ---- multi-GPU groups (loom_group_*; NCCL owned by the library) -------------
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL id for loom_group_create_rank (made by rank 0, shared by the caller)."""
+    buf = (C.c_uint8 * NCCL_ID_BYTES)()
+    _check(lib().loom_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def shard_range(begin: int, end: int, rank: int, world: int) -> tuple[int, int]:
+    """The library's contiguous shard of [begin, end) for rank of world (host)."""
+    b, e = C.c_uint64(), C.c_uint64()
+    _check(lib().loom_shard_range(begin, end, rank, world, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+class Group:
+    """A set of GPUs searching one plan space together (loom_group_*): the
+    plan space is sharded by contiguous index ranges inside the library and
+    the per-rank results are exchanged with ncclAllGather; every rank gets the
+    same answer.  Group(device_mask=m): this process drives every GPU in m;
+    Group(device=d, rank=r, world=w, nccl_id=id): one process per GPU."""
+
+    def __init__(self, device_mask: int | None = None, *, device: int = 0, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None, stream: int | None = None):
+        h = C.c_void_p()
+        if device_mask is not None:
+            _check(lib().loom_group_create(device_mask, C.byref(h)))
+        else:
+            idb = (C.c_uint8 * NCCL_ID_BYTES).from_buffer_copy(nccl_id)
+            handle = None if stream is None else C.c_void_p(stream if stream else 1)
+            _check(lib().loom_group_create_rank(device, handle, idb, rank, world, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    world = property(lambda self: lib().loom_group_world(self._h))
+    local = property(lambda self: lib().loom_group_local(self._h))
+    rank = property(lambda self: lib().loom_group_rank(self._h))
+
+    def launches(self) -> int:
+        return sum(lib().loom_ctx_launch_count(lib().loom_group_ctx(self._h, i)) for i in range(self.local))
+
+    def close(self) -> None:
+        if self._h:
+            lib().loom_group_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search_argmin(self, problem: Problem, obj: Objective, begin: int = 0, end: int | None = None) -> dict:
+        w = Winner()
+        end = (1 << 64) - 1 if end is None else end
+        _check(lib().loom_group_search_argmin(self._h, C.byref(problem), C.byref(obj), begin, end, C.byref(w)))
+        return w.as_dict()
+
+    def search_pareto_points(self, problem: Problem, begin: int = 0, end: int | None = None) -> list[dict]:
+        end = (1 << 64) - 1 if end is None else end
+        cnt = C.c_uint64(0)
+        _check(lib().loom_group_search_pareto_points(self._h, C.byref(problem), begin, end, None, 0, C.byref(cnt)))
+        buf = (Point * max(1, cnt.value))()
+        _check(lib().loom_group_search_pareto_points(self._h, C.byref(problem), begin, end, buf, cnt.value,
+                                                      C.byref(cnt)))
+        return [buf[i].as_dict() for i in range(cnt.value)]
+
+    def search_argmin_batch(self, problems: Sequence[Problem], objectives: Sequence[Objective]
+                            ) -> list[tuple[int, dict]]:
+        n = len(problems)
+        P = (Problem * n)(*problems)
+        O = (Objective * n)(*objectives)
+        W = (Winner * n)()
+        S = (C.c_int32 * n)()
+        _check(lib().loom_group_search_argmin_batch(self._h, P, O, n, W, S))
+        return [(S[i], W[i].as_dict()) for i in range(n)]
+
+    def exhaustive_search(self, dag: Any, library: Any, objective_: Any, bounds: Any) -> dict:
+        """loom_group_exhaustive_search_json: the drop-in call over the group."""
+        return _json_call(lib().loom_group_exhaustive_search_json, self._h, dag, library, objective_, bounds)
+
+
+def _json_call(fn, handle, dag: Any, library: Any, objective_: Any, bounds: Any) -> dict:
+    if isinstance(objective_, str) and not objective_.lstrip().startswith("{"):
+        objective_ = {"constraint": objective_}
+    need = C.c_size_t(0)
+    cap = 1 << 16
+    buf = C.create_string_buffer(cap)
+    rc = fn(handle, _text(dag), _text(library), _text(objective_), _text(bounds), buf, cap, C.byref(need))
+    if rc != LOOM_OK and need.value > cap:
+        buf = C.create_string_buffer(need.value)
+        rc = fn(handle, _text(dag), _text(library), _text(objective_), _text(bounds), buf, need.value,
+                C.byref(need))
+    out = json.loads(buf.value.decode())
+    if rc != LOOM_OK:
+        _raise(rc, out.get("message", last_error()))
+    return out
 
 
 def exhaustive_search(dag: Any, library: Any, objective_: Any, bounds: Any, ctx: Context | None = None) -> dict:

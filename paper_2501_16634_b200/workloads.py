@@ -247,6 +247,17 @@ C4_BOUNDS = {"max_fanout": 2, "max_paths": 1, "sku_pool_cap": {"cpu-epyc": 96, "
              "sku_total_cap": {"cpu-epyc": 192, "gpu-a100": 16, "gpu-h100": 16}}
 
 
+# C4's binding objective: every tenant asks for MIN_COST under its own latency
+# SLO of 110 % of its fastest plan (the critical path with every node at its
+# fastest option, loom_latency_floor).  Without an SLO every C4 winner is an
+# all-CPU plan (gpu_wh = 0) that node-local choices already find.
+C4_SLO_PERCENT = 110
+
+
+def c4_slo_objective(latency_floor_us: int) -> dict:
+    return {"constraint": "MIN_COST", "latency_slo_us": latency_floor_us * C4_SLO_PERCENT // 100}
+
+
 def config4(n_jobs: int = 10_000, seed: int = C4_SEED) -> list[Workload]:
     lib = config4_library(seed)
     return [Workload(f"c4_job{j}", config4_job(j, seed), lib, C4_BOUNDS, {"constraint": "MIN_COST"})

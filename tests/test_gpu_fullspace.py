@@ -71,7 +71,8 @@ def test_c3_binding_slo_is_not_the_greedy_seed(ctx, golden, c3):
     dp.search_async(0, None)
     assert dp.result() == got
     st = loom.bnb_last_stats()
-    assert not st["aborted"] and 0 < st["child_evaluations"] < lw.total // 10 ** 4
+    assert not st["aborted"] and not st["depth_first"] and 0 < st["child_evaluations"] < lw.total // 10 ** 4
+    assert 0 < st["leaves"] <= st["child_evaluations"] and st["max_frontier"] > 0
     dp.close()
 
 
@@ -94,15 +95,31 @@ def test_c3_full_space_one_plan_per_thread(ctx, golden, c3):
     _check(loom.search_argmin(ctx, lw.problem, loom.objective(o), 0, None, loom.ALGO_FULL), case, lw)
 
 
-@pytest.mark.parametrize("token", ["MIN_COST", "MIN_LATENCY"])
+def c4_objectives(jobs, token):
+    """The objective(s) of a C4 golden column; MIN_COST_SLO: one objective per
+    job, its SLO 110 % of the job's fastest plan (loom_latency_floor)."""
+    if token != "MIN_COST_SLO":
+        return {"constraint": token}
+    objs = []
+    for j in jobs:
+        lw = loom.Lowered(j.dag, j.library, j.bounds)
+        objs.append(W.c4_slo_objective(loom.latency_floor(lw.problem)))
+        lw.close()
+    return objs
+
+
+@pytest.mark.parametrize("token", ["MIN_COST", "MIN_LATENCY", "MIN_COST_SLO"])
 def test_c4_all_jobs(ctx, golden, token):
     """All 10,000 C4 jobs through the multi-tenant JSON call against the flat
     oracle's per-job answers."""
-    gold = golden("c4/all_jobs.json")["objectives"][token]
+    g_all = golden("c4/all_jobs.json")
+    gold = g_all["objectives"][token]
     jobs = W.config4(10_000)
     dags = [json.dumps(j.dag) for j in jobs]
-    res = loom.exhaustive_search_batch(dags, json.dumps(jobs[0].library), {"constraint": token},
-                                       json.dumps(jobs[0].bounds), ctx=ctx)
+    objs = c4_objectives(jobs, token)
+    if token == "MIN_COST_SLO":
+        assert [o["latency_slo_us"] for o in objs] == g_all["slo_us"]
+    res = loom.exhaustive_search_batch(dags, json.dumps(jobs[0].library), objs, json.dumps(jobs[0].bounds), ctx=ctx)
     assert len(res) == len(gold) == 10_000
     mism = []
     for k, g in enumerate(gold):
@@ -116,18 +133,23 @@ def test_c4_all_jobs(ctx, golden, token):
     assert not mism, mism[:10]
 
 
-def test_c4_min_latency_is_not_greedy(golden):
-    """MIN_LATENCY on C4 is a real search: off the critical path a node takes
-    its lowest-energy option with slack, so most winners differ from the
-    node-local greedy seed (every node at its smallest wall)."""
-    gold = golden("c4/all_jobs.json")["objectives"]["MIN_LATENCY"]
-    jobs = W.config4(200)
+def test_c4_slo_binds(golden):
+    """C4's binding objective: under 110 % of its fastest plan most jobs put
+    work on GPUs (gpu_wh > 0), so most winners differ from the unconstrained
+    MIN_COST winner (an all-CPU plan) and from the node-local greedy seed."""
+    g = golden("c4/all_jobs.json")["objectives"]
+    slo, cost = g["MIN_COST_SLO"], g["MIN_COST"]
+    assert all(r is not None for r in slo)
+    assert all(c[2] == 0.0 for c in cost)
+    assert sum(1 for r, c in zip(slo, cost) if r[0] != c[0] and r[2] > 0) > 8000
+    jobs = W.config4(100)
     differ = 0
-    for j, g in zip(jobs, gold):
+    for j, r in zip(jobs, slo):
         lw = loom.Lowered(j.dag, j.library, j.bounds)
-        differ += g[0] != _greedy_seed(lw, loom.objective("MIN_LATENCY"))
+        o = loom.objective(W.c4_slo_objective(loom.latency_floor(lw.problem)))
+        differ += r[0] != _greedy_seed(lw, o)
         lw.close()
-    assert differ > 100
+    assert differ > 80
 
 
 def test_c5_full_frontier(ctx, golden):

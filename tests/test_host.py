@@ -208,3 +208,36 @@ def test_bench_fast_path_matches_compiled_sass(loomlib):
     import bench
     fp = bench.FAST_PATH
     assert (fp["issue"], fp["alu"], fp["fp64"]) in rows, (fp, rows)
+
+
+@pytest.mark.parametrize("w", list(_workloads())[:12], ids=lambda w: w.name)
+def test_latency_floor_is_min_latency(loomlib, w):
+    """loom_latency_floor (every node at its fastest option meeting the
+    floor) equals the latency of the oracle's MIN_LATENCY argmin."""
+    lw = loom.Lowered(w.dag, w.library, w.bounds)
+    p = O.problem(w.dag, w.library, w.bounds)
+    for extra in ({}, {"quality_floor": 2}):
+        o = {"constraint": "MIN_LATENCY", **extra}
+        ref = O.argmin(p, o, 0, min(p.total, 2_000_000)) if p.total <= 2_000_000 else None
+        try:
+            got = loom.latency_floor(lw.problem, loom.objective(o))
+        except loom.NoFeasibleConfigError:
+            assert ref is None or p.total > 2_000_000
+            continue
+        if ref is not None:
+            assert got == ref["latency_us"]
+    lw.close()
+
+
+def test_batch_objective_array_is_validated(loomlib):
+    """The multi-tenant JSON call takes one objective or one per job; a
+    mismatched array is a schema error (status 2), before any device work."""
+    jobs = W.config4(3)
+    import json
+
+    class _Unused:  # the objectives are parsed before the context is touched
+        handle = C.c_void_p(16)
+
+    with pytest.raises(loom.LoomError, match="objective array has 2 entries for 3 jobs"):
+        loom.exhaustive_search_batch([j.dag for j in jobs], json.dumps(jobs[0].library),
+                                     [{"constraint": "MIN_COST"}] * 2, json.dumps(jobs[0].bounds), ctx=_Unused())

@@ -1,0 +1,20 @@
+#!/bin/bash
+# One GPU-box pass: GPU tests, the bench, the bench's launch list, and a full
+# ncu capture of the branch-and-bound kernel.  Outputs under gpurun_out/.
+set -u
+mkdir -p gpurun_out
+nvidia-smi -L > gpurun_out/smi.txt
+if [ "${SKIP_TESTS:-0}" != 1 ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS:-} > gpurun_out/gputest.log 2>&1
+  tail -3 gpurun_out/gputest.log
+fi
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -c 3000 gpurun_out/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-configs \
+  > gpurun_out/bench_ncu.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:bnb_kernel -s 1 -c 1 \
+  -o gpurun_out/bnb_full -f python tools/prof_bnb.py > gpurun_out/ncu_bnb.log 2>&1
+ncu -i gpurun_out/bnb_full.ncu-rep --page raw --csv > gpurun_out/bnb_raw.csv 2>/dev/null
+ncu -i gpurun_out/bnb_full.ncu-rep --page source --csv > gpurun_out/bnb_source.csv 2>/dev/null
+ls -la gpurun_out
