@@ -53,7 +53,8 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
     cu_obj = OBJ if variant is None else OBJ / "variants" / variant
     lib = LIB if variant is None else cu_obj / "libloom_b200.so"
     cu_obj.mkdir(parents=True, exist_ok=True)
-    headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.hpp")) + list((ROOT / "include").rglob("*.h*"))
+    headers = (list(CSRC.glob("*.h")) + list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh"))
+               + list((ROOT / "include").rglob("*.h*")))
     log: list[str] = []
     objs = []
     for src in CU_SOURCES:
