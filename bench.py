@@ -212,7 +212,19 @@ def b200_arm(args) -> None:
         else:
             dist.init_process_group(backend)
     stream = torch.cuda.Stream()
-    ctx = loom.Context(local, stream.cuda_stream)
+    # N > 1 over NCCL: the library's own multi-GPU group (loom_group_create_rank:
+    # its NCCL communicator, the sharded search and the ncclAllGather of the
+    # per-rank records all live in libloom_b200.so); torch.distributed only
+    # hands rank 0's NCCL id to the other ranks and times the ranks
+    use_group = world > 1 and backend == "nccl"
+    group = None
+    if use_group:
+        ids = [loom.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        group = loom.Group(device=local, rank=rank, world=world, nccl_id=ids[0], stream=stream.cuda_stream)
+        ctx = None
+    else:
+        ctx = loom.Context(local, stream.cuda_stream)
     w = W.config3(slo_us=W.C3_BINDING_SLO_US)
     dag_t, lib_t, obj_t, bounds_t = w.texts()
 
@@ -220,7 +232,7 @@ def b200_arm(args) -> None:
     obj = loom.objective(w.objective)
     total = lw.total
     begin, end = D.shard_range(total, rank, world)
-    dp = loom.DeviceProblem(ctx, lw.problem, obj)
+    dp = loom.DeviceProblem(ctx, lw.problem, obj) if not use_group else None
     scratch = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 
     def barrier():
@@ -231,7 +243,11 @@ def b200_arm(args) -> None:
                 dist.barrier()
         torch.cuda.synchronize()
 
+    group_out = {}
+
     def shard_result():
+        if use_group:
+            return group_out["w"]
         try:
             return dp.result()
         except loom.NoFeasibleConfigError:  # nothing feasible in this rank's shard
@@ -242,7 +258,9 @@ def b200_arm(args) -> None:
     # incumbent (loom_search_argmin_shard), so every shard prunes like the
     # whole-space search; the reduce over ranks is still the exact argmin.
     def search(b, e):
-        if world > 1:
+        if use_group:  # the whole space, sharded and exchanged inside the library
+            group_out["w"] = group.search_argmin(lw.problem, obj)
+        elif world > 1:
             dp.search_shard_async(b, e)
         else:
             dp.search_async(b, e)
@@ -250,7 +268,8 @@ def b200_arm(args) -> None:
     for _ in range(args.warmup):
         search(begin, end)
         shard_result()
-    launches0 = ctx.launches
+    count_launches = (lambda: group.launches()) if use_group else (lambda: ctx.launches)
+    launches0 = count_launches()
     step_ms = []
     with ClockSampler(local) as clocks:
         barrier()
@@ -264,7 +283,7 @@ def b200_arm(args) -> None:
             shard_result()
             step_ms.append(e0.elapsed_time(e1))
         barrier()
-    launches = ctx.launches - launches0
+    launches = count_launches() - launches0
     bnb = loom.bnb_last_stats()  # the last timed launch (this rank's job)
     local_ms = sum(step_ms) / len(step_ms)
     red_dev = "cuda" if backend == "nccl" else "cpu"
@@ -276,7 +295,7 @@ def b200_arm(args) -> None:
 
     # winners must agree with a full-space reduce (checked every run)
     local_w = shard_result()
-    winners = D.allgather_winners(local_w, device=red_dev) if world > 1 else [local_w]
+    winners = D.allgather_winners(local_w, device=red_dev) if world > 1 and not use_group else [local_w]
     chosen = D.combine(winners, obj)
     seed = greedy_seed_index(loom, lw, obj)
     # the headline is a real search: the SLO binds and the argmin is not the
@@ -287,6 +306,8 @@ def b200_arm(args) -> None:
     def e2e_step():
         if world == 1:
             return loom.exhaustive_search(dag_t, lib_t, obj_t, bounds_t, ctx=ctx)
+        if use_group:
+            return group.exhaustive_search(dag_t, lib_t, obj_t, bounds_t)
         low = loom.Lowered(dag_t, lib_t, bounds_t)
         o = loom.objective(obj_t)
         mine = D.search_shard(ctx, low.problem, o, rank, world)
@@ -308,6 +329,12 @@ def b200_arm(args) -> None:
     e2e_value = total / (float(te.item()) / 1e3)
     assert out["plan_index"] == chosen["plan_index"], (out, chosen)
 
+    if dp is not None:
+        image_bytes = dp.image_bytes
+    else:
+        probe = loom.DeviceProblem(group.context(0), lw.problem, obj)
+        image_bytes = probe.image_bytes
+        probe.close()
     if rank == 0:
         pk = peaks()
         clk = clocks.summary()
@@ -335,7 +362,7 @@ def b200_arm(args) -> None:
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "objective": w.objective,
-                       "plans_per_step": total, "parallelism": f"plan-index range x{world}",
+                       "plans_per_step": total, "parallelism": f"plan-index range x{world}" + (" (loom_group: NCCL inside the library)" if use_group else ""),
                        "l2": "flushed between timed steps (256 MiB write); the problem image is 8 KB in smem",
                        "value_counts": "plans COVERED per second: every plan of the space is in the argmin's "
                                        "domain; subtrees whose exact criteria bound is infeasible or strictly "
@@ -350,9 +377,10 @@ def b200_arm(args) -> None:
                        "chosen_latency_us": chosen["latency_us"], "chosen_gpu_wh": chosen["gpu_wh"],
                        "golden": "tests/golden/c3/full_space.json (CPU oracle, whole space)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": float(te.item()),
-                    "h2d_bytes_per_step": dp.image_bytes + 64, "d2h_bytes_per_step": 64,
+                    "h2d_bytes_per_step": image_bytes + 64, "d2h_bytes_per_step": 64,
                     "path": "loom_exhaustive_search_json: JSON parse + lowering + H2D + kernel + D2H + decode"
-                    if world == 1 else "lowering + loom_search_argmin_shard (range + greedy incumbent) + NCCL all-gather + reduce + decode"},
+                    if world == 1 else "loom_group_exhaustive_search_json: JSON parse + lowering + per-rank shard "
+                    "search (range + greedy incumbent) + ncclAllGather of the rank records + reduce + decode"},
             "roofline": {"bound": "instruction issue", "kernel": "bnb_kernel" if bnb["depth_first"] else "bfs_kernel", "achieved": achieved, "peak": peak,
                          "unit": "subtree bounds + leaf evaluations per second per GPU", "frac": achieved / peak,
                          "traffic": traffic, "evaluations_per_launch": evals,
@@ -369,8 +397,12 @@ def b200_arm(args) -> None:
         if not args.no_configs and world == 1:
             line["configs"] = other_configs(ctx, loom, W, issue)
         print(json.dumps(line), flush=True)
-    dp.close()
-    ctx.close()
+    if dp is not None:
+        dp.close()
+    if ctx is not None:
+        ctx.close()
+    if group is not None:
+        group.close()
     if world > 1:
         dist.destroy_process_group()
 

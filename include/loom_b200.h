@@ -302,6 +302,11 @@ int loom_search_argmin_algo_async(loom_ctx* ctx, loom_device_problem* dp, uint64
  * out[4] = complete plans evaluated exactly (leaves),
  * out[5] = children evaluated by the depth-first search. */
 int loom_bnb_last_stats(uint64_t* out);
+/* Per-level timeline of the last frontier search (profiling aid): out[0] =
+ * start and out[1] = end (%globaltimer ns), then per depth d out[2d+2] = end of
+ * the level, out[2d+3] = parents expanded (bit 63: evaluated redundantly by
+ * every CTA, without a grid barrier).  cap entries at most (<= 68). */
+int loom_bfs_trace(uint64_t* out, int32_t cap);
 /* Wait for the last enqueued search of dp and decode its result. */
 int loom_search_argmin_result(loom_ctx* ctx, loom_device_problem* dp, loom_winner* out);
 

@@ -2314,7 +2314,9 @@ int bnb_ctas_for(const loom_ctx* c, size_t blob, int n) {
 
 // Frontier search (bfs.cuh): shared memory = problem image + one column of
 // finish times per thread; one cooperative wave of CTAs.
-size_t bfs_smem_bytes(size_t blob, int n) { return ((blob + 127) & ~size_t(127)) + sizeof(int64_t) * kBlock * n; }
+size_t bfs_smem_bytes(size_t blob, int n) {
+  return ((blob + 127) & ~size_t(127)) + sizeof(int64_t) * kBfsBlock * n + 2 * sizeof(FrontierEntry) * kBfsBlock;
+}
 
 bool bfs_usable(const Built& b, int n) { return n >= 1 && b.bfs_bits <= 64 && !b.blob.empty(); }
 
@@ -2347,7 +2349,7 @@ int bfs_ctas_for(const loom_ctx* c, size_t blob, int n) {
     return 0;
   }
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(bfs_kernel), kBlock, smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(bfs_kernel), kBfsBlock, smem) !=
           cudaSuccess ||
       nb < 1) {
     cudaGetLastError();
@@ -2363,14 +2365,14 @@ int bfs_ctas_for(const loom_ctx* c, size_t blob, int n) {
 std::atomic<int> g_last_default_bfs{0};
 
 int launch_bfs(loom_ctx* c, int ctas, const uint8_t* d_blob, size_t blob_bytes, int n, const JobDesc* d_job,
-               JobSync* d_ticket, Rec* d_out) {
+               Rec* d_slots, JobSync* d_ticket, Rec* d_out) {
   if (int rc = ensure_bfs(c)) return rc;
   FrontierEntry* b0 = c->d_front;
   FrontierEntry* b1 = c->d_front + c->front_cap;
   uint64_t cap = c->front_cap;
   BfsSync* bs = c->d_bfs;
-  void* args[] = {&d_blob, &d_job, &bs, &b0, &b1, &cap, &d_ticket, &d_out};
-  LOOM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bfs_kernel), dim3(ctas), dim3(kBlock), args,
+  void* args[] = {&d_blob, &d_job, &bs, &b0, &b1, &cap, &d_slots, &d_ticket, &d_out};
+  LOOM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bfs_kernel), dim3(ctas), dim3(kBfsBlock), args,
                                         bfs_smem_bytes(blob_bytes, n), c->stream));
   ++c->launches;
   g_last_default_bfs = 1;
@@ -2577,6 +2579,14 @@ int loom_search_argmin_algo_async(loom_ctx* c, loom_device_problem* dp, uint64_t
   return search_async_impl(c, dp, begin, end, incumbent == UINT64_MAX - 1 ? kNoIncumbent : incumbent, algo);
 }
 
+int loom_bfs_trace(uint64_t* out, int32_t cap) {
+  if (!out || cap < 2) return LOOM_INVALID;
+  uint64_t buf[2 * (kMaxNodes + 2)];
+  if (cudaMemcpyFromSymbol(buf, g_bfs_trace, sizeof buf) != cudaSuccess) return LOOM_DEVICE_ERROR;
+  for (int i = 0; i < cap && i < 2 * (kMaxNodes + 2); ++i) out[i] = buf[i];
+  return LOOM_OK;
+}
+
 int loom_bnb_last_stats(uint64_t* out) {
   if (!out) return LOOM_INVALID;
   uint64_t dfs[6] = {0, 0, 0, 0, 0, 0}, bfs[6] = {0, 0, 0, 0, 0, 0};
@@ -2626,7 +2636,8 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   const int bctas = algo == kAlgoAuto ? bnb_ctas_for(c, b.blob.size(), p->n_nodes) : 0;
   if (int rc = ensure(c->d_arena, c->arena_cap, b.blob.size())) return rc;
   if (int rc = ensure(c->d_jobs, c->jobs_cap, 1)) return rc;
-  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(std::max(ctas, bctas)))) return rc;
+  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(std::max({ctas, bctas, c->sms * 4}))))
+    return rc;
   if (int rc = ensure_tickets(c, 1)) return rc;
   if (int rc = ensure_bsync(c, 1)) return rc;
   if (int rc = ensure(c->d_out, c->out_cap, 1)) return rc;
@@ -2636,7 +2647,8 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
   const int fctas = algo == kAlgoAuto && bfs_usable(b, p->n_nodes) ? bfs_ctas_for(c, b.blob.size(), p->n_nodes) : 0;
   if (fctas) {
-    if (int rc = launch_bfs(c, fctas, c->d_arena, b.blob.size(), p->n_nodes, c->d_jobs, c->d_tickets, c->d_out))
+    if (int rc = launch_bfs(c, fctas, c->d_arena, b.blob.size(), p->n_nodes, c->d_jobs, c->d_scratch, c->d_tickets,
+                            c->d_out))
       return rc;
   } else if (algo == kAlgoAuto) {
     g_last_default_bfs = 0;
@@ -2837,7 +2849,7 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   dp->bfs_ctas = bfs_usable(dp->built, dp->host.n_nodes) ? bfs_ctas_for(c, dp->built.blob.size(), dp->host.n_nodes) : 0;
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
-             cudaMalloc(&dp->d_scratch, sizeof(Rec) * std::max(ctas, dp->bnb_ctas)) == cudaSuccess &&
+             cudaMalloc(&dp->d_scratch, sizeof(Rec) * std::max({ctas, dp->bnb_ctas, dp->bfs_ctas})) == cudaSuccess &&
              cudaMalloc(&dp->d_bsync, sizeof(BnbSync)) == cudaSuccess &&
              cudaMemset(dp->d_bsync, 0, sizeof(BnbSync)) == cudaSuccess &&
              cudaMalloc(&dp->d_ticket, sizeof(JobSync)) == cudaSuccess &&
@@ -2887,7 +2899,7 @@ int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint
   LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
   if (algo == kAlgoAuto && dp->bfs_ctas) {
     if (int rc = launch_bfs(c, dp->bfs_ctas, dp->d_blob, dp->built.blob.size(), dp->host.n_nodes, dp->d_job,
-                            dp->d_ticket, dp->d_out))
+                            dp->d_scratch, dp->d_ticket, dp->d_out))
       return rc;
   } else if (algo == kAlgoAuto) {
     g_last_default_bfs = 0;

@@ -178,6 +178,7 @@ def lib() -> C.CDLL:
         "loom_search_argmin_shard_async": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64], C.c_int),
         "loom_search_argmin_algo_async": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32], C.c_int),
         "loom_bnb_last_stats": ([C.POINTER(C.c_uint64)], C.c_int),
+        "loom_bfs_trace": ([C.POINTER(C.c_uint64), C.c_int32], C.c_int),
         "loom_device_problem_bytes": ([vp], C.c_uint64),
         "loom_search_argmin_result": ([vp, vp, W], C.c_int),
         "loom_search_pareto": ([vp, P, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.c_uint64,
@@ -467,6 +468,21 @@ NO_INCUMBENT = (1 << 64) - 2
 ALGO_AUTO, ALGO_FULL, ALGO_SWEEP = 0, 1, 2
 
 
+def bfs_trace() -> dict:
+    """Per-level timeline of the last frontier search: microseconds per level,
+    parents expanded, and whether the level ran redundantly in every CTA."""
+    buf = (C.c_uint64 * 68)()
+    _check(lib().loom_bfs_trace(buf, 68))
+    t0, levels, prev = buf[0], [], buf[0]
+    for d in range(33):
+        end, par = buf[2 * d + 2], buf[2 * d + 3]
+        if not end:
+            break
+        levels.append({"us": (end - prev) / 1e3, "parents": par & ((1 << 63) - 1), "redundant": bool(par >> 63)})
+        prev = end
+    return {"total_us": (buf[1] - t0) / 1e3 if buf[1] else None, "levels": levels}
+
+
 def latency_floor(problem: Problem, obj: Objective | None = None) -> int:
     """Smallest latency of any plan (loom_latency_floor): the critical path
     with every node at its fastest option meeting the quality floor."""
@@ -674,6 +690,22 @@ def shard_range(begin: int, end: int, rank: int, world: int) -> tuple[int, int]:
     return b.value, e.value
 
 
+class BorrowedContext:
+    """A loom_ctx owned by someone else (a group member): usable wherever a
+    Context is, never destroyed through this handle."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @property
+    def launches(self) -> int:
+        return lib().loom_ctx_launch_count(self._h)
+
+
 class Group:
     """A set of GPUs searching one plan space together (loom_group_*): the
     plan space is sharded by contiguous index ranges inside the library and
@@ -702,6 +734,10 @@ class Group:
 
     def launches(self) -> int:
         return sum(lib().loom_ctx_launch_count(lib().loom_group_ctx(self._h, i)) for i in range(self.local))
+
+    def context(self, i: int = 0) -> "BorrowedContext":
+        """Member i's device context (owned by the group)."""
+        return BorrowedContext(lib().loom_group_ctx(self._h, i))
 
     def close(self) -> None:
         if self._h:

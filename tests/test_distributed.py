@@ -144,3 +144,62 @@ def test_sharded_frontier_allgather(world):
     w = W.config5(n_nodes=4)
     assert got == [o["index"] for o in O.pareto(O.problem(w.dag, w.library, w.bounds), threads=2)]
     assert len(got) > 3
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_library_shards_with_common_incumbent_reduce_to_argmin(world):
+    """The library's group search (loom_group_search_argmin) on N = 2, 4, 8
+    ranks, emulated on CPU: rank r's shard is loom_shard_range(r, N); each
+    rank's answer is the argmin of its shard plus the common incumbent (the
+    greedy seed, loom_greedy_seed), here computed by the oracle; the
+    exchanged records reduce (loom_winner_reduce, the same host function
+    the group calls after ncclAllGather) to the whole-space argmin."""
+    import ctypes as C
+    from oracle import oracle as O
+    from paper_2501_16634_b200 import loom, workloads as W
+
+    cases = [(W.config1(), t) for t in TOKENS] + [(W.config2(), "MIN_LATENCY"), (W.config2(), "MIN_COST")]
+    cases += [(W.random_scenario(s, max_nodes=4), t) for s in (1, 5, 9) for t in TOKENS]
+    for w, token in cases:
+        lw = loom.Lowered(w.dag, w.library, w.bounds)
+        p = O.problem(w.dag, w.library, w.bounds)
+        obj = {"constraint": token}
+        ob = loom.objective(obj)
+        seed_d = (C.c_int32 * lw.problem.n_nodes)()
+        has_seed = loom.lib().loom_greedy_seed(C.byref(lw.problem), C.byref(ob), seed_d) == 0
+        seed = 0
+        for d, r in zip(seed_d, lw.radix):
+            seed = seed * r + d
+        shards = [loom.shard_range(0, lw.total, r, world) for r in range(world)]
+        assert shards[0][0] == 0 and shards[-1][1] == lw.total
+        assert all(shards[r][1] == shards[r + 1][0] for r in range(world - 1))
+        assert max(e - b for b, e in shards) - min(e - b for b, e in shards) <= 1
+        recs = []
+        for b, e in shards:
+            best = O.argmin(p, obj, b, e, threads=2) if b < e else None
+            cands = [loom.winner_from_dict(lw.evaluate(best["index"]))] if best else []
+            if has_seed:
+                s = lw.evaluate(seed)
+                feas = O.argmin(p, obj, seed, seed + 1, threads=1)
+                s["found"] = 1 if feas else 0
+                cands.append(loom.winner_from_dict(s))
+            recs.append(loom.winner_from_dict(loom.winner_reduce(cands, ob) if cands and any(
+                c.found for c in cands) else loom.Winner().as_dict()) if cands else loom.Winner())
+        full = O.argmin(p, obj, threads=4)
+        if full is None:
+            with pytest.raises(loom.NoFeasibleConfigError):
+                loom.winner_reduce(recs, ob)
+        else:
+            assert loom.winner_reduce(recs, ob)["plan_index"] == full["index"]
+        lw.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_library_job_shards(world):
+    """Batches shard by contiguous job ranges (loom_group_search_argmin_batch):
+    every job lands in exactly one rank, ranks differ by at most one job."""
+    from paper_2501_16634_b200 import loom
+    for n in (0, 1, 7, 10_000):
+        shards = [loom.shard_range(0, n, r, world) for r in range(world)]
+        covered = [j for b, e in shards for j in range(b, e)]
+        assert covered == list(range(n))

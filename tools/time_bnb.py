@@ -29,5 +29,8 @@ for o in objs:
     st = loom.bnb_last_stats()
     tot += min(ts)
     print(json.dumps({"objective": o, "ms": round(1e3 * min(ts), 3), "index": r["plan_index"], **st}), flush=True)
+    tr = loom.bfs_trace()
+    print("   trace", round(tr["total_us"] or 0, 1), [(round(l["us"], 1), l["parents"], "R" if l["redundant"] else "D")
+                                               for l in tr["levels"]], flush=True)
     dp.close()
 print(os.environ.get("LOOM_B200_LIB", "default"), "total ms", round(1e3 * tot, 3))
