@@ -345,7 +345,7 @@ typedef struct loom_estimate_streams {
 int loom_estimate_range(loom_ctx* ctx, const loom_problem* problem, uint64_t begin, uint64_t end,
                         const loom_estimate_streams* out);
 /* Same into DEVICE arrays on the ctx's device, enqueued on the ctx stream
- * without synchronising (16-byte aligned arrays leave through TMA bulk stores). */
+ * without synchronising (each warp stores whole aligned 32-element windows). */
 int loom_estimate_range_device(loom_ctx* ctx, const loom_problem* problem, uint64_t begin, uint64_t end,
                                const loom_estimate_streams* out);
 /* Batched estimate of arbitrary plans: element i =

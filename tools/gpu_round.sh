@@ -13,8 +13,9 @@ tail -c 3000 gpurun_out/bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-configs \
   > gpurun_out/bench_ncu.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:bnb_kernel -s 1 -c 1 \
-  -o gpurun_out/bnb_full -f python tools/prof_bnb.py > gpurun_out/ncu_bnb.log 2>&1
-ncu -i gpurun_out/bnb_full.ncu-rep --page raw --csv > gpurun_out/bnb_raw.csv 2>/dev/null
-ncu -i gpurun_out/bnb_full.ncu-rep --page source --csv > gpurun_out/bnb_source.csv 2>/dev/null
+K=${KERNEL:-bfs_kernel}
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:$K -s 1 -c 1 \
+  -o gpurun_out/${K}_full -f python tools/prof_bnb.py > gpurun_out/ncu_$K.log 2>&1
+ncu -i gpurun_out/${K}_full.ncu-rep --page raw --csv > gpurun_out/${K}_raw.csv 2>/dev/null
+ncu -i gpurun_out/${K}_full.ncu-rep --page source --csv --print-source sass > gpurun_out/${K}_sass.csv 2>/dev/null
 ls -la gpurun_out
