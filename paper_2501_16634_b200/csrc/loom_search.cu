@@ -1253,7 +1253,7 @@ __global__ void __launch_bounds__(kBlock, PT ? LOOM_PT_CTAS : 512 / kBlock)
 using KernelFn = void (*)(const uint8_t*, const JobDesc*, int, Rec*, JobSync*, Rec*, InnerParams);
 
 #include "bnb.cuh"
-#include "bfs.cuh"
+#include "frontier.cuh"
 
 
 // pt: the innermost table comes from the kernel parameter (single-problem
@@ -2234,6 +2234,10 @@ JobDesc make_desc(const Built& b, uint64_t begin, uint64_t end, bool full_eval_o
 // context + C ABI
 // ---------------------------------------------------------------------------
 
+namespace {
+struct FrPlan;
+}
+
 struct loom_device_problem {
   loom_ctx* ctx = nullptr;
   Built built;
@@ -2254,7 +2258,9 @@ struct loom_device_problem {
   cudaEvent_t done = nullptr;
   BnbSync* d_bsync = nullptr;
   int bnb_ctas = 0;  // 0: the image does not fit the branch-and-bound kernel
-  int bfs_ctas = 0;  // 0: no frontier search for this problem
+  FrPlan* fr = nullptr;  // frontier search plan (variant 0: none)
+  JobDesc last_job;      // the JobDesc d_job holds
+  bool job_valid = false;
 };
 
 namespace {
@@ -2312,18 +2318,18 @@ int bnb_ctas_for(const loom_ctx* c, size_t blob, int n) {
   return c->sms * nb;
 }
 
-// Frontier search (bfs.cuh): shared memory = problem image + one column of
-// finish times per thread; one cooperative wave of CTAs.
-size_t bfs_smem_bytes(size_t blob, int n) {
-  return ((blob + 127) & ~size_t(127)) + sizeof(int64_t) * kBfsBlock * n + 2 * sizeof(FrontierEntry) * kBfsBlock;
+// ---------------------------------------------------------------------------
+// Frontier search (frontier.cuh): host-built parameters and the launch.
+// ---------------------------------------------------------------------------
+size_t fr_smem_bytes(size_t blob) {
+  static_assert(kFrStage * kFrWarps <= kFrSmall, "per-warp staging lives in the sparse-children slots");
+  return ((blob + 127) & ~size_t(127)) + 2 * sizeof(FrontierEntry) * kFrSmall + sizeof(FrPar) * kFrBlock;
 }
-
-bool bfs_usable(const Built& b, int n) { return n >= 1 && b.bfs_bits <= 64 && !b.blob.empty(); }
 
 size_t bfs_cap_entries() {
   static const size_t cap = [] {
     const char* e = std::getenv("LOOM_BFS_CAP");
-    return e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : (size_t(1) << 23);  // 8M entries x 32 B x 2
+    return e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : (size_t(1) << 23);  // 8M entries x 48 B x 2
   }();
   return cap;
 }
@@ -2340,40 +2346,258 @@ int ensure_bfs(loom_ctx* c) {
   return LOOM_OK;
 }
 
-// CTAs of one co-resident wave of bfs_kernel (0: it does not fit).
-int bfs_ctas_for(const loom_ctx* c, size_t blob, int n) {
-  const size_t smem = bfs_smem_bytes(blob, n);
-  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(bfs_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem)) != cudaSuccess) {
+// Directed rounding on the host, exact: the rounding error of a sum (TwoSum)
+// or a product (fma) decides whether the nearest result lies above.
+double add_rd(double x, double y) {
+  const double s = x + y;
+  if (!std::isfinite(s)) return s;
+  const double bp = s - x;
+  const double e = (x - (s - bp)) + (y - bp);
+  return e < 0 ? std::nextafter(s, -INFINITY) : s;
+}
+double mul_rd(double x, double y) {
+  const double p = x * y;
+  const double e = std::fma(x, y, -p);
+  return e < 0 ? std::nextafter(p, -INFINITY) : p;
+}
+
+// The exact record of plan `index` (eval_digits restated on the host from the
+// problem image: same folds, same order, llround quantization).
+Rec host_rec(const Built& b, uint64_t index) {
+  const uint8_t* base = b.blob.data();
+  const BlobHeader* h = reinterpret_cast<const BlobHeader*>(base);
+  const int n = h->n_nodes;
+  auto I32 = [&](int off) { return reinterpret_cast<const int32_t*>(base + off); };
+  const int32_t *radix = I32(h->off_radix), *optoff = I32(h->off_optoff), *topo = I32(h->off_topo),
+                *predoff = I32(h->off_predoff), *pred = I32(h->off_pred), *qq = I32(h->off_q);
+  const double* ga = reinterpret_cast<const double*>(base + h->off_ga);
+  const double* gb = reinterpret_cast<const double*>(base + h->off_gb);
+  const int64_t* wall = reinterpret_cast<const int64_t*>(base + h->off_wall);
+  const uint64_t* lexw = reinterpret_cast<const uint64_t*>(base + h->off_lexw);
+  int d[kMaxNodes];
+  uint64_t x = index;
+  for (int i = n - 1; i >= 0; --i) {
+    d[i] = static_cast<int>(x % static_cast<uint64_t>(radix[i]));
+    x /= static_cast<uint64_t>(radix[i]);
+  }
+  double ea = 0.0, eb = 0.0;
+  int32_t qual = INT_MAX;
+  uint64_t lex = 0;
+  for (int i = 0; i < n; ++i) {
+    const int o = optoff[i] + d[i];
+    ea += ga[o];
+    eb += gb[o];
+    qual = std::min(qual, qq[o]);
+    lex += lexw[o];
+  }
+  int64_t fin[kMaxNodes];
+  int64_t lat = 0;
+  for (int t = 0; t < n; ++t) {
+    const int node = topo[t];
+    int64_t st = 0;
+    for (int e = predoff[node]; e < predoff[node + 1]; ++e) st = std::max(st, fin[pred[e]]);
+    fin[node] = st + wall[optoff[node] + d[node]];
+    lat = std::max(lat, fin[node]);
+  }
+  Rec r{0, 0, lat, lex, index, qual, lat <= h->slo_eff ? 1 : 0};
+  if (r.found) {
+    r.qa = static_cast<int64_t>(std::llround(ea * 1e9));
+    r.qb = static_cast<int64_t>(std::llround(eb * 1e9));
+  }
+  return r;
+}
+
+// Which instantiation a problem takes: <16, int32> when it has at most 16
+// nodes and every latency stays below 2^30 us, else <32, int64>.  0: the
+// frontier search does not apply (packed digits over 64 bits, or an image too
+// large for shared memory next to the frontier slots).
+struct FrPlan {
+  int variant = 0;
+  int cl = 0;  // compile-time criteria list (fr_crit) or 0
+  int ctas = 0;
+  BfsParams<16> p16;
+  BfsParams<32> p32;
+};
+
+const void* fr_fn(int variant, int cl) {
+  if (variant == 2) return reinterpret_cast<const void*>(bfs_kernel<32, int64_t, 0>);
+  switch (cl) {
+    case 1: return reinterpret_cast<const void*>(bfs_kernel<16, int32_t, 1>);
+    case 2: return reinterpret_cast<const void*>(bfs_kernel<16, int32_t, 2>);
+    case 3: return reinterpret_cast<const void*>(bfs_kernel<16, int32_t, 3>);
+    default: return reinterpret_cast<const void*>(bfs_kernel<16, int32_t, 0>);
+  }
+}
+
+// The compile-time criteria list (fr_crit) a blob's objective matches, or 0.
+int fr_crit_list(const BlobHeader* h) {
+  auto is = [&](std::initializer_list<int> l) {
+    if (static_cast<int>(l.size()) != h->n_crit) return false;
+    int i = 0;
+    for (int c : l)
+      if (h->crit[i++] != c) return false;
+    return true;
+  };
+  if (is({kFpA, kLat})) return 1;
+  if (is({kLat, kFpA})) return 2;
+  if (is({kQual, kFpA, kLat})) return 3;
+  return 0;
+}
+
+template <int NB>
+void fill_fr_params(const Built& b, BfsParams<NB>& P) {
+  const uint8_t* base = b.blob.data();
+  const BlobHeader* h = reinterpret_cast<const BlobHeader*>(base);
+  const int n = h->n_nodes;
+  auto I32 = [&](int off) { return reinterpret_cast<const int32_t*>(base + off); };
+  const int32_t *radix = I32(h->off_radix), *optoff = I32(h->off_optoff), *topo = I32(h->off_topo),
+                *predoff = I32(h->off_predoff), *pred = I32(h->off_pred), *qq = I32(h->off_q),
+                *perm = I32(h->off_perm), *nok = I32(h->off_nok);
+  const double* ga = reinterpret_cast<const double*>(base + h->off_ga);
+  const double* gb = reinterpret_cast<const double*>(base + h->off_gb);
+  const int64_t* wall = reinterpret_cast<const int64_t*>(base + h->off_wall);
+  const uint64_t* lexw = reinterpret_cast<const uint64_t*>(base + h->off_lexw);
+  const BnbMin* bm = reinterpret_cast<const BnbMin*>(base + h->off_bmin);
+  const uint64_t* rk = reinterpret_cast<const uint64_t*>(base + h->off_rk);
+  std::memset(&P, 0, sizeof P);
+  P.n = n;
+  P.n_crit = h->n_crit;
+  for (int i = 0; i < 4; ++i) P.crit[i] = i < h->n_crit ? h->crit[i] : kFrNone;
+  P.slo_eff = h->slo_eff;
+  for (int t = 0; t < n; ++t) P.pos[topo[t]] = t;
+  int s = 0;
+  for (int i = 0; i < n; ++i) {
+    int bits = 1;
+    while ((int64_t(1) << bits) < radix[i]) ++bits;
+    P.shift[i] = s;
+    P.bits[i] = static_cast<uint32_t>((uint64_t(1) << bits) - 1);
+    s += bits;
+    P.optoff[i] = optoff[i];
+    P.nok[i] = nok[i];
+    P.radix[i] = radix[i];
+  }
+  std::vector<int32_t> oprim(n), owall(n);
+  for (int i = 0; i < n; ++i) {
+    oprim[i] = nok[i] ? perm[optoff[i]] : 0;  // exploration order's first: best on the primary criterion
+    owall[i] = nok[i] ? bm[i].o_wall : 0;
+    const int kp = optoff[i] + oprim[i], kw = optoff[i] + owall[i];
+    P.pa[i] = ga[kp];
+    P.pb[i] = gb[kp];
+    P.pq[i] = qq[kp];
+    P.wa[i] = ga[kw];
+    P.wb[i] = gb[kw];
+    P.wq[i] = qq[kw];
+  }
+  for (int t = 0; t < n; ++t) {
+    const int x = topo[t];
+    P.tnode[t] = x;
+    for (int e = predoff[x]; e < predoff[x + 1]; ++e) {
+      const int pp = P.pos[pred[e]];
+      P.pmask[t] |= 1u << pp;
+      P.smask[pp] |= 1u << t;
+    }
+    P.tshift[t] = P.shift[x];
+    P.tbits[t] = P.bits[x];
+    P.toptoff[t] = optoff[x];
+    P.twmin[t] = nok[x] ? bm[x].w : 0;
+    P.twprim[t] = wall[optoff[x] + oprim[x]];
+  }
+  uint64_t lp = 0, lw = 0, ip = 0, iw = 0;
+  double sa = 0.0, sb = 0.0, fac = 1.0;
+  int32_t sq = INT_MAX;
+  uint64_t sl = 0;
+  for (int k = n; k >= 0; --k) {
+    if (k < n) {
+      lp += lexw[optoff[k] + oprim[k]];
+      lw += lexw[optoff[k] + owall[k]];
+      ip += static_cast<uint64_t>(oprim[k]) * rk[k + 1];
+      iw += static_cast<uint64_t>(owall[k]) * rk[k + 1];
+      sa = add_rd(sa, bm[k].a);  // (any order: a lower bound of the exact sum; BnbSuf, bnb.cuh)
+      sb = add_rd(sb, bm[k].b);
+      fac = mul_rd(fac, 1.0 - 0x1.0p-53);
+      sq = std::min(sq, bm[k].q);
+      sl += bm[k].lex;
+    }
+    P.lexp_suf[k] = lp;
+    P.lexw_suf[k] = lw;
+    P.idxp_suf[k] = ip;
+    P.idxw_suf[k] = iw;
+    P.rk[k] = rk[k];
+    P.suf[k] = BnbSuf{sa, sb, fac, sl, sq, 0};
+  }
+}
+
+template <int NB>
+void set_fr_job(const Built& b, const JobDesc& d, BfsParams<NB>& P) {
+  P.begin = d.begin;
+  P.end = d.end;
+  P.ranged = d.begin > 0 || d.end < b.total;
+  P.has_seed = d.has_seed != 0;
+  P.seed = d.has_seed ? host_rec(b, d.seed) : Rec{0, 0, 0, 0, 0, 0, 0};
+}
+
+// Plan the frontier search of a built problem (variant 0: not applicable).
+int prepare_fr(const loom_ctx* c, const Built& b, FrPlan& f) {
+  f.variant = 0;
+  f.ctas = 0;
+  if (b.blob.empty() || b.bfs_bits > 64) return LOOM_OK;
+  const BlobHeader* h = reinterpret_cast<const BlobHeader*>(b.blob.data());
+  const int n = h->n_nodes;
+  if (n < 1) return LOOM_OK;
+  // largest latency of a plan of floor-passing options
+  const int32_t* optoff = reinterpret_cast<const int32_t*>(b.blob.data() + h->off_optoff);
+  const int32_t* perm = reinterpret_cast<const int32_t*>(b.blob.data() + h->off_perm);
+  const int32_t* nok = reinterpret_cast<const int32_t*>(b.blob.data() + h->off_nok);
+  const int64_t* wall = reinterpret_cast<const int64_t*>(b.blob.data() + h->off_wall);
+  int64_t wsum = 0;
+  for (int i = 0; i < n; ++i) {
+    int64_t m = 0;
+    for (int j = 0; j < nok[i]; ++j) m = std::max(m, wall[optoff[i] + perm[optoff[i] + j]]);
+    wsum += m;
+  }
+  const int variant = n <= 16 && wsum < (int64_t(1) << 30) ? 1 : 2;
+  const int cl = variant == 1 ? fr_crit_list(h) : 0;
+  const size_t smem = fr_smem_bytes(b.blob.size());
+  const void* fn = fr_fn(variant, cl);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
     cudaGetLastError();
-    return 0;
+    return LOOM_OK;
   }
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(bfs_kernel), kBfsBlock, smem) !=
-          cudaSuccess ||
-      nb < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kFrBlock, smem) != cudaSuccess || nb < 1) {
     cudaGetLastError();
-    return 0;
+    return LOOM_OK;
   }
-#ifdef LOOM_BFS_CTAS_PER_SM
-  nb = std::min(nb, LOOM_BFS_CTAS_PER_SM);
-#endif
-  return c->sms * nb;
+  f.variant = variant;
+  f.cl = cl;
+  f.ctas = c->sms * std::min(nb, 1);
+  if (variant == 1) fill_fr_params(b, f.p16);
+  else fill_fr_params(b, f.p32);
+  return LOOM_OK;
 }
 
 // Which search the last default launch started with (loom_bnb_last_stats).
 std::atomic<int> g_last_default_bfs{0};
 
-int launch_bfs(loom_ctx* c, int ctas, const uint8_t* d_blob, size_t blob_bytes, int n, const JobDesc* d_job,
-               Rec* d_slots, JobSync* d_ticket, Rec* d_out) {
+int launch_fr(loom_ctx* c, FrPlan& f, const Built& b, const JobDesc& d, const uint8_t* d_blob, Rec* d_slots,
+              JobSync* d_ticket, Rec* d_out) {
   if (int rc = ensure_bfs(c)) return rc;
   FrontierEntry* b0 = c->d_front;
   FrontierEntry* b1 = c->d_front + c->front_cap;
   uint64_t cap = c->front_cap;
   BfsSync* bs = c->d_bfs;
-  void* args[] = {&d_blob, &d_job, &bs, &b0, &b1, &cap, &d_slots, &d_ticket, &d_out};
-  LOOM_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bfs_kernel), dim3(ctas), dim3(kBfsBlock), args,
-                                        bfs_smem_bytes(blob_bytes, n), c->stream));
+  uint32_t bytes = static_cast<uint32_t>(b.blob.size());
+  void* pp;
+  if (f.variant == 1) {
+    set_fr_job(b, d, f.p16);
+    pp = &f.p16;
+  } else {
+    set_fr_job(b, d, f.p32);
+    pp = &f.p32;
+  }
+  void* args[] = {&d_blob, &bytes, &bs, &b0, &b1, &cap, &d_slots, &d_ticket, &d_out, pp};
+  LOOM_CUDA(cudaLaunchCooperativeKernel(fr_fn(f.variant, f.cl), dim3(f.ctas), dim3(kFrBlock), args,
+                                        fr_smem_bytes(b.blob.size()), c->stream));
   ++c->launches;
   g_last_default_bfs = 1;
   return LOOM_OK;
@@ -2579,6 +2803,14 @@ int loom_search_argmin_algo_async(loom_ctx* c, loom_device_problem* dp, uint64_t
   return search_async_impl(c, dp, begin, end, incumbent == UINT64_MAX - 1 ? kNoIncumbent : incumbent, algo);
 }
 
+// Experiment builds (LOOM_FR_PROF=1): the frontier kernel's phase marks.
+int loom_debug_fr_prof(uint64_t* out, int32_t cap) {
+  uint64_t buf[8 * (kMaxNodes + 1)];
+  if (!out || cudaMemcpyFromSymbol(buf, g_fr_prof, sizeof buf) != cudaSuccess) return LOOM_DEVICE_ERROR;
+  for (int i = 0; i < cap && i < 8 * (kMaxNodes + 1); ++i) out[i] = buf[i];
+  return LOOM_OK;
+}
+
 int loom_bfs_trace(uint64_t* out, int32_t cap) {
   if (!out || cap < 2) return LOOM_INVALID;
   uint64_t buf[2 * (kMaxNodes + 2)];
@@ -2645,11 +2877,10 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  const int fctas = algo == kAlgoAuto && bfs_usable(b, p->n_nodes) ? bfs_ctas_for(c, b.blob.size(), p->n_nodes) : 0;
-  if (fctas) {
-    if (int rc = launch_bfs(c, fctas, c->d_arena, b.blob.size(), p->n_nodes, c->d_jobs, c->d_scratch, c->d_tickets,
-                            c->d_out))
-      return rc;
+  FrPlan fr;
+  if (algo == kAlgoAuto) prepare_fr(c, b, fr);
+  if (fr.variant) {
+    if (int rc = launch_fr(c, fr, b, d, c->d_arena, c->d_scratch, c->d_tickets, c->d_out)) return rc;
   } else if (algo == kAlgoAuto) {
     g_last_default_bfs = 0;
   }
@@ -2846,10 +3077,11 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
   const int ctas = c->sms * resident_ctas(dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)));
   dp->ctas = ctas;
   dp->bnb_ctas = dp->built.blob.empty() ? 0 : bnb_ctas_for(c, dp->built.blob.size(), dp->host.n_nodes);
-  dp->bfs_ctas = bfs_usable(dp->built, dp->host.n_nodes) ? bfs_ctas_for(c, dp->built.blob.size(), dp->host.n_nodes) : 0;
+  dp->fr = new FrPlan;
+  prepare_fr(c, dp->built, *dp->fr);
   bool okk = cudaMalloc(&dp->d_blob, dp->built.blob.size()) == cudaSuccess &&
              cudaMalloc(&dp->d_job, sizeof(JobDesc)) == cudaSuccess &&
-             cudaMalloc(&dp->d_scratch, sizeof(Rec) * std::max({ctas, dp->bnb_ctas, dp->bfs_ctas})) == cudaSuccess &&
+             cudaMalloc(&dp->d_scratch, sizeof(Rec) * std::max({ctas, dp->bnb_ctas, dp->fr->ctas})) == cudaSuccess &&
              cudaMalloc(&dp->d_bsync, sizeof(BnbSync)) == cudaSuccess &&
              cudaMemset(dp->d_bsync, 0, sizeof(BnbSync)) == cudaSuccess &&
              cudaMalloc(&dp->d_ticket, sizeof(JobSync)) == cudaSuccess &&
@@ -2876,6 +3108,7 @@ int loom_problem_release(loom_device_problem* dp) {
   cudaFree(dp->d_out);
   if (dp->h_out) cudaFreeHost(dp->h_out);
   if (dp->done) cudaEventDestroy(dp->done);
+  delete dp->fr;
   delete dp;
   return LOOM_OK;
 }
@@ -2896,11 +3129,13 @@ int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint
   if (d.begin >= d.end) return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: empty range");
   const uint64_t units = (d.sub_hi - d.sub_lo) + (d.head_end - d.begin) + (d.end - d.tail_begin);
   const int ctas = std::min(dp->ctas, ctas_for(c, units, dp->fn, smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built))));
-  LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
-  if (algo == kAlgoAuto && dp->bfs_ctas) {
-    if (int rc = launch_bfs(c, dp->bfs_ctas, dp->d_blob, dp->built.blob.size(), dp->host.n_nodes, dp->d_job,
-                            dp->d_scratch, dp->d_ticket, dp->d_out))
-      return rc;
+  if (!dp->job_valid || std::memcmp(&dp->last_job, &d, sizeof d) != 0) {  // the device copy is still current otherwise
+    dp->last_job = d;
+    dp->job_valid = true;
+    LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &dp->last_job, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  }
+  if (algo == kAlgoAuto && dp->fr->variant) {
+    if (int rc = launch_fr(c, *dp->fr, dp->built, d, dp->d_blob, dp->d_scratch, dp->d_ticket, dp->d_out)) return rc;
   } else if (algo == kAlgoAuto) {
     g_last_default_bfs = 0;
   }

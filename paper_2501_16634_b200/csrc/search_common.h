@@ -171,40 +171,35 @@ struct alignas(128) BnbSync {
 };
 
 // Per-job state of the frontier (level-synchronous) branch and bound
-// (bfs.cuh), zero between launches: survivors per depth, the grid barrier,
-// the job's incumbent under a lock, and launch evidence.
+// (frontier.cuh), zero between launches (the last CTA to finish resets it):
+// survivors per depth, parents handed out per depth, the grid barrier, the
+// exit ticket and launch evidence.
 struct alignas(128) BfsSync {
   unsigned long long count[kMaxNodes + 1];  // frontier entries per depth
   unsigned long long next[kMaxNodes + 1];   // parents handed out per depth (dynamic distribution)
   unsigned bar_count;
   unsigned bar_gen;
-  unsigned lock;
+  unsigned ticket;   // CTA exits: the last one writes the result and resets
   unsigned overflow;
   unsigned long long evals;   // children evaluated (subtree bounds + leaves)
   unsigned long long leaves;  // complete plans evaluated exactly
   unsigned long long max_frontier;
   unsigned long long pad;
-  Rec best;
 };
 
-// One surviving prefix of the frontier (64 bytes): its digits bit-packed
-// (node i at BfsShared.shift[i]), the exact dag-order folds of its FP terms,
-// its bound on the first criterion, the latency terms of the next node and
-// the minimum quality of its nodes.
+// One surviving prefix of the frontier (48 bytes): its digits bit-packed
+// (node i at BfsParams.shift[i]), the exact dag-order folds of its FP terms,
+// its bound on the first criterion and the minimum quality of its nodes.
+// The latency terms of the next node are computed when the prefix is
+// expanded (frontier.cuh), not stored.
 struct alignas(16) FrontierEntry {
   uint64_t dig;
   double fa;
   double fb;
   int64_t key;  // the prefix's bound on the first criterion (larger = worse), re-checked before expanding
-  // Latency of the next node x to fix (the prefix's depth), with the other
-  // free nodes at their smallest walls: any path avoids x (at most `lnot`) or
-  // runs through it (`head` + wall(x) + `tail`), so a child's latency bound
-  // is max(lnot, head + wall + tail) -- exact at the leaves.
-  int64_t lnot;
-  int64_t head;
-  int64_t tail;
   int32_t q;
-  int32_t pad;
+  int32_t live;  // 0: a dropped child slot of a redundant level (frontier.cuh)
+  uint64_t pad;
 };
 
 // Per-job launch descriptor (global memory).
