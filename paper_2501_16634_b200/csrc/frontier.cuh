@@ -48,9 +48,11 @@
 // arrive as a __grid_constant__ kernel parameter built on the host.  A
 // frontier that outgrows its buffer sets `overflow`: the job's best so far
 // goes to out[0], JobSync.pad = kBfsOverflow, and the depth-first kernel
-// (bnb.cuh) that follows on the stream takes over from that incumbent (then
-// the sweep, if it too runs out of budget).  Otherwise JobSync.pad = kBnbDone
-// and both follow-up launches retire at once.
+// (bnb.cuh) that follows takes over from that incumbent (then the sweep, if
+// it too runs out of budget).  Launched in a plain stream, both follow-up
+// launches otherwise retire at once (JobSync.pad = kBnbDone); inside the
+// search graph of a device problem they sit behind a conditional node that
+// this kernel sets only on overflow (cudaGraphSetConditional).
 
 __device__ unsigned long long g_bfs_last[6];  // evidence of the last frontier launch
 // Per-level trace of the last launch (CTA 0): [0] start, [1] end, [2d+2] =
@@ -64,6 +66,11 @@ __device__ unsigned long long g_bfs_trace[2 * (kMaxNodes + 2)];
 #define LOOM_FR_PROF 0
 #endif
 __device__ unsigned long long g_fr_prof[8 * (kMaxNodes + 1)];
+__device__ unsigned long long g_fr_prof2[16];  // LOOM_FR_PROF=3: marks inside an expansion (depth 3, lane 0)
+#define FR_MARK2(i)                                                                                   \
+  do {                                                                                                \
+    if (LOOM_FR_PROF == 3 && blockIdx.x == 0 && threadIdx.x == 0 && k == 3) g_fr_prof2[i] = clock64(); \
+  } while (0)
 #define FR_MARK(d, i)                                                                                   \
   do {                                                                                                  \
     if (LOOM_FR_PROF && blockIdx.x == 0 && threadIdx.x == 0) g_fr_prof[8 * (d) + (i)] = clock64();     \
@@ -98,8 +105,12 @@ struct BfsParams {
   Rec seed;  // the incumbent every CTA starts from (exact record, host-evaluated)
   // by topological position t
   int32_t tnode[NB];    // node at position t
-  uint32_t pmask[NB];   // predecessors of position t (bit = position)
-  uint32_t smask[NB];   // successors of position t
+  // pm[t][p] = ~0 if position p precedes position t by an edge, else 0;
+  // sm[t][s] likewise for successors.  Indexed by compile-time constants
+  // after unrolling, so every mask is an instruction operand from the
+  // parameter bank (no load, no branch): F[t] = W[t] + max_p (F[p] & pm[t][p]).
+  uint32_t pm[NB][NB];
+  uint32_t sm[NB][NB];
   int32_t tshift[NB];   // digit of node tnode[t]: (dig >> tshift) & tbits
   uint32_t tbits[NB];
   int32_t toptoff[NB];
@@ -289,6 +300,11 @@ __device__ __forceinline__ void fr_offer(const BfsParams<NB>& P, const FrTab& T,
 // one lane runs them in turn.  L: int32_t when every latency stays below
 // 2^30 us (host-checked), else int64_t.
 template <int CL, int NB, typename L>
+__device__ __forceinline__ L fr_mask(L v, uint32_t m) {
+  return v & static_cast<L>(static_cast<int32_t>(m));  // m is 0 or ~0: sign-extends to 0 or all ones
+}
+
+template <int CL, int NB, typename L>
 __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, const FrontierEntry& e, int k, int job,
                                        FrPar& out, Rec& cand) {
   constexpr L kGone = -(L(1) << (sizeof(L) * 8 - 2));  // a removed node: paths through it never win a max
@@ -297,44 +313,48 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
   // the FP folds of a completion continue in dag order (estimator.hpp:50-60)
   double a = e.fa, b = e.fb;
   int32_t q = e.q;
-  if (job != 0) {
+  if (job != 0) {  // lanes of jobs 1 and 2 run the same instructions (operands selected per lane)
+    const bool pj = job == 1;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       if (i >= n) break;
       if (i >= k) {
-        a = __dadd_rn(a, job == 1 ? P.pa[i] : P.wa[i]);
-        b = __dadd_rn(b, job == 1 ? P.pb[i] : P.wb[i]);
-        q = min(q, job == 1 ? P.pq[i] : P.wq[i]);
+        const double ta = P.pa[i], tb = P.pb[i], wa = P.wa[i], wb = P.wb[i];
+        const int32_t tq = P.pq[i], wq = P.wq[i];
+        a = __dadd_rn(a, pj ? ta : wa);
+        b = __dadd_rn(b, pj ? tb : wb);
+        q = min(q, pj ? tq : wq);
       }
     }
-    if (job == 1 && fr_worse_before_lat<CL>(P, quantize_dev(a), quantize_dev(b), q, cand)) return;
+    if (pj && fr_worse_before_lat<CL>(P, quantize_dev(a), quantize_dev(b), q, cand)) return;
   }
+  FR_MARK2(1);
+  const bool prim = job == 1;
   L W[NB];
 #pragma unroll
   for (int t = 0; t < NB; ++t) {
     if (t >= n) break;
-    W[t] = static_cast<L>(job == 1 ? P.twprim[t] : P.twmin[t]);
+    W[t] = static_cast<L>(prim ? P.twprim[t] : P.twmin[t]);
     if (P.tnode[t] < k)
       W[t] = static_cast<L>(T.wall[P.toptoff[t] + static_cast<int>((e.dig >> P.tshift[t]) & P.tbits[t])]);
   }
+  FR_MARK2(2);
   // forward; job 0 removes node k
   L F[NB];
   L lmax = 0, head = 0;
+  const bool rm = job == 0;
 #pragma unroll
   for (int t = 0; t < NB; ++t) {
     if (t >= n) break;
     L st = 0;
 #pragma unroll
-    for (int p = 0; p < t; ++p)
-      if ((P.pmask[t] >> p) & 1u) st = max(st, F[p]);
-    if (job == 0 && t == xpos) {
-      head = st;
-      F[t] = kGone;
-    } else {
-      F[t] = st + W[t];
-      lmax = max(lmax, F[t]);
-    }
+    for (int p = 0; p < t; ++p) st = max(st, fr_mask<CL, NB, L>(F[p], P.pm[t][p]));
+    const bool x = rm && t == xpos;
+    head = x ? st : head;
+    F[t] = x ? kGone : st + W[t];
+    lmax = max(lmax, F[t]);
   }
+  FR_MARK2(3);
   if (job != 0) {
     fr_offer<CL>(P, T, e.dig, k, job, a, b, q, static_cast<int64_t>(lmax), cand);
     return;
@@ -345,16 +365,15 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
     if (t < n && t > xpos) {
       L m = 0;
 #pragma unroll
-      for (int s = t + 1; s < NB; ++s)
-        if ((P.smask[t] >> s) & 1u) m = max(m, F[s]);
+      for (int s2 = t + 1; s2 < NB; ++s2) m = max(m, fr_mask<CL, NB, L>(F[s2], P.sm[t][s2]));
       F[t] = m + W[t];
     }
   }
+  FR_MARK2(4);
   L tail = 0;
-  const uint32_t sx = P.smask[xpos];
 #pragma unroll
-  for (int s = 1; s < NB; ++s)
-    if (s > xpos && s < n && ((sx >> s) & 1u)) tail = max(tail, F[s]);
+  for (int s2 = 1; s2 < NB; ++s2)
+    if (s2 > xpos && s2 < n) tail = max(tail, fr_mask<CL, NB, L>(F[s2], P.sm[xpos][s2]));
   out.dig = e.dig;
   out.fa = e.fa;
   out.fb = e.fb;
@@ -363,6 +382,7 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
   out.head = head;
   out.tail = tail;
   out.live = 1;
+  FR_MARK2(5);
 }
 
 // Phase B: child `slot` (exploration rank) of parent `par` at depth d.  A
@@ -525,6 +545,7 @@ __device__ __forceinline__ void fr_batch(const BfsParams<NB>& P, const FrTab& T,
                                          uint64_t p0, int np, int d, bool leaf, bool redundant, unsigned magic, FrPar* pb, Rec& cand,
                                          FrOut& o, unsigned long long& evals, unsigned long long& leaves) {
   const int lane = threadIdx.x & 31;
+  { const int k = d; FR_MARK2(0); }
   const Rec before = cand;
   // a small batch gives each parent three lanes (one job each), else one
   const bool split = np * 3 <= 32;
@@ -540,9 +561,15 @@ __device__ __forceinline__ void fr_batch(const BfsParams<NB>& P, const FrTab& T,
     if (e.live && e.key <= fr_bound_key<CL>(P, cand)) {
 #pragma unroll 1
       for (int j = j0; j <= j1; ++j) fr_job<CL, NB, L>(P, T, e, d, j, fp, cand);
+      if (LOOM_FR_PROF == 2) {  // experiment: the same work again, warm (instruction cache)
+        FR_MARK(d, 7);
+#pragma unroll 1
+        for (int j = j0; j <= j1; ++j) fr_job<CL, NB, L>(P, T, e, d, j, fp, cand);
+      }
     }
   }
   FR_MARK(d, 1);
+  { const int k = d; FR_MARK2(6); }
   if (j0 == 0 && pl < 32) pb[pl] = fp;
   // plans found while expanding prune the children of the whole warp
   if (__any_sync(0xffffffffu, cand.index != before.index || cand.found != before.found)) fr_warp_best<CL>(P, cand);
@@ -587,7 +614,7 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     bfs_kernel(const uint8_t* __restrict__ blob, uint32_t blob_bytes, BfsSync* __restrict__ bs,
                FrontierEntry* __restrict__ buf0, FrontierEntry* __restrict__ buf1, uint64_t cap,
                Rec* __restrict__ slots, JobSync* __restrict__ sync, Rec* __restrict__ out,
-               const __grid_constant__ BfsParams<NB> P) {
+               cudaGraphConditionalHandle fallback, int32_t in_graph, const __grid_constant__ BfsParams<NB> P) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ FrShared S;
   load_blob(smem, blob, blob_bytes, &S.mbar);
@@ -775,7 +802,11 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     __threadfence();
     const bool of = __ldcg(&bs->overflow) != 0u;
     out[0] = S.best;
-    sync[0].pad = of ? kBfsOverflow : kBnbDone;
+    // Inside the search graph the fallback kernels sit behind a conditional
+    // node that runs only on overflow; in a plain stream they always follow
+    // and retire at once on kBnbDone.
+    if (in_graph) cudaGraphSetConditional(fallback, of ? 1u : 0u);
+    sync[0].pad = of ? kBfsOverflow : (in_graph ? 0u : kBnbDone);
     g_bfs_last[0] = __ldcg(&bs->evals);
     g_bfs_last[1] = of;
     g_bfs_last[2] = __ldcg(&bs->max_frontier);

@@ -2417,6 +2417,19 @@ struct FrPlan {
   int ctas = 0;
   BfsParams<16> p16;
   BfsParams<32> p32;
+  // Search graph of a device problem: frontier kernel -> conditional node
+  // {depth-first kernel -> sweep kernel} (taken only on frontier overflow)
+  // -> D2H of the winner.  One graph launch per search instead of three
+  // kernel launches and a copy; rebuilt when the sweep's grid changes.
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t kn = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+  int sweep_ctas = -1;
+  ~FrPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
 };
 
 const void* fr_fn(int variant, int cl) {
@@ -2493,8 +2506,8 @@ void fill_fr_params(const Built& b, BfsParams<NB>& P) {
     P.tnode[t] = x;
     for (int e = predoff[x]; e < predoff[x + 1]; ++e) {
       const int pp = P.pos[pred[e]];
-      P.pmask[t] |= 1u << pp;
-      P.smask[pp] |= 1u << t;
+      P.pm[t][pp] = ~0u;
+      P.sm[pp][t] = ~0u;
     }
     P.tshift[t] = P.shift[x];
     P.tbits[t] = P.bits[x];
@@ -2579,6 +2592,28 @@ int prepare_fr(const loom_ctx* c, const Built& b, FrPlan& f) {
 // Which search the last default launch started with (loom_bnb_last_stats).
 std::atomic<int> g_last_default_bfs{0};
 
+// Kernel arguments of the frontier kernel, in its parameter order.
+struct FrArgs {
+  const uint8_t* blob;
+  uint32_t bytes;
+  BfsSync* bs;
+  FrontierEntry* b0;
+  FrontierEntry* b1;
+  uint64_t cap;
+  Rec* slots;
+  JobSync* ticket;
+  Rec* out;
+  cudaGraphConditionalHandle cond;
+  int32_t in_graph;
+  void* params;
+  void* ptrs[12];
+  void** bind() {
+    void* a[12] = {&blob, &bytes, &bs, &b0, &b1, &cap, &slots, &ticket, &out, &cond, &in_graph, params};
+    for (int i = 0; i < 12; ++i) ptrs[i] = a[i];
+    return ptrs;
+  }
+};
+
 int launch_fr(loom_ctx* c, FrPlan& f, const Built& b, const JobDesc& d, const uint8_t* d_blob, Rec* d_slots,
               JobSync* d_ticket, Rec* d_out) {
   if (int rc = ensure_bfs(c)) return rc;
@@ -2595,7 +2630,9 @@ int launch_fr(loom_ctx* c, FrPlan& f, const Built& b, const JobDesc& d, const ui
     set_fr_job(b, d, f.p32);
     pp = &f.p32;
   }
-  void* args[] = {&d_blob, &bytes, &bs, &b0, &b1, &cap, &d_slots, &d_ticket, &d_out, pp};
+  cudaGraphConditionalHandle none = 0;
+  int32_t in_graph = 0;
+  void* args[] = {&d_blob, &bytes, &bs, &b0, &b1, &cap, &d_slots, &d_ticket, &d_out, &none, &in_graph, pp};
   LOOM_CUDA(cudaLaunchCooperativeKernel(fr_fn(f.variant, f.cl), dim3(f.ctas), dim3(kFrBlock), args,
                                         fr_smem_bytes(b.blob.size()), c->stream));
   ++c->launches;
@@ -2809,6 +2846,11 @@ int loom_debug_fr_prof(uint64_t* out, int32_t cap) {
   if (!out || cudaMemcpyFromSymbol(buf, g_fr_prof, sizeof buf) != cudaSuccess) return LOOM_DEVICE_ERROR;
   for (int i = 0; i < cap && i < 8 * (kMaxNodes + 1); ++i) out[i] = buf[i];
   return LOOM_OK;
+}
+
+int loom_debug_fr_prof2(uint64_t* out) {
+  return out && cudaMemcpyFromSymbol(out, g_fr_prof2, sizeof(uint64_t) * 16) == cudaSuccess ? LOOM_OK
+                                                                                          : LOOM_DEVICE_ERROR;
 }
 
 int loom_bfs_trace(uint64_t* out, int32_t cap) {
@@ -3121,6 +3163,96 @@ uint64_t loom_device_problem_bytes(const loom_device_problem* dp) {
 
 namespace {
 
+// Launch the default search of a device problem as its search graph (see
+// FrPlan), building or rebuilding the graph when needed.
+int fr_graph_launch(loom_ctx* c, loom_device_problem* dp, const JobDesc& d, int sweep_ctas) {
+  FrPlan& f = *dp->fr;
+  if (int rc = ensure_bfs(c)) return rc;
+  FrArgs A{dp->d_blob, static_cast<uint32_t>(dp->built.blob.size()), c->d_bfs, c->d_front, c->d_front + c->front_cap,
+           static_cast<uint64_t>(c->front_cap), dp->d_scratch, dp->d_ticket, dp->d_out, 0, 1, nullptr, {}};
+  if (f.variant == 1) {
+    set_fr_job(dp->built, d, f.p16);
+    A.params = &f.p16;
+  } else {
+    set_fr_job(dp->built, d, f.p32);
+    A.params = &f.p32;
+  }
+  const size_t fsmem = fr_smem_bytes(dp->built.blob.size());
+  if (!f.exec || f.sweep_ctas != sweep_ctas) {
+    if (f.exec) cudaGraphExecDestroy(f.exec);
+    if (f.graph) cudaGraphDestroy(f.graph);
+    f.exec = nullptr;
+    f.graph = nullptr;
+    LOOM_CUDA(cudaGraphCreate(&f.graph, 0));
+    LOOM_CUDA(cudaGraphConditionalHandleCreate(&f.cond, f.graph, 0, cudaGraphCondAssignDefault));
+    A.cond = f.cond;
+    cudaKernelNodeParams kp{};
+    kp.func = const_cast<void*>(fr_fn(f.variant, f.cl));
+    kp.gridDim = dim3(f.ctas);
+    kp.blockDim = dim3(kFrBlock);
+    kp.sharedMemBytes = static_cast<unsigned>(fsmem);
+    kp.kernelParams = A.bind();
+    LOOM_CUDA(cudaGraphAddKernelNode(&f.kn, f.graph, nullptr, 0, &kp));
+    cudaLaunchAttributeValue coop{};
+    coop.cooperative = 1;
+    LOOM_CUDA(cudaGraphKernelNodeSetAttribute(f.kn, cudaLaunchAttributeCooperative, &coop));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = f.cond;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn = nullptr;
+    LOOM_CUDA(cudaGraphAddNode(&cn, f.graph, &f.kn, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    // the fallback: depth first from the frontier's incumbent, then the sweep
+    cudaGraphNode_t b1 = nullptr, b2 = nullptr;
+    const uint8_t* blob = dp->d_blob;
+    const JobDesc* job = dp->d_job;
+    int bctas = dp->bnb_ctas;
+    Rec* scratch = dp->d_scratch;
+    JobSync* ticket = dp->d_ticket;
+    BnbSync* bsync = dp->d_bsync;
+    Rec* out = dp->d_out;
+    int sctas = sweep_ctas;
+    InnerParams ip = dp->built.ip;
+    if (bctas) {
+      void* ba[] = {&blob, &job, &bctas, &scratch, &ticket, &bsync, &out};
+      cudaKernelNodeParams bp{};
+      bp.func = reinterpret_cast<void*>(bnb_kernel);
+      bp.gridDim = dim3(bctas);
+      bp.blockDim = dim3(kBlock);
+      bp.sharedMemBytes = static_cast<unsigned>(bnb_smem_bytes(dp->built.blob.size(), dp->host.n_nodes));
+      bp.kernelParams = ba;
+      LOOM_CUDA(cudaGraphAddKernelNode(&b1, body, nullptr, 0, &bp));
+    }
+    void* sa[] = {&blob, &job, &sctas, &scratch, &ticket, &out, &ip};
+    cudaKernelNodeParams sp{};
+    sp.func = reinterpret_cast<void*>(dp->fn);
+    sp.gridDim = dim3(sweep_ctas);
+    sp.blockDim = dim3(kBlock);
+    sp.sharedMemBytes = static_cast<unsigned>(smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)));
+    sp.kernelParams = sa;
+    LOOM_CUDA(cudaGraphAddKernelNode(&b2, body, b1 ? &b1 : nullptr, b1 ? 1 : 0, &sp));
+    cudaGraphNode_t mn = nullptr;
+    LOOM_CUDA(cudaGraphAddMemcpyNode1D(&mn, f.graph, &cn, 1, dp->h_out, dp->d_out, sizeof(Rec), cudaMemcpyDeviceToHost));
+    LOOM_CUDA(cudaGraphInstantiate(&f.exec, f.graph, 0));
+    f.sweep_ctas = sweep_ctas;
+  } else {  // the same graph, this search's job fields (range, incumbent)
+    A.cond = f.cond;
+    cudaKernelNodeParams kp{};
+    kp.func = const_cast<void*>(fr_fn(f.variant, f.cl));
+    kp.gridDim = dim3(f.ctas);
+    kp.blockDim = dim3(kFrBlock);
+    kp.sharedMemBytes = static_cast<unsigned>(fsmem);
+    kp.kernelParams = A.bind();
+    LOOM_CUDA(cudaGraphExecKernelNodeSetParams(f.exec, f.kn, &kp));
+  }
+  LOOM_CUDA(cudaGraphLaunch(f.exec, c->stream));
+  c->launches += 1;
+  g_last_default_bfs = 1;
+  return LOOM_OK;
+}
+
 int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint64_t end, uint64_t incumbent,
                       int32_t algo) {
   if (!c || !dp) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
@@ -3133,6 +3265,11 @@ int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint
     dp->last_job = d;
     dp->job_valid = true;
     LOOM_CUDA(cudaMemcpyAsync(dp->d_job, &dp->last_job, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  }
+  if (algo == kAlgoAuto && dp->fr->variant && !std::getenv("LOOM_NO_GRAPH")) {
+    if (int rc = fr_graph_launch(c, dp, d, ctas)) return rc;
+    LOOM_CUDA(cudaEventRecord(dp->done, c->stream));
+    return LOOM_OK;
   }
   if (algo == kAlgoAuto && dp->fr->variant) {
     if (int rc = launch_fr(c, *dp->fr, dp->built, d, dp->d_blob, dp->d_scratch, dp->d_ticket, dp->d_out)) return rc;

@@ -23,6 +23,8 @@ names = ["startA", "A->warpbest", "->phaseB end", "->batches", "->blockbest", "-
 print(o)
 for d in range(lw.problem.n_nodes):
     m = [buf[8 * d + i] for i in range(8)]
+    if m[7] and m[1] > m[7] > m[0]:  # LOOM_FR_PROF=2: mark 7 = end of the first (cold) expansion
+        print(d, "expand cold", m[7] - m[0], "warm", m[1] - m[7])
     if not m[0]:
         continue
     segs = []
@@ -33,3 +35,9 @@ for d in range(lw.problem.n_nodes):
             prev = m[i]
     nxt = buf[8 * (d + 1)] if d + 1 < 33 else 0
     print(d, " | ".join(segs), "| to next level", (nxt - prev) if nxt > prev else "")
+
+b2 = (C.c_uint64 * 16)()
+if loom.lib().loom_debug_fr_prof2(b2) == 0 and b2[0]:
+    m = list(b2)
+    print("depth-3 expansion, lane 0 (job 0): batch start -> folds", m[1] - m[0], "| W", m[2] - m[1],
+          "| forward", m[3] - m[2], "| backward", m[4] - m[3], "| tail+store", m[5] - m[4], "| warp done", m[6] - m[5])
