@@ -369,21 +369,48 @@ def b200_arm(args) -> None:
         props = torch.cuda.get_device_properties(local)
         sms = props.multi_processor_count
         issue = sms * 4 * 32 * f_mhz * 1e6  # thread-instructions per second
-        # Dominant kernel: bfs_kernel (frontier branch and bound; bnb_kernel if
-        # the depth-first fallback ran).  Its unit of work is one evaluation of a
-        # child of the enumeration tree -- a subtree's criteria bound, or a
-        # leaf's exact record -- which is one plan evaluation with the free
-        # nodes at their minima: SURVEY.md §8(d)'s full-evaluation count
-        # I = 12N + 3E + 20 thread-instructions.
+        # Dominant kernel: bfs_kernel, the frontier branch and bound (the whole
+        # timed step is one graph launch: this kernel, a conditional node that
+        # stays closed unless the frontier overflows, and the 48-byte D2H).
+        # Its duration is read live from the kernel's own %globaltimer trace
+        # (CTA 0's start to the last CTA's exit) over a few extra searches.
+        kern_us, levels = [], None
+        for _ in range(5):
+            search(begin, end)
+            shard_result()
+            tr = loom.bfs_trace()
+            if tr["total_us"]:
+                kern_us.append(tr["total_us"])
+                levels = tr["levels"]
+        kernel_s = statistics.median(kern_us) / 1e6 if kern_us else local_ms / 1e3
         n_nodes, n_edges = lw.problem.n_nodes, lw.problem.n_edges
-        i_eval = 12 * n_nodes + 3 * n_edges + 20
+        i_eval = 12 * n_nodes + 3 * n_edges + 20  # SURVEY.md §8(d) full-evaluation count
         evals = bnb["child_evaluations"]
-        achieved = evals / (local_ms / 1e3)
-        peak = issue / i_eval
-        traffic = None
-        prof = ROOT / "profiles" / "ncu_summary.json"
-        if prof.exists():
-            traffic = json.loads(prof.read_text()).get("bnb_dram_bytes_per_launch")
+        prof_p = ROOT / "profiles" / "ncu_summary.json"
+        prof = json.loads(prof_p.read_text()) if prof_p.exists() else {}
+        fr = prof.get("bfs_kernel", {})
+        inst = fr.get("warp_inst_per_launch")
+        issue_peak = sms * 4 * f_mhz * 1e6  # warp instructions per second (one issue per SMSP per clock)
+        roofline = {
+            "bound": "instruction issue (latency-limited: level-synchronous critical path)",
+            "kernel": "bfs_kernel" if not bnb["depth_first"] else "bnb_kernel",
+            "achieved": inst / kernel_s if inst else None, "peak": issue_peak, "unit": "warp instructions/s",
+            "frac": inst / kernel_s / issue_peak if inst else None,
+            "traffic": fr.get("dram_bytes_per_launch"),
+            "kernel_us": 1e6 * kernel_s,
+            "warp_inst_per_launch": inst,
+            "work": {"unit": "subtree bounds + leaf evaluations (children) per second",
+                     "children_per_launch": evals, "achieved": evals / kernel_s,
+                     "full_evaluation_ceiling": issue * 1.0 / i_eval,
+                     "frac": evals / kernel_s / (issue / i_eval),
+                     "inst_per_evaluation": i_eval},
+            "levels": levels,
+            "note": "achieved = warp instructions of one launch (ncu smsp__inst_executed.sum, profiles/ncu_summary.json) "
+                    "/ the launch's live device time; peak = SMs x 4 SMSPs x measured SM clock.  The kernel is bound "
+                    "by the latency of its per-level critical path (grid barrier + one expansion chain per level, "
+                    "'levels' = per-level device time), not by issue or HBM: 'work' compares the children it "
+                    f"evaluates with the full-evaluation ceiling (12N+3E+20 = {i_eval} thread-instructions each, "
+                    "SURVEY.md §8d).  traffic = DRAM bytes per launch (ncu)."}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -408,14 +435,7 @@ def b200_arm(args) -> None:
                     "path": "loom_exhaustive_search_json: JSON parse + lowering + H2D + kernel + D2H + decode"
                     if world == 1 else "loom_group_exhaustive_search_json: JSON parse + lowering + per-rank shard "
                     "search (range + greedy incumbent) + ncclAllGather of the rank records + reduce + decode"},
-            "roofline": {"bound": "instruction issue", "kernel": "bnb_kernel" if bnb["depth_first"] else "bfs_kernel", "achieved": achieved, "peak": peak,
-                         "unit": "subtree bounds + leaf evaluations per second per GPU", "frac": achieved / peak,
-                         "traffic": traffic, "evaluations_per_launch": evals,
-                         "inst_per_evaluation": i_eval,
-                         "note": "peak = SMs x 4 SMSPs x 32 lanes x measured SM clock / (12N+3E+20) "
-                                 "thread-instructions per evaluation (SURVEY.md §8d full-evaluation count; "
-                                 f"N={n_nodes}, E={n_edges}); achieved = evaluations of the launch / its "
-                                 "device time; traffic = DRAM bytes per launch (ncu)"},
+            "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk,
         }

@@ -43,7 +43,10 @@ constexpr int kBnbTasksPerWarp = 64;
 // Evidence of the last launch's job 0: child evaluations and the abort flag
 // (loom_bnb_last_stats).
 __device__ unsigned long long g_bnb_last[6];
-__device__ unsigned long long g_bnb_acc[2];  // running: max expansions of one task, tasks alive at the root
+__device__ unsigned long long g_bnb_acc[2];
+// Test knob (LOOM_BNB_BUDGET, read at context creation): a fixed evaluation
+// budget, so tests can drive the depth-first search into its sweep fallback.
+__device__ unsigned long long g_bnb_budget;  // running: max expansions of one task, tasks alive at the root
 
 // Bounds of the free nodes below a child of node k (nodes k+1 .. n-1), per
 // CTA.  FP sums: the fold of a child's prefix continued with the free
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(kBlock)
   while (!empty && T < n - 1 && n_tasks < tpw * warps) n_tasks *= static_cast<uint64_t>(B.nok[T++]);
   if (empty) n_tasks = 0;
   const bool ranged = jd.begin > 0 || jd.end < h->total;
-  const uint64_t budget = max(h->total / 64, static_cast<uint64_t>(1) << 16);
+  const uint64_t budget = g_bnb_budget ? g_bnb_budget : max(h->total / 64, static_cast<uint64_t>(1) << 16);
   uint64_t work_local = 0, leaf_local = 0;
   unsigned steps = 0;
   bool aborted = false;

@@ -457,6 +457,15 @@ int loom_greedy_search_json(loom_ctx* ctx, const char* dag_json, const char* lib
                             const char* bounds_json, int32_t max_sweeps, char* out_json, size_t cap, size_t* needed) {
   int rc = LOOM_OK;
   std::string result;
+  const bool trace = std::getenv("LOOM_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[loom trace] exhaustive_json %s %.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  };
   try {
     const loom::WorkflowDag dag = loom::WorkflowDag::from_json_text(dag_json ? dag_json : "");
     const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json ? library_json : "");
@@ -798,17 +807,29 @@ int exhaustive_json(const SearchFn& search, const char* dag_json, const char* li
                     size_t* needed) {
   int rc = LOOM_OK;
   std::string result;
+  const bool trace = std::getenv("LOOM_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[loom trace] exhaustive_json %s %.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  };
   try {
     const loom::WorkflowDag dag = loom::WorkflowDag::from_json_text(dag_json ? dag_json : "");
     const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json ? library_json : "");
     const loom::SearchBounds bounds = loom::SearchBounds::from_json_text(bounds_json ? bounds_json : "{}");
     const ParsedObjective obj = parse_objective_json(objective_json ? objective_json : "");
+    mark("parse");
     const loom::LoweredProblem L = loom::lower(dag, lib, bounds);
     if (L.total == 0) throw loom::NoFeasibleConfigError("no configuration satisfies the quality floor and bounds");
     const loom_problem view = L.view();
     const loom_objective o = to_objective(obj.hierarchy, obj.slo);
+    mark("lower");
     loom_winner w;
     rc = search(&view, &o, L.total, &w);
+    mark("search");
     if (rc == LOOM_OK) {
       const loom::ConfigEstimate e = loom::estimate(L.config_of(w.plan_index), dag, lib);
       if (e.latency_us != w.latency_us || e.gpu_wh != w.gpu_wh || e.dollars != w.dollars)
@@ -817,6 +838,7 @@ int exhaustive_json(const SearchFn& search, const char* dag_json, const char* li
         result = estimate_json(e, w.plan_index, L.total);
     }
     if (rc != LOOM_OK) result = error_json(loom_last_error());
+    mark("estimate + json");
   } catch (const loom::Error& e) {
     rc = loomi::fail(status_of(e), e.what());
     result = error_json(e.what());

@@ -49,6 +49,7 @@
 #include <mutex>
 #include <queue>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "internal.h"
@@ -2301,21 +2302,54 @@ int ensure_bsync(loom_ctx* c, size_t need) {
 
 // CTAs of one full wave of the branch-and-bound kernel at this image size
 // (0 when its shared memory does not fit: the sweep alone then searches).
-int bnb_ctas_for(const loom_ctx* c, size_t blob, int n) {
-  const size_t smem = bnb_smem_bytes(blob, n);
-  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(bnb_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem)) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
+// Occupancy queries and shared-memory attributes are driver calls of a few
+// microseconds each, and a one-shot search makes several; both are cached
+// per (device, kernel, dynamic shared memory).  An attribute already set to
+// at least the requested size is not set again.
+std::mutex g_occ_mu;
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+std::map<std::pair<int, const void*>, size_t> g_smem_set;
+
+cudaError_t smem_attr(const void* fn, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    auto it = g_smem_set.find({dev, fn});
+    if (it != g_smem_set.end() && it->second >= smem) return cudaSuccess;
+  }
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    size_t& v = g_smem_set[{dev, fn}];
+    v = std::max(v, smem);
+  }
+  return e;
+}
+
+// Resident blocks per SM (0: does not fit), shared-memory attribute included.
+int blocks_per_sm(const void* fn, int block, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, fn, block, smem);
+  {
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
   }
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(bnb_kernel), kBlock, smem) !=
-          cudaSuccess ||
-      nb < 1) {
+  if (smem_attr(fn, smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, block, smem) != cudaSuccess || nb < 1) {
     cudaGetLastError();
-    return 0;
+    nb = 0;
   }
-  return c->sms * nb;
+  std::lock_guard<std::mutex> g(g_occ_mu);
+  g_occ[key] = nb;
+  return nb;
+}
+
+int bnb_ctas_for(const loom_ctx* c, size_t blob, int n) {
+  return c->sms * blocks_per_sm(reinterpret_cast<const void*>(bnb_kernel), kBlock, bnb_smem_bytes(blob, n));
 }
 
 // ---------------------------------------------------------------------------
@@ -2572,15 +2606,8 @@ int prepare_fr(const loom_ctx* c, const Built& b, FrPlan& f) {
   const int cl = variant == 1 ? fr_crit_list(h) : 0;
   const size_t smem = fr_smem_bytes(b.blob.size());
   const void* fn = fr_fn(variant, cl);
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
-    cudaGetLastError();
-    return LOOM_OK;
-  }
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kFrBlock, smem) != cudaSuccess || nb < 1) {
-    cudaGetLastError();
-    return LOOM_OK;
-  }
+  const int nb = blocks_per_sm(fn, kFrBlock, smem);
+  if (nb < 1) return LOOM_OK;
   f.variant = variant;
   f.cl = cl;
   f.ctas = c->sms * std::min(nb, 1);
@@ -2662,19 +2689,13 @@ int ensure_host_arena(loom_ctx* c, size_t need) {
 }
 
 int set_smem(KernelFn fn, size_t bytes) {
-  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes)));
+  LOOM_CUDA(smem_attr(reinterpret_cast<const void*>(fn), bytes));
   return LOOM_OK;
 }
 
 // Resident CTAs per SM for a kernel instantiation at a given image size.
 int resident_ctas(KernelFn fn, size_t smem) {
-  int nb = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, reinterpret_cast<const void*>(fn), kBlock, smem) !=
-          cudaSuccess ||
-      nb < 1)
-    nb = 1;
-  return nb;
+  return std::max(1, blocks_per_sm(reinterpret_cast<const void*>(fn), kBlock, smem));
 }
 
 int ctas_for(const loom_ctx* c, uint64_t work_units, KernelFn fn, size_t smem) {
@@ -2771,6 +2792,10 @@ int loom_ctx_create(int32_t device, void* cuda_stream, loom_ctx** out) {
   loom_ctx* c = new loom_ctx;
   c->device = device;
   c->sms = prop.multiProcessorCount;
+  if (const char* bud = std::getenv("LOOM_BNB_BUDGET")) {  // test knob (bnb.cuh)
+    const unsigned long long v = std::strtoull(bud, nullptr, 10);
+    cudaMemcpyToSymbol(g_bnb_budget, &v, sizeof v);
+  }
   if (cuda_stream) {
     c->stream = static_cast<cudaStream_t>(cuda_stream);
   } else {
@@ -2895,11 +2920,13 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   if (!c || !p || !o || !out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   std::memset(out, 0, sizeof *out);
   LOOM_CUDA(cudaSetDevice(c->device));
+  Trace tr("search_argmin");
   Built b;
   const uint64_t target = static_cast<uint64_t>(c->sms) * 2 * kBlock;
   if (int rc = build_image(p, o, target, b)) return rc;
   if (b.total == 0)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+  tr.mark("image");
   const JobDesc d = make_desc(b, begin, end, algo == kAlgoFull, p, o, incumbent);
   if (d.begin >= d.end)
     return loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
@@ -2917,6 +2944,7 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   if (int rc = ensure(c->d_out, c->out_cap, 1)) return rc;
   if (int rc = ensure_host(c, 1)) return rc;
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
+  tr.mark("plan + buffers");
   LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
   FrPlan fr;
@@ -2937,7 +2965,9 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+  tr.mark("copies + launches");
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
+  tr.mark("device");
   return finish_winner(p, c->h_out[0], out);
 }
 
@@ -3037,8 +3067,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
         nmax = std::max(nmax, problems[j].n_nodes);
       }
     if (int rc = ensure_bsync(c, all.size())) return rc;
-    if (cudaFuncSetAttribute(reinterpret_cast<const void*>(bnb_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(bsmem)) == cudaSuccess) {
+    if (smem_attr(reinterpret_cast<const void*>(bnb_kernel), static_cast<size_t>(bsmem)) == cudaSuccess) {
       bnb_kernel<<<static_cast<int>(all.size()), kBlock, bsmem, c->stream>>>(c->d_arena, c->d_jobs, 1, c->d_scratch,
                                                                           c->d_tickets, c->d_bsync, c->d_out);
       LOOM_CUDA(cudaGetLastError());
@@ -3392,8 +3421,7 @@ int refine_and_filter(loom_ctx* c, ParetoPoint* d_in, uint64_t n, std::vector<Pa
   ParetoPoint* cur = d_in;
   ParetoPoint* nxt = d_a.p;
   const size_t gsmem = kGuardBytes;
-  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pareto_prefilter_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem)));
+  LOOM_CUDA(smem_attr(reinterpret_cast<const void*>(pareto_prefilter_kernel), static_cast<size_t>(gsmem)));
   for (int round = 0; round < 8 && n > kSub; ++round) {
     const uint64_t stride = n / kSub;
     LOOM_CUDA(cudaMemcpy2DAsync(d_sub.p, sizeof(ParetoPoint), cur, sizeof(ParetoPoint) * stride, sizeof(ParetoPoint),
@@ -3445,10 +3473,8 @@ int pareto_run(loom_ctx* c, const loom_problem* p, uint64_t begin, uint64_t end,
   DevBuf<uint8_t> d_blob(c);
   LOOM_CUDA(d_blob.alloc(bytes));
   LOOM_CUDA(cudaMemcpyAsync(d_blob.p, b.blob.data(), bytes, cudaMemcpyHostToDevice, c->stream));
-  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pareto_eval_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pareto_points_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes + 128)));
+  LOOM_CUDA(smem_attr(reinterpret_cast<const void*>(pareto_eval_kernel), static_cast<size_t>(smem)));
+  LOOM_CUDA(smem_attr(reinterpret_cast<const void*>(pareto_points_kernel), static_cast<size_t>(bytes + 128)));
 
   // guard: exact frontier of an evenly strided sample of the range
   const auto t_guard = std::chrono::steady_clock::now();
@@ -3642,8 +3668,7 @@ extern "C" int loom_search_greedy(loom_ctx* c, const loom_problem* p, const loom
   LOOM_CUDA(cudaMemcpyAsync(d_blob.p, b.blob.data(), bytes, cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(d_ord.p, ord.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
   LOOM_CUDA(cudaMemcpyAsync(d_seed.p, sd.data(), 4 * n, cudaMemcpyHostToDevice, c->stream));
-  LOOM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(greedy_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes + 128)));
+  LOOM_CUDA(smem_attr(reinterpret_cast<const void*>(greedy_kernel), static_cast<size_t>(bytes + 128)));
   greedy_kernel<<<1, kBlock, bytes + 128, c->stream>>>(d_blob.p, bytes, d_ord.p, d_seed.p, max_sweeps, d_out.p,
                                                        d_sw.p);
   LOOM_CUDA(cudaGetLastError());
