@@ -383,6 +383,15 @@ int loom_exhaustive_search_json(loom_ctx* ctx, const char* dag_json, const char*
                                 const char* objective_json, const char* bounds_json, char* out_json,
                                 size_t cap, size_t* needed);
 
+/* The --pin path (loom_main.cpp:125-146): parse a config point
+ * (config.hpp:66-117 parse_config_point, with its SchemaError messages) and
+ * return estimate(config, dag, library) (estimator.hpp:43-78) as the same
+ * ConfigEstimate JSON, without "plan_index"/"plans".  Host only: one plan.
+ * Missing dag tasks are rejected like the pinned-plan mode
+ * (ValidationError: pinned_plan: missing assignment for task '<id>'). */
+int loom_estimate_config_json(const char* dag_json, const char* library_json, const char* config_json,
+                              char* out_json, size_t cap, size_t* needed);
+
 #ifdef __cplusplus
 }
 #endif

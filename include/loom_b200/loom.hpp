@@ -195,7 +195,13 @@ struct ConfigPoint {
   std::map<std::string, NodeAssignment> nodes;
   std::string identifier() const;
   std::string to_json_text() const;
+  static ConfigPoint from_json_text(const std::string& text);  // = parse_config_point
 };
+
+// A config point / --pin file (config.hpp:66-117, parse_config_point):
+// SchemaError("malformed config point: ...") or the per-node checks'
+// messages on bad input.
+ConfigPoint parse_config_point(const std::string& text);
 
 // Substring one node contributes to ConfigPoint::identifier().
 std::string assignment_token(const std::string& node_id, const NodeAssignment& a);

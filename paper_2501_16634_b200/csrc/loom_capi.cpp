@@ -789,6 +789,37 @@ int loom_exhaustive_search_json(loom_ctx* ctx, const char* dag_json, const char*
       dag_json, library_json, objective_json, bounds_json, out_json, cap, needed);
 }
 
+int loom_estimate_config_json(const char* dag_json, const char* library_json, const char* config_json,
+                              char* out_json, size_t cap, size_t* needed) {
+  int rc = LOOM_OK;
+  std::string result;
+  try {
+    const loom::WorkflowDag dag = loom::WorkflowDag::from_json_text(dag_json ? dag_json : "");
+    const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json ? library_json : "");
+    const loom::ConfigPoint config = loom::parse_config_point(config_json ? config_json : "");
+    for (const auto& node : dag.nodes)
+      if (!config.nodes.count(node.id))
+        throw loom::ValidationError("pinned_plan: missing assignment for task '" + node.id + "'");
+    const loom::ConfigEstimate e = loom::estimate(config, dag, lib);
+    loomjson::Value v = loomjson::parse(estimate_json(e, 0, 0));
+    loomjson::Value o = loomjson::Value::make_object();
+    for (const auto& [k, x] : v.members())
+      if (k != "plan_index" && k != "plans") o.set(k, x);
+    result = o.dump();
+  } catch (const loom::Error& e) {
+    rc = loomi::fail(status_of(e), e.what());
+    result = error_json(e.what());
+  } catch (const std::exception& e) {
+    rc = loomi::fail(LOOM_INVALID, std::string("InvalidConfigError: ") + e.what());
+    result = error_json(loom_last_error());
+  }
+  const std::string err = loom_last_error();
+  const int crc = copy_out(result, out_json, cap, needed);
+  if (rc == LOOM_OK) return crc;
+  loomi::set_error(err);
+  return rc;
+}
+
 int loom_group_exhaustive_search_json(loom_group* g, const char* dag_json, const char* library_json,
                                       const char* objective_json, const char* bounds_json, char* out_json,
                                       size_t cap, size_t* needed) {

@@ -434,6 +434,43 @@ std::string ConfigPoint::to_json_text() const {
   return v.dump();
 }
 
+// Reader of a config point / --pin file (config.hpp:66-117: from_json of
+// Placement, NodeAssignment and ConfigPoint with their defaults -- workers 1,
+// path_count 1, label "" -- then parse_config_point's checks and messages).
+ConfigPoint parse_config_point(const std::string& text) {
+  ConfigPoint c;
+  try {
+    const Value j = loomjson::parse(text);
+    if (const Value* v = j.find("label")) c.label = v->as_string("label");
+    for (const auto& [node_id, a] : j.at("nodes").members()) {
+      NodeAssignment na;
+      na.implementation = a.at("implementation").as_string("implementation");
+      for (const Value& pv : a.at("placements").items()) {
+        Placement pl;
+        pl.sku = pv.at("sku").as_string("sku");
+        pl.units = static_cast<int>(pv.at("units").as_int("units"));
+        if (const Value* w = pv.find("workers")) pl.workers = static_cast<int>(w->as_int("workers"));
+        na.placements.push_back(pl);
+      }
+      if (const Value* pc = a.find("path_count")) na.path_count = static_cast<int>(pc->as_int("path_count"));
+      c.nodes[node_id] = std::move(na);
+    }
+  } catch (const loomjson::ParseError& e) {
+    throw SchemaError(std::string("malformed config point: ") + e.what());
+  }
+  for (const auto& [node_id, a] : c.nodes) {
+    if (a.implementation.empty()) throw SchemaError("config node '" + node_id + "': empty implementation");
+    if (a.placements.empty()) throw SchemaError("config node '" + node_id + "': no placements");
+    for (const auto& pl : a.placements)
+      if (pl.units < 1 || pl.workers < 1)
+        throw SchemaError("config node '" + node_id + "': units and workers must be >= 1");
+    if (a.path_count < 1) throw SchemaError("config node '" + node_id + "': path_count must be >= 1");
+  }
+  return c;
+}
+
+ConfigPoint ConfigPoint::from_json_text(const std::string& text) { return parse_config_point(text); }
+
 // ---------------------------------------------------------------------------
 // chunking + node plan
 // ---------------------------------------------------------------------------

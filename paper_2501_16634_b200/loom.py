@@ -195,6 +195,8 @@ def lib() -> C.CDLL:
         "loom_lowered_sweep_order": ([vp, C.POINTER(C.c_int32)], C.c_int),
         "loom_greedy_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32, C.c_char_p,
                                      C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+        "loom_estimate_config_json": ([C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t,
+                                       C.POINTER(C.c_size_t)], C.c_int),
         "loom_exhaustive_search_json": ([vp, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
                                          C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
         "loom_search_argmin_lowered_each": ([vp, C.POINTER(vp), C.c_int32, O, W, C.POINTER(C.c_int32)], C.c_int),
@@ -813,6 +815,24 @@ def exhaustive_search(dag: Any, library: Any, objective_: Any, bounds: Any, ctx:
         buf = C.create_string_buffer(need.value)
         rc = lib().loom_exhaustive_search_json(ctx.handle, _text(dag), _text(library), _text(objective_),
                                                _text(bounds), buf, need.value, C.byref(need))
+    out = json.loads(buf.value.decode())
+    if rc != LOOM_OK:
+        _raise(rc, out.get("message", last_error()))
+    return out
+
+
+def estimate_config(dag: Any, library: Any, config: Any) -> dict:
+    """The --pin path (loom_main.cpp:125-146): parse_config_point
+    (config.hpp:66-117) + estimate (estimator.hpp:43-78) of one config point on
+    the host; the ConfigEstimate as a dict (no plan_index)."""
+    need = C.c_size_t(0)
+    cap = 1 << 16
+    buf = C.create_string_buffer(cap)
+    rc = lib().loom_estimate_config_json(_text(dag), _text(library), _text(config), buf, cap, C.byref(need))
+    if rc != LOOM_OK and need.value > cap:
+        buf = C.create_string_buffer(need.value)
+        rc = lib().loom_estimate_config_json(_text(dag), _text(library), _text(config), buf, need.value,
+                                             C.byref(need))
     out = json.loads(buf.value.decode())
     if rc != LOOM_OK:
         _raise(rc, out.get("message", last_error()))
