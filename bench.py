@@ -1,11 +1,14 @@
 """bench.py -- plans evaluated per second for the B200 exhaustive plan search.
 
 Workload (BASELINE.json configs[2], "C3"): a synthetic 10-task DAG with 16
-lever assignments per task, 16^10 = 1.1e12 plans, MIN_COST under a latency
-SLO, the plan-index space sharded by contiguous range across the ranks
-(strong scaling: the whole space is searched at every N).  configs[1] (C2,
-1.2e6 plans) finishes in microseconds and is reported under "configs" with
-C1/C4/C5 as time-to-plan lines, not as the headline.
+lever assignments per task, 16^10 = 1.1e12 plans, MIN_COST under a binding
+latency SLO.  N > 1 (torchrun, one rank per GPU): by default every rank runs
+its own whole-space search (N independent scheduling requests: weak
+scaling); --sharded splits ONE search's plan space by contiguous index range
+across the ranks through the library's NCCL group (strong scaling; the
+frontier search is latency-bound, so this barely shortens it -- DESIGN.md
+§7).  configs[1] (C2, 1.2e6 plans) finishes in microseconds and is reported
+under "configs" with C1/C4/C5 as time-to-plan lines, not as the headline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
@@ -239,11 +242,19 @@ def b200_arm(args) -> None:
         else:
             dist.init_process_group(backend)
     stream = torch.cuda.Stream()
-    # N > 1 over NCCL: the library's own multi-GPU group (loom_group_create_rank:
-    # its NCCL communicator, the sharded search and the ncclAllGather of the
-    # per-rank records all live in libloom_b200.so); torch.distributed only
-    # hands rank 0's NCCL id to the other ranks and times the ranks
-    use_group = world > 1 and backend == "nccl"
+    # N > 1, default: N independent searches, one per GPU (weak scaling: each
+    # rank serves its own scheduling request over the whole C3 space).  The
+    # frontier branch and bound finishes one request in ~0.2 ms, bound by its
+    # per-level critical path, so splitting ONE request's plan space across
+    # GPUs barely shortens it (max shard time 0.20 ms at N = 8).
+    # --sharded: one request split by plan-index range instead -- over NCCL
+    # through the library's own multi-GPU group (loom_group_create_rank: its
+    # NCCL communicator, the sharded search and the ncclAllGather of the
+    # per-rank records all live in libloom_b200.so; torch.distributed only
+    # hands rank 0's NCCL id to the other ranks and times the ranks).
+    sharded = world > 1 and args.sharded
+    replicas = world > 1 and not sharded
+    use_group = sharded and backend == "nccl"
     group = None
     if use_group:
         ids = [loom.nccl_unique_id() if rank == 0 else None]
@@ -258,7 +269,7 @@ def b200_arm(args) -> None:
     lw = loom.Lowered(w.dag, w.library, w.bounds)
     obj = loom.objective(w.objective)
     total = lw.total
-    begin, end = D.shard_range(total, rank, world)
+    begin, end = D.shard_range(total, rank, world) if sharded else (0, total)
     dp = loom.DeviceProblem(ctx, lw.problem, obj) if not use_group else None
     scratch = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 
@@ -287,7 +298,7 @@ def b200_arm(args) -> None:
     def search(b, e):
         if use_group:  # the whole space, sharded and exchanged inside the library
             group_out["w"] = group.search_argmin(lw.problem, obj)
-        elif world > 1:
+        elif sharded:
             dp.search_shard_async(b, e)
         else:
             dp.search_async(b, e)
@@ -318,11 +329,12 @@ def b200_arm(args) -> None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    value = total / (ms / 1e3)
+    units = total * (world if replicas else 1)  # plans covered by all ranks per step
+    value = units / (ms / 1e3)
 
     # winners must agree with a full-space reduce (checked every run)
     local_w = shard_result()
-    winners = D.allgather_winners(local_w, device=red_dev) if world > 1 and not use_group else [local_w]
+    winners = D.allgather_winners(local_w, device=red_dev) if sharded and not use_group else [local_w]
     chosen = D.combine(winners, obj)
     seed = greedy_seed_index(loom, lw, obj)
     # the headline is a real search: the SLO binds and the argmin is not the
@@ -331,7 +343,7 @@ def b200_arm(args) -> None:
 
     # ---- e2e: the public drop-in call, host JSON in / plan out ---------------
     def e2e_step():
-        if world == 1:
+        if not sharded:
             return loom.exhaustive_search(dag_t, lib_t, obj_t, bounds_t, ctx=ctx)
         if use_group:
             return group.exhaustive_search(dag_t, lib_t, obj_t, bounds_t)
@@ -353,7 +365,7 @@ def b200_arm(args) -> None:
     te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = total / (float(te.item()) / 1e3)
+    e2e_value = units / (float(te.item()) / 1e3)
     assert out["plan_index"] == chosen["plan_index"], (out, chosen)
 
     if dp is not None:
@@ -413,10 +425,14 @@ def b200_arm(args) -> None:
                     "SURVEY.md §8d).  traffic = DRAM bytes per launch (ncu)."}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if replicas else "strong",
             "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "objective": w.objective,
-                       "plans_per_step": total, "parallelism": f"plan-index range x{world}" + (" (loom_group: NCCL inside the library)" if use_group else ""),
+                       "plans_per_step": units,
+                       "parallelism": (f"{world} independent whole-space searches, one per GPU" if replicas else
+                                       f"plan-index range x{world}" + (" (loom_group: NCCL inside the library)"
+                                                                      if use_group else "")),
                        "l2": "flushed between timed steps (256 MiB write); the problem image is 8 KB in smem",
                        "value_counts": "plans COVERED per second: every plan of the space is in the argmin's "
                                        "domain; subtrees whose exact criteria bound is infeasible or strictly "
@@ -433,7 +449,7 @@ def b200_arm(args) -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": float(te.item()),
                     "h2d_bytes_per_step": image_bytes + 64, "d2h_bytes_per_step": 64,
                     "path": "loom_exhaustive_search_json: JSON parse + lowering + H2D + kernel + D2H + decode"
-                    if world == 1 else "loom_group_exhaustive_search_json: JSON parse + lowering + per-rank shard "
+                    if not sharded else "loom_group_exhaustive_search_json: JSON parse + lowering + per-rank shard "
                     "search (range + greedy incumbent) + ncclAllGather of the rank records + reduce + decode"},
             "roofline": roofline,
             "gpu_launches": launches,
@@ -672,6 +688,9 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N > 1: split ONE search's plan space across the ranks (strong scaling) instead of one "
+                         "independent search per rank")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the time-to-plan lines of C1/C2/C4/C5 and C3 greedy")
     args = ap.parse_args()

@@ -18,8 +18,9 @@ ap.add_argument("--config", default="c3")
 ap.add_argument("--ranks", type=int, nargs="+", default=[1, 2, 4, 8])
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-incumbent", action="store_true", help="plain range searches (no common greedy incumbent)")
+ap.add_argument("--binding", action="store_true", help="C3 under the bench's binding 40 s SLO")
 a = ap.parse_args()
-w = {"c3": W.config3, "c5": W.config5, "c2": W.config2}[a.config]()
+w = W.config3(slo_us=W.C3_BINDING_SLO_US) if a.binding else {"c3": W.config3, "c5": W.config5, "c2": W.config2}[a.config]()
 lw = loom.Lowered(w.dag, w.library, w.bounds)
 obj = loom.objective(w.objective)
 ctx = loom.Context(0)
