@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -265,7 +266,13 @@ ConfigEstimate greedy_search(const WorkflowDag& dag, const AgentLibrary& library
 // ---- lowering: the flat tables the kernels read --------------------------
 struct LoweredProblem {
   std::vector<std::string> node_ids;                 // dag.nodes order
-  std::vector<std::vector<NodeAssignment>> options;  // node_options per node
+  std::vector<std::vector<NodeAssignment>> options;  // node_options per node (empty when shared_options is used)
+  // node_options per node shared with a LowerCache (batch lowering): the
+  // option list of a node does not depend on its work, only the numbers do
+  std::vector<std::shared_ptr<const std::vector<NodeAssignment>>> shared_options;
+  const std::vector<NodeAssignment>& node_opts(int i) const {
+    return shared_options.empty() ? options[i] : *shared_options[i];
+  }
   std::vector<int32_t> radix;
   std::vector<int64_t> wall_us;
   std::vector<double> gpu_wh, cpu_wh, dollars;       // already x path_count
@@ -279,5 +286,15 @@ struct LoweredProblem {
 };
 
 LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const SearchBounds& bounds);
+
+// Option sets memoised across the DAGs of a batch (one library, one set of
+// bounds, one thread): per node, the options, their identifier ranks and how
+// each option's numbers are computed depend only on the node's capability,
+// fan-out cap, path cap and which CPU+GPU splits are possible, so a hit costs
+// the per-option numbers alone.  The result equals lower() exactly.
+class LowerCache;
+std::shared_ptr<LowerCache> make_lower_cache();
+LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const SearchBounds& bounds,
+                     LowerCache& cache);
 
 }  // namespace loom

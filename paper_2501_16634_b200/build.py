@@ -68,7 +68,7 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
             _run(["g++", *CXX_FLAGS, "-c", str(CSRC / src), "-o", str(o)], log)
         objs.append(o)
     if force or _stale(lib, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lpthread", "-lnccl"], log)
+        _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lpthread", "-ldl"], log)
     if verbose:
         print("\n".join(log))
     (cu_obj / "build.log").write_text("\n".join(log))

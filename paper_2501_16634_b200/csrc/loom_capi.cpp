@@ -457,15 +457,6 @@ int loom_greedy_search_json(loom_ctx* ctx, const char* dag_json, const char* lib
                             const char* bounds_json, int32_t max_sweeps, char* out_json, size_t cap, size_t* needed) {
   int rc = LOOM_OK;
   std::string result;
-  const bool trace = std::getenv("LOOM_TRACE") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  auto mark = [&](const char* what) {
-    if (!trace) return;
-    const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[loom trace] exhaustive_json %s %.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(t - t0).count());
-    t0 = t;
-  };
   try {
     const loom::WorkflowDag dag = loom::WorkflowDag::from_json_text(dag_json ? dag_json : "");
     const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json ? library_json : "");
@@ -622,11 +613,14 @@ int loom_lower_batch(const char* library_json, const char* bounds_json, const ch
     std::vector<std::thread> pool;
     for (int w = 0; w < t; ++w)
       pool.emplace_back([&, w] {
+        // option sets repeat across the jobs of a batch: one cache per thread
+        const auto cache = loom::make_lower_cache();
         for (int i = w; i < n; i += t) {
           out[i] = nullptr;
           try {
             auto lw = std::make_unique<loom_lowered>();
-            lw->L = loom::lower(loom::WorkflowDag::from_json_text(dag_jsons[i] ? dag_jsons[i] : ""), lib, bounds);
+            lw->L = loom::lower(loom::WorkflowDag::from_json_text(dag_jsons[i] ? dag_jsons[i] : ""), lib, bounds,
+                                *cache);
             lw->view = lw->L.view();
             out[i] = lw.release();
             status[i] = LOOM_OK;
@@ -754,11 +748,11 @@ int loom_lowered_config_json(const loom_lowered* lw, uint64_t plan_index, char* 
 int loom_lowered_option_json(const loom_lowered* lw, int32_t node, int32_t option, char* buf, size_t cap,
                              size_t* needed) {
   if (!lw) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null lowered");
-  if (node < 0 || node >= static_cast<int>(lw->L.options.size()) || option < 0 ||
-      option >= static_cast<int>(lw->L.options[node].size()))
+  if (node < 0 || node >= static_cast<int>(lw->L.radix.size()) || option < 0 ||
+      option >= static_cast<int>(lw->L.node_opts(node).size()))
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: option out of range");
   loom::ConfigPoint c;
-  c.nodes[lw->L.node_ids[node]] = lw->L.options[node][option];
+  c.nodes[lw->L.node_ids[node]] = lw->L.node_opts(node)[option];
   loomjson::Value v = loomjson::parse(c.to_json_text()).at("nodes").at(lw->L.node_ids[node]);
   v.set("identifier", loomjson::Value::make_string(c.identifier()));
   return copy_out(v.dump(), buf, cap, needed);

@@ -22,12 +22,14 @@
 // contiguous job ranges; an all-gather of the padded per-job records
 // assembles the results on every rank.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cstring>
 #include <functional>
 #include <string>
+#include <type_traits>
 #include <thread>
 #include <vector>
 
@@ -48,6 +50,51 @@ struct loom_group {
 
 namespace {
 
+// NCCL is loaded when a group is first created, not when libloom_b200.so
+// loads: linking it would put the system libnccl into every process that
+// loads this library, ahead of the NCCL build PyTorch bundles (whose newer
+// symbols torch then fails to resolve).  A libnccl.so.2 already in the
+// process (e.g. PyTorch's) is used; else the loader's default one.
+struct NcclApi {
+  decltype(&::ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&::ncclGroupStart) GroupStart = nullptr;
+  decltype(&::ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&::ncclAllGather) AllGather = nullptr;
+  decltype(&::ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&::ncclCommInitAll) CommInitAll = nullptr;
+  decltype(&::ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&::ncclCommDestroy) CommDestroy = nullptr;
+  std::string error;
+  bool ok() const { return error.empty(); }
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.error = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+      return a;
+    }
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn && a.error.empty()) a.error = std::string("libnccl.so.2 lacks ") + name;
+    };
+    sym(a.GetErrorString, "ncclGetErrorString");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.AllGather, "ncclAllGather");
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitAll, "ncclCommInitAll");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    return a;
+  }();
+  return api;
+}
+
 struct alignas(16) RankRecord {  // one rank's argmin result on the wire
   loom_winner w;
   int32_t status;
@@ -56,7 +103,7 @@ struct alignas(16) RankRecord {  // one rank's argmin result on the wire
 static_assert(sizeof(RankRecord) == 80, "RankRecord is the all-gather unit");
 
 int nccl_fail(ncclResult_t r, const char* what) {
-  return loomi::fail(LOOM_DEVICE_ERROR, std::string("DeviceError: ") + what + ": " + ncclGetErrorString(r));
+  return loomi::fail(LOOM_DEVICE_ERROR, std::string("DeviceError: ") + what + ": " + nccl().GetErrorString(r));
 }
 
 #define LOOM_NCCL(call)                                     \
@@ -115,12 +162,12 @@ int allgather(loom_group* g, const std::vector<const void*>& send, size_t unit, 
     cudaSetDevice(g->device[i]);
     LOOM_CUDA_G(cudaMemcpyAsync(g->d_buf[i], send[i], unit, cudaMemcpyHostToDevice, g->stream[i]));
   }
-  LOOM_NCCL(ncclGroupStart());
+  LOOM_NCCL(nccl().GroupStart());
   for (int i = 0; i < m; ++i) {
     uint8_t* b = static_cast<uint8_t*>(g->d_buf[i]);
-    LOOM_NCCL(ncclAllGather(b, b + unit, unit, ncclUint8, g->comm[i], g->stream[i]));
+    LOOM_NCCL(nccl().AllGather(b, b + unit, unit, ncclUint8, g->comm[i], g->stream[i]));
   }
-  LOOM_NCCL(ncclGroupEnd());
+  LOOM_NCCL(nccl().GroupEnd());
   all.resize(total);
   cudaSetDevice(g->device[0]);
   LOOM_CUDA_G(cudaMemcpyAsync(all.data(), static_cast<uint8_t*>(g->d_buf[0]) + unit, total, cudaMemcpyDeviceToHost,
@@ -153,8 +200,9 @@ int loom_shard_range(uint64_t begin, uint64_t end, int32_t rank, int32_t world, 
 
 int loom_nccl_unique_id(uint8_t* out) {
   if (!out) return loomi::fail(LOOM_INVALID, "InvalidConfigError: null out");
+  if (!nccl().ok()) return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: " + nccl().error);
   ncclUniqueId id;
-  LOOM_NCCL(ncclGetUniqueId(&id));
+  LOOM_NCCL(nccl().GetUniqueId(&id));
   static_assert(sizeof(id) == LOOM_NCCL_ID_BYTES, "ncclUniqueId size");
   std::memcpy(out, &id, sizeof id);
   return LOOM_OK;
@@ -167,6 +215,7 @@ int loom_group_create(uint64_t device_mask, loom_group** out) {
   for (int d = 0; d < 64; ++d)
     if (device_mask >> d & 1) devs.push_back(d);
   if (devs.empty()) return loomi::fail(LOOM_INVALID, "InvalidConfigError: empty device mask");
+  if (!nccl().ok()) return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: " + nccl().error);
   auto* g = new loom_group;
   for (int d : devs) {
     loom_ctx* c = nullptr;
@@ -182,7 +231,7 @@ int loom_group_create(uint64_t device_mask, loom_group** out) {
   g->comm.assign(devs.size(), nullptr);
   g->d_buf.assign(devs.size(), nullptr);
   g->buf_cap.assign(devs.size(), 0);
-  const ncclResult_t r = ncclCommInitAll(g->comm.data(), g->world, devs.data());
+  const ncclResult_t r = nccl().CommInitAll(g->comm.data(), g->world, devs.data());
   if (r != ncclSuccess) {
     g->comm.clear();
     loom_group_destroy(g);
@@ -197,6 +246,7 @@ int loom_group_create_rank(int32_t device, void* cuda_stream, const uint8_t* ncc
   if (!out || !nccl_id || world < 1 || rank < 0 || rank >= world)
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: bad group rank");
   *out = nullptr;
+  if (!nccl().ok()) return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: " + nccl().error);
   auto* g = new loom_group;
   loom_ctx* c = nullptr;
   if (int rc = loom_ctx_create(device, cuda_stream, &c)) {
@@ -214,7 +264,7 @@ int loom_group_create_rank(int32_t device, void* cuda_stream, const uint8_t* ncc
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
   cudaSetDevice(device);
-  const ncclResult_t r = ncclCommInitRank(&g->comm[0], world, id, rank);
+  const ncclResult_t r = nccl().CommInitRank(&g->comm[0], world, id, rank);
   if (r != ncclSuccess) {
     g->comm.clear();
     loom_group_destroy(g);
@@ -227,7 +277,7 @@ int loom_group_create_rank(int32_t device, void* cuda_stream, const uint8_t* ncc
 int loom_group_destroy(loom_group* g) {
   if (!g) return LOOM_OK;
   for (size_t i = 0; i < g->comm.size(); ++i)
-    if (g->comm[i]) ncclCommDestroy(g->comm[i]);
+    if (g->comm[i]) nccl().CommDestroy(g->comm[i]);
   for (size_t i = 0; i < g->d_buf.size(); ++i)
     if (g->d_buf[i]) {
       cudaSetDevice(g->device[i]);

@@ -686,6 +686,132 @@ std::vector<NodeAssignment> node_options(const DagNode& node, const AgentLibrary
 }
 
 // ---------------------------------------------------------------------------
+// option-set cache of a batch lowering
+// ---------------------------------------------------------------------------
+class LowerCache {
+ public:
+  // per capability: each implementation's usable workers and the (gpu, cpu)
+  // pairs that fit the caps, in enumerate_options' order
+  struct Impl {
+    const Implementation* impl;
+    std::vector<Worker> usable;
+    std::vector<std::pair<Worker, Worker>> pairs;
+  };
+  // one option set: the options (shared with every lowered problem that
+  // uses it), per option how its plan is computed, and the identifier ranks
+  struct Set {
+    std::shared_ptr<const std::vector<NodeAssignment>> opts;
+    std::vector<const Implementation*> impl;
+    std::vector<Worker> w0, w1;   // the worker (single sku) or the (gpu, cpu) pair
+    std::vector<int32_t> fan;     // single sku: the fan-out; 0: hybrid pair
+    std::vector<int32_t> base;    // option whose plan this one shares (its path copies)
+    std::vector<int32_t> rank;    // identifier-substring rank within the node
+  };
+  std::map<std::string, std::vector<Impl>, std::less<>> caps;
+  std::map<std::string, Set, std::less<>> sets;
+  std::string key;  // scratch
+};
+
+std::shared_ptr<LowerCache> make_lower_cache() { return std::make_shared<LowerCache>(); }
+
+namespace {
+const std::vector<LowerCache::Impl>& cap_entry(LowerCache& c, const std::string& cap, const AgentLibrary& library,
+                                               const SearchBounds& bounds) {
+  auto it = c.caps.find(cap);
+  if (it != c.caps.end()) return it->second;
+  std::vector<LowerCache::Impl> v;
+  for (const Implementation* impl : library.implementations_for(cap)) {
+    LowerCache::Impl e{impl, {}, {}};
+    for (const ExecutionProfile* p : library.profiles_for(impl->name)) {
+      const HardwareSku* sku = library.sku(p->sku);
+      if (impl->supports(sku->hardware_class)) e.usable.push_back({p, sku});
+    }
+    for (const Worker& g : e.usable) {
+      if (g.sku->hardware_class != HardwareClass::gpu) continue;
+      for (const Worker& cw : e.usable) {
+        if (cw.sku->hardware_class != HardwareClass::cpu) continue;
+        if (fits(bounds, g.profile->sku, g.profile->units, g.profile->units) &&
+            fits(bounds, cw.profile->sku, cw.profile->units, cw.profile->units))
+          e.pairs.emplace_back(g, cw);
+      }
+    }
+    v.push_back(std::move(e));
+  }
+  return c.caps.emplace(cap, std::move(v)).first->second;
+}
+
+// The option set of a node (enumerate_options' order and contents), built on
+// a miss.  Keyed by what enumerate_options depends on besides the library
+// and bounds: capability, fan-out cap, path cap, hybrids, and per fitting
+// (gpu, cpu) pair whether the work splits across both.
+const LowerCache::Set& option_set(LowerCache& c, const DagNode& node, const AgentLibrary& library,
+                                  const SearchBounds& bounds) {
+  const int paths_max = node.multi_path ? std::max(1, bounds.max_paths) : 1;
+  const int fan_cap =
+      node.splittable ? std::min(bounds.max_fanout, chunk_capacity(node.work_units, node.min_chunk)) : 1;
+  const int fan_hi = std::max(1, fan_cap);
+  const bool hybrids = node.splittable && bounds.max_fanout >= 2;
+  const auto& impls = cap_entry(c, node.capability, library, bounds);
+  std::string& key = c.key;
+  key.assign(node.capability);
+  key.push_back('\x1f');
+  key.append(std::to_string(fan_hi));
+  key.push_back('/');
+  key.append(std::to_string(paths_max));
+  key.push_back(hybrids ? 'h' : '-');
+  std::vector<uint8_t> split_ok;
+  if (hybrids)
+    for (const auto& e : impls)
+      for (const auto& [g, cw] : e.pairs) {
+        const auto split = water_fill_split(node.work_units, node.min_chunk, {g.profile->throughput, cw.profile->throughput});
+        const bool ok = !(node.work_units > 0 && (split[0] <= 0 || split[1] <= 0));
+        split_ok.push_back(ok);
+        key.push_back(ok ? '1' : '0');
+      }
+  auto it = c.sets.find(key);
+  if (it != c.sets.end()) return it->second;
+
+  LowerCache::Set set;
+  auto opts = std::make_shared<std::vector<NodeAssignment>>();
+  auto emit = [&](const Implementation* impl, std::vector<Placement> placements, Worker w0, Worker w1, int fan) {
+    const int first = static_cast<int>(opts->size());
+    for (int k = 1; k <= paths_max; ++k) {
+      opts->push_back({impl->name, placements, k});
+      set.impl.push_back(impl);
+      set.w0.push_back(w0);
+      set.w1.push_back(w1);
+      set.fan.push_back(fan);
+      set.base.push_back(first);
+    }
+  };
+  std::size_t pi = 0;
+  for (const auto& e : impls) {
+    for (const Worker& u : e.usable)
+      for (int w = 1; w <= fan_hi; ++w)
+        if (fits(bounds, u.profile->sku, u.profile->units, u.profile->units * w))
+          emit(e.impl, {{u.profile->sku, u.profile->units, w}}, u, u, w);
+    if (!hybrids) continue;
+    for (const auto& [g, cw] : e.pairs)
+      if (split_ok[pi++])
+        emit(e.impl, {{g.profile->sku, g.profile->units, 1}, {cw.profile->sku, cw.profile->units, 1}}, g, cw, 0);
+  }
+  // identifier ranks: the substrings of one node share their "<id>=" prefix,
+  // so their order does not depend on the node id
+  const int r = static_cast<int>(opts->size());
+  std::vector<std::string> tokens;
+  tokens.reserve(r);
+  for (const NodeAssignment& a : *opts) tokens.push_back(assignment_token("", a));
+  std::vector<int> order(r);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tokens[a] < tokens[b]; });
+  set.rank.assign(r, 0);
+  for (int k = 0; k < r; ++k) set.rank[order[k]] = k;
+  set.opts = std::move(opts);
+  return c.sets.emplace(key, std::move(set)).first->second;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
 // estimate / order (host copies used for the winner and for small API calls)
 // ---------------------------------------------------------------------------
 namespace {
@@ -786,7 +912,9 @@ bool meets_quality_floor(const ConfigEstimate& e, const ObjectiveHierarchy& obje
 // ---------------------------------------------------------------------------
 // lowering
 // ---------------------------------------------------------------------------
-LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const SearchBounds& bounds) {
+namespace {
+LoweredProblem lower_impl(const WorkflowDag& dag, const AgentLibrary& library, const SearchBounds& bounds,
+                          LowerCache* cache) {
   LoweredProblem L;
   const int n = static_cast<int>(dag.nodes.size());
   std::map<std::string, int> index;
@@ -843,9 +971,44 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
   impls.reserve(32);
   L.radix.reserve(n);
   L.options.reserve(n);
+  if (cache) L.shared_options.reserve(n);
   for (int i = 0; i < n; ++i) {
     const DagNode& node = dag.nodes[i];
     check_name(node.id);
+    if (cache) {  // the option set from the cache; only the numbers are per node
+      const LowerCache::Set& set = option_set(*cache, node, library, bounds);
+      const int r = static_cast<int>(set.opts->size());
+      L.radix.push_back(r);
+      if (r == 0) L.total = 0;
+      else if (L.total && L.total > UINT64_MAX / static_cast<uint64_t>(r))
+        throw InvalidConfigError("plan space exceeds 2^64 plans");
+      else L.total *= static_cast<uint64_t>(r);
+      NodePlan plan;
+      std::vector<Worker> workers;
+      for (int o = 0; o < r; ++o) {
+        const NodeAssignment& a = (*set.opts)[o];
+        if (o == 0 || set.base[o] != set.base[o - 1]) {  // == plan_node_execution(node, a, library)
+          check_name(a.implementation);
+          for (const Placement& p : a.placements) check_name(p.sku);
+          if (set.fan[o] > 0) {
+            workers.assign(static_cast<std::size_t>(set.fan[o]), set.w0[o]);
+            plan = plan_workers(node, workers.data(), workers.size(), 1, set.fan[o]);
+          } else {
+            const Worker pair[2] = {set.w0[o], set.w1[o]};
+            plan = plan_workers(node, pair, 2, 2, 2);
+          }
+        }
+        const double k = static_cast<double>(a.path_count);
+        L.wall_us.push_back(plan.wall_us);
+        L.gpu_wh.push_back(plan.gpu_wh * k);
+        L.cpu_wh.push_back(plan.cpu_wh * k);
+        L.dollars.push_back(plan.dollars * k);
+        L.quality.push_back(node_quality(node, *set.impl[o], a.path_count));
+      }
+      L.lexrank.insert(L.lexrank.end(), set.rank.begin(), set.rank.end());
+      L.shared_options.push_back(set.opts);
+      continue;
+    }
     std::vector<NodeAssignment> opts;
     opts.reserve(32);
     plans.clear();
@@ -901,6 +1064,16 @@ LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const 
   }
   return L;
 }
+}  // namespace
+
+LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const SearchBounds& bounds) {
+  return lower_impl(dag, library, bounds, nullptr);
+}
+
+LoweredProblem lower(const WorkflowDag& dag, const AgentLibrary& library, const SearchBounds& bounds,
+                     LowerCache& cache) {
+  return lower_impl(dag, library, bounds, &cache);
+}
 
 loom_problem LoweredProblem::view() const {
   loom_problem p{};
@@ -923,7 +1096,7 @@ ConfigPoint LoweredProblem::config_of(uint64_t plan_index) const {
   ConfigPoint c;
   for (int i = static_cast<int>(radix.size()) - 1; i >= 0; --i) {
     const uint64_t r = static_cast<uint64_t>(radix[i]);
-    c.nodes[node_ids[i]] = options[i][plan_index % r];
+    c.nodes[node_ids[i]] = node_opts(i)[plan_index % r];
     plan_index /= r;
   }
   return c;

@@ -241,3 +241,39 @@ def test_batch_objective_array_is_validated(loomlib):
     with pytest.raises(loom.LoomError, match="objective array has 2 entries for 3 jobs"):
         loom.exhaustive_search_batch([j.dag for j in jobs], json.dumps(jobs[0].library),
                                      [{"constraint": "MIN_COST"}] * 2, json.dumps(jobs[0].bounds), ctx=_Unused())
+
+
+def test_batch_lowering_cache_equals_plain_lowering(loomlib):
+    """loom_lower_batch memoises option sets across the DAGs of a batch
+    (LowerCache); every table, option config and identifier must equal the
+    plain per-DAG lowering: 300 C4 jobs (one library), and per random
+    scenario a batch of the scenario's DAG with work units and chunks
+    perturbed (same capabilities, other fan-out caps / split validity)."""
+    import json as _json
+    jobs = W.config4(300)
+    cases = [([j.dag for j in jobs], jobs[0].library, jobs[0].bounds)]
+    rng = random.Random(11)
+    for seed in range(0, 40, 2):
+        w = W.random_scenario(seed)
+        dags = []
+        for _ in range(6):
+            d = _json.loads(_json.dumps(w.dag))
+            for node in d["nodes"]:
+                node["work_units"] = node["work_units"] * rng.choice([0.25, 0.5, 1.0, 2.0, 5.0])
+                if node.get("min_chunk"):
+                    node["min_chunk"] = node["min_chunk"] * rng.choice([0.5, 1.0, 3.0])
+            dags.append(d)
+        cases.append((dags, w.library, w.bounds))
+    for dags, lib_, bounds in cases:
+        batch = loom.LoweredBatch(dags, lib_, bounds, threads=2)
+        for k, d in enumerate(dags):
+            plain = loom.Lowered(d, lib_, bounds)
+            got = batch[k]
+            assert _tables(got) == _tables(plain), k
+            for idx in {0, plain.total // 3, plain.total - 1}:
+                assert got.config(idx) == plain.config(idx)
+            for node in range(plain.problem.n_nodes):
+                for opt in range(plain.problem.radix[node]):
+                    assert got.option(node, opt) == plain.option(node, opt)
+            plain.close()
+        batch.close()
