@@ -626,6 +626,22 @@ def other_configs(ctx, loom, W, issue: float) -> dict:
     out["c5"] = {"plans": lw5.total, "frontier_points": len(front), "time_to_frontier_ms": 1e3 * t5,
                  "plans_per_s": lw5.total / t5}
     out["c3_score_stream"] = score_stream(ctx, loom, W)
+    # dominant kernels of C4 / C5 against the instruction-issue roofline, from
+    # one ncu capture each (tools/ncu_c4c5.sh -> profiles/ncu_summary.json):
+    # warp instructions / kernel time vs SMs x 4 SMSPs x clock
+    prof_p = ROOT / "profiles" / "ncu_summary.json"
+    prof = json.loads(prof_p.read_text()) if prof_p.exists() else {}
+    for key, name, kern in (("c4", "c4_bnb_kernel", "bnb_kernel (depth-first branch and bound, one CTA per job)"),
+                            ("c5", "c5_pareto_eval_kernel", "pareto_eval_kernel (corner-pruned evaluation)")):
+        k = prof.get(name)
+        if k and key in out:
+            t = k["duration_ns_under_ncu"] / 1e9
+            ach = k["warp_inst_per_launch"] / t
+            out[key]["roofline"] = {"bound": "instruction issue", "kernel": kern, "achieved": ach, "peak": issue / 32,
+                                    "unit": "warp instructions/s", "frac": ach * 32 / issue,
+                                    "traffic": k["dram_bytes_per_launch"], "kernel_ms_under_ncu": 1e3 * t,
+                                    "source": "one ncu --set full capture (profiles/ncu_summary.json); the "
+                                              "configuration's time_to_plan is host-inclusive"}
     return out
 
 

@@ -296,6 +296,8 @@ __device__ __forceinline__ void fr_offer(const BfsParams<NB>& P, const FrTab& T,
 //          offered to `cand` (skipped when the criteria ranked before
 //          latency already lose)
 //   job 2  completion with every free node at its smallest wall, offered
+//          (its latency is max(lnot, head + wmin + tail): no recursion when
+//          job 0 ran on the same lane)
 // A small batch runs the three jobs of a parent on three lanes; otherwise
 // one lane runs them in turn.  L: int32_t when every latency stays below
 // 2^30 us (host-checked), else int64_t.
@@ -306,7 +308,7 @@ __device__ __forceinline__ L fr_mask(L v, uint32_t m) {
 
 template <int CL, int NB, typename L>
 __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, const FrontierEntry& e, int k, int job,
-                                       FrPar& out, Rec& cand) {
+                                       FrPar& out, Rec& cand, bool have_terms) {
   constexpr L kGone = -(L(1) << (sizeof(L) * 8 - 2));  // a removed node: paths through it never win a max
   const int n = P.n;
   const int xpos = P.pos[k];
@@ -329,6 +331,11 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
     if (pj && fr_worse_before_lat<CL>(P, quantize_dev(a), quantize_dev(b), q, cand)) return;
   }
   FR_MARK2(1);
+  if (job == 2 && have_terms) {  // job 0 ran on this lane: the smallest-wall completion's latency is the bound
+    const int64_t lat = max(out.lnot, out.head + P.twmin[xpos] + out.tail);
+    fr_offer<CL>(P, T, e.dig, k, 2, a, b, q, lat, cand);
+    return;
+  }
   const bool prim = job == 1;
   L W[NB];
 #pragma unroll
@@ -560,12 +567,7 @@ __device__ __forceinline__ void fr_batch(const BfsParams<NB>& P, const FrTab& T,
     // (found after it was kept) is not expanded
     if (e.live && e.key <= fr_bound_key<CL>(P, cand)) {
 #pragma unroll 1
-      for (int j = j0; j <= j1; ++j) fr_job<CL, NB, L>(P, T, e, d, j, fp, cand);
-      if (LOOM_FR_PROF == 2) {  // experiment: the same work again, warm (instruction cache)
-        FR_MARK(d, 7);
-#pragma unroll 1
-        for (int j = j0; j <= j1; ++j) fr_job<CL, NB, L>(P, T, e, d, j, fp, cand);
-      }
+      for (int j = j0; j <= j1; ++j) fr_job<CL, NB, L>(P, T, e, d, j, fp, cand, j == 2 && j0 == 0);
     }
   }
   FR_MARK(d, 1);
