@@ -2581,6 +2581,15 @@ void set_fr_job(const Built& b, const JobDesc& d, BfsParams<NB>& P) {
   P.ranged = d.begin > 0 || d.end < b.total;
   P.has_seed = d.has_seed != 0;
   P.seed = d.has_seed ? host_rec(b, d.seed) : Rec{0, 0, 0, 0, 0, 0, 0};
+  P.seed_dig = 0;
+  if (d.has_seed) {  // packed like FrontierEntry.dig
+    uint64_t x = d.seed;
+    for (int i = P.n - 1; i >= 0; --i) {
+      const uint64_t r = static_cast<uint64_t>(P.radix[i]);
+      P.seed_dig |= (x % r) << P.shift[i];
+      x /= r;
+    }
+  }
 }
 
 // Plan the frontier search of a built problem (variant 0: not applicable).
