@@ -95,6 +95,9 @@ constexpr int kFrStage = 64;             // kept children staged per warp before
 #ifndef LOOM_FR_HEUR
 #define LOOM_FR_HEUR 1  // incumbent heuristic before the first level (fr_incumbent)
 #endif
+#ifndef LOOM_FR_HPASS
+#define LOOM_FR_HPASS 2  // its 1-opt passes at most (more found nothing on the C3 goldens)
+#endif
 
 // Per-problem constants of the frontier search (a kernel parameter; every
 // array index below is a compile-time constant after unrolling, or uniform).
@@ -110,6 +113,8 @@ struct BfsParams {
   uint64_t end;
   Rec seed;  // the incumbent every CTA starts from (exact record, host-evaluated)
   uint64_t seed_dig;  // its digits, packed like FrontierEntry.dig
+  int32_t n_qlev;     // distinct option qualities (descending, at most 8): targets of the quality-first heuristic
+  int32_t qlev[8];
   // by topological position t
   int32_t tnode[NB];    // node at position t
   // pm[t][p] = ~0 if position p precedes position t by an edge, else 0;
@@ -538,34 +543,50 @@ __device__ __forceinline__ Rec fr_block_best(const BfsParams<NB>& P, Rec r, bool
 //   H1 (FP-primary objectives): thread t picks, per node, the option
 //       minimising primary term + lambda_t x wall (a Lagrangian relaxation of
 //       "min energy s.t. latency <= SLO"; lambda_0 = 0, the others a
-//       geometric grid over 1e-10 .. 1) and offers the plan.
+//       geometric grid over 1e-10 .. 1) and offers the plan.  Quality-primary
+//       objectives do the same per quality target (options below the target
+//       skipped) with the next FP criterion as the primary term.
 //   H2: best-improvement 1-opt from the incumbent, one (node, option) swap
-//       per thread, up to 4 passes.
+//       per thread, up to LOOM_FR_HPASS passes.
 template <int CL, int NB, typename L>
 __device__ void fr_incumbent(const BfsParams<NB>& P, const FrTab& T, FrShared& S) {
   const int n = P.n;
   Rec cand = S.best;
   uint64_t cdig = S.hdig;
   const int32_t c0 = fr_crit<CL>(P, 0);
-  if (P.n_crit > 0 && (c0 == kFpA || c0 == kFpB)) {
-    const double lam = threadIdx.x == 0 ? 0.0 : 1e-10 * exp10(10.0 * threadIdx.x / (kFrBlock - 1));
-    const double* g = c0 == kFpA ? T.ga : T.gb;
+  const int32_t c1 = fr_ncrit<CL>() > 1 ? fr_crit<CL>(P, 1) : kFrNone;
+  const bool fp_first = P.n_crit > 0 && (c0 == kFpA || c0 == kFpB);
+  const bool q_first = P.n_crit > 0 && c0 == kQual && P.n_qlev > 0;
+  if (fp_first || q_first) {
+    // quality first: thread t targets quality level t mod n_qlev (options
+    // below it are skipped where a node has one at or above it) and trades
+    // the next FP criterion against walls
+    const int nq = q_first ? P.n_qlev : 1;
+    const int li = static_cast<int>(threadIdx.x) / nq;
+    const int nl = (kFrBlock + nq - 1) / nq;
+    const int32_t qt = q_first ? P.qlev[threadIdx.x % nq] : INT_MIN;
+    const double lam = li == 0 ? 0.0 : 1e-10 * exp10(10.0 * li / max(1, nl - 1));
+    const int32_t cg = fp_first ? c0 : (c1 == kFpA || c1 == kFpB ? c1 : kFrNone);
+    const double* g = cg == kFpB ? T.gb : T.ga;
+    const double gs = cg == kFrNone ? 0.0 : 1.0;
     uint64_t dig = 0;
     for (int i = 0; i < n; ++i) {
       const int base = P.optoff[i];
       double bv = INFINITY;
       int64_t bw = INT64_MAX;
-      int bc = 0;
-      for (int sl = 0; sl < P.nok[i]; ++sl) {
-        const int c = T.perm[base + sl];
-        const int64_t w = T.wall[base + c];
-        const double v = g[base + c] + lam * static_cast<double>(w);
-        if (v < bv || (v == bv && w < bw)) {
-          bv = v;
-          bw = w;
-          bc = c;
+      int bc = -1;
+      for (int pass = 0; pass < 2 && bc < 0; ++pass)  // pass 1: the node has no option at the target
+        for (int sl = 0; sl < P.nok[i]; ++sl) {
+          const int c = T.perm[base + sl];
+          if (pass == 0 && T.q[base + c] < qt) continue;
+          const int64_t w = T.wall[base + c];
+          const double v = gs * g[base + c] + lam * static_cast<double>(w);
+          if (v < bv || (v == bv && w < bw)) {
+            bv = v;
+            bw = w;
+            bc = c;
+          }
         }
-      }
       dig |= static_cast<uint64_t>(bc) << P.shift[i];
     }
     const uint64_t before = cand.index;
@@ -576,7 +597,7 @@ __device__ void fr_incumbent(const BfsParams<NB>& P, const FrTab& T, FrShared& S
   int slots = 0;
   for (int i = 0; i < n; ++i) slots += P.nok[i];
 #pragma unroll 1
-  for (int pass = 0; pass < 5; ++pass) {
+  for (int pass = 0; pass <= LOOM_FR_HPASS; ++pass) {
     // the block's best; its owner publishes the packed digits
     const Rec b0 = S.best;
     const Rec cb = fr_block_best<CL>(P, cand, cand.found && (!b0.found || cand.index != b0.index), S.warp_slot);
@@ -588,7 +609,7 @@ __device__ void fr_incumbent(const BfsParams<NB>& P, const FrTab& T, FrShared& S
     if (!S.flag && pass > 0) break;
     if (S.flag && cand.found && cand.index == S.best.index) S.hdig = cdig;
     __syncthreads();
-    if (pass == 4 || !S.best.found) break;
+    if (pass == LOOM_FR_HPASS || !S.best.found) break;
     // H2: one swap per thread from the incumbent
     const uint64_t D = S.hdig;
     cand = S.best;

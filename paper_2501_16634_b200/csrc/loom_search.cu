@@ -2549,6 +2549,15 @@ void fill_fr_params(const Built& b, BfsParams<NB>& P) {
     P.twmin[t] = nok[x] ? bm[x].w : 0;
     P.twprim[t] = wall[optoff[x] + oprim[x]];
   }
+  {  // distinct qualities of the options meeting the floor, descending (quality-first heuristic)
+    std::vector<int32_t> ql;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < nok[i]; ++j) ql.push_back(qq[optoff[i] + perm[optoff[i] + j]]);
+    std::sort(ql.begin(), ql.end(), std::greater<int32_t>());
+    ql.erase(std::unique(ql.begin(), ql.end()), ql.end());
+    P.n_qlev = static_cast<int32_t>(std::min<size_t>(8, ql.size()));
+    for (int i = 0; i < P.n_qlev; ++i) P.qlev[i] = ql[i];
+  }
   uint64_t lp = 0, lw = 0, ip = 0, iw = 0;
   double sa = 0.0, sb = 0.0, fac = 1.0;
   int32_t sq = INT_MAX;
