@@ -683,6 +683,11 @@ __device__ __forceinline__ void fr_flush(FrOut& o) {
   __syncwarp();
 }
 
+// How the depth-first and sweep kernels follow a frontier launch.
+constexpr int32_t kFollowAlways = 0;  // launched after it on the stream; they retire at once unless it overflowed
+constexpr int32_t kFollowGraph = 1;   // behind the search graph's conditional node (cudaGraphSetConditional)
+constexpr int32_t kFollowHost = 2;    // launched by the host only after reading JobSync.pad == kBfsOverflow
+
 // One warp: expand parents [p0, p0 + np) of depth d (np <= 32) and evaluate
 // their children.  redundant: children go to o.sparse by child index.
 template <int CL, int NB, typename L>
@@ -754,7 +759,7 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     bfs_kernel(const uint8_t* __restrict__ blob, uint32_t blob_bytes, BfsSync* __restrict__ bs,
                FrontierEntry* __restrict__ buf0, FrontierEntry* __restrict__ buf1, uint64_t cap,
                Rec* __restrict__ slots, JobSync* __restrict__ sync, Rec* __restrict__ out,
-               cudaGraphConditionalHandle fallback, int32_t in_graph, const __grid_constant__ BfsParams<NB> P) {
+               cudaGraphConditionalHandle fallback, int32_t follow, const __grid_constant__ BfsParams<NB> P) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ FrShared S;
   load_blob(smem, blob, blob_bytes, &S.mbar);
@@ -944,11 +949,11 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     __threadfence();
     const bool of = __ldcg(&bs->overflow) != 0u;
     out[0] = S.best;
-    // Inside the search graph the fallback kernels sit behind a conditional
-    // node that runs only on overflow; in a plain stream they always follow
-    // and retire at once on kBnbDone.
-    if (in_graph) cudaGraphSetConditional(fallback, of ? 1u : 0u);
-    sync[0].pad = of ? kBfsOverflow : (in_graph ? 0u : kBnbDone);
+    // How the fallback kernels follow (FrFollow): always launched, retiring
+    // at once on kBnbDone; behind the search graph's conditional node, opened
+    // only on overflow; or launched by the host only on overflow.
+    if (follow == kFollowGraph) cudaGraphSetConditional(fallback, of ? 1u : 0u);
+    sync[0].pad = of ? kBfsOverflow : (follow == kFollowAlways ? kBnbDone : 0u);
     g_bfs_last[0] = __ldcg(&bs->evals);
     g_bfs_last[1] = of;
     g_bfs_last[2] = __ldcg(&bs->max_frontier);

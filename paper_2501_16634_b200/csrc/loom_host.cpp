@@ -130,10 +130,10 @@ void AgentLibrary::add_implementation(Implementation impl) {
 }
 
 void AgentLibrary::add_profile(ExecutionProfile p) {
-  const std::string who = "profile (" + p.implementation + ", " + p.sku + ")";
-  if (p.throughput <= 0) throw ValidationError(who + ": throughput must be > 0");
-  if (p.setup_seconds < 0) throw ValidationError(who + ": setup latency must be >= 0");
-  if (p.units < 1) throw ValidationError(who + ": units must be >= 1");
+  const auto who = [&] { return "profile (" + p.implementation + ", " + p.sku + ")"; };  // only built on error
+  if (p.throughput <= 0) throw ValidationError(who() + ": throughput must be > 0");
+  if (p.setup_seconds < 0) throw ValidationError(who() + ": setup latency must be >= 0");
+  if (p.units < 1) throw ValidationError(who() + ": units must be >= 1");
   if (!impls_.count(p.implementation))
     throw DanglingReferenceError("profile references unknown implementation '" + p.implementation + "'");
   if (!skus_.count(p.sku)) throw DanglingReferenceError("profile references unknown sku '" + p.sku + "'");
@@ -150,7 +150,170 @@ void AgentLibrary::add_profile(ExecutionProfile p) {
     v.push_back(&j->second);
 }
 
+namespace {
+// The library bundle without a DOM (the single-search drop-in parses one per
+// call).  The arrays are read into staging records, then registered in the
+// DOM reader's order (skus, agents, implementations, profiles) with the same
+// add_* calls, so every registration error is the DOM reader's.  Anything
+// unusual (escapes, duplicate keys, missing or mistyped fields) returns false
+// and from_json_text falls back to the DOM reader.
+struct SkuRec {
+  std::string id, cls;
+  double busy = 0, idle = 0, dollars = 0;
+};
+struct ImplRec {
+  std::string name, capability;
+  long long quality = 0;
+  std::vector<std::string> classes;
+};
+
+bool read_library_fast(const std::string& text, AgentLibrary& lib) {
+  loomjson::Cursor c(text);
+  std::vector<SkuRec> skus;
+  std::vector<std::string> caps;
+  std::vector<ImplRec> impls;
+  std::vector<ExecutionProfile> profs;
+  unsigned seen_top = 0;
+  // an array of objects: `member(field)` reads one field of the current element
+  auto objects = [&](auto&& begin, auto&& member, auto&& finish) {
+    if (!c.open('[')) return false;
+    if (c.empty(']')) return true;
+    for (bool more = true; more;) {
+      begin();
+      if (!c.open('{') || c.empty('}')) return false;
+      for (bool m = true; m;) {
+        std::string_view f;
+        if (!c.key(f) || !member(f) || !c.next('}', m)) return false;
+      }
+      if (!finish() || !c.next(']', more)) return false;
+    }
+    return true;
+  };
+  if (!c.open('{')) return false;
+  if (!c.empty('}'))
+    for (bool more = true; more;) {
+      std::string_view k;
+      if (!c.key(k)) return false;
+      unsigned bit = k == "skus" ? 1 : k == "agents" ? 2 : k == "implementations" ? 4 : k == "profiles" ? 8 : 0;
+      if (bit & seen_top) return false;
+      seen_top |= bit;
+      bool ok = true;
+      if (bit == 1) {
+        unsigned f = 0;
+        ok = objects([&] { skus.emplace_back(); f = 0; },
+                     [&](std::string_view n) {
+                       SkuRec& r = skus.back();
+                       unsigned b = n == "id" ? 1 : n == "class" ? 2 : n == "busy_watts_per_unit" ? 4
+                                    : n == "idle_watts_per_unit" ? 8 : n == "dollars_per_unit_hour" ? 16 : 0;
+                       if (b & f) return false;
+                       f |= b;
+                       switch (b) {
+                         case 1: return c.str(r.id);
+                         case 2: return c.str(r.cls);
+                         case 4: return c.num(r.busy);
+                         case 8: return c.num(r.idle);
+                         case 16: return c.num(r.dollars);
+                         default: return c.skip();
+                       }
+                     },
+                     [&] { return f == 31; });
+      } else if (bit == 2) {
+        unsigned f = 0;
+        ok = objects([&] { caps.emplace_back(); f = 0; },
+                     [&](std::string_view n) {
+                       if (n != "capability") return c.skip();
+                       if (f) return false;
+                       f = 1;
+                       return c.str(caps.back());
+                     },
+                     [&] { return f == 1; });
+      } else if (bit == 4) {
+        unsigned f = 0;
+        ok = objects([&] { impls.emplace_back(); f = 0; },
+                     [&](std::string_view n) {
+                       ImplRec& r = impls.back();
+                       unsigned b = n == "name" ? 1 : n == "capability" ? 2 : n == "quality" ? 4
+                                    : n == "supported_classes" ? 8 : 0;
+                       if (b & f) return false;
+                       f |= b;
+                       switch (b) {
+                         case 1: return c.str(r.name);
+                         case 2: return c.str(r.capability);
+                         case 4: return c.integer(r.quality);
+                         case 8: {
+                           if (!c.open('[')) return false;
+                           if (c.empty(']')) return true;
+                           for (bool m = true; m;) {
+                             r.classes.emplace_back();
+                             if (!c.str(r.classes.back()) || !c.next(']', m)) return false;
+                           }
+                           return true;
+                         }
+                         default: return c.skip();
+                       }
+                     },
+                     [&] { return f == 15; });
+      } else if (bit == 8) {
+        unsigned f = 0;
+        ok = objects([&] { profs.emplace_back(); f = 0; },
+                     [&](std::string_view n) {
+                       ExecutionProfile& r = profs.back();
+                       unsigned b = n == "implementation" ? 1 : n == "sku" ? 2 : n == "units" ? 4
+                                    : n == "throughput" ? 8 : n == "setup_seconds" ? 16 : 0;
+                       if (b & f) return false;
+                       f |= b;
+                       long long u = 0;
+                       switch (b) {
+                         case 1: return c.str(r.implementation);
+                         case 2: return c.str(r.sku);
+                         case 4:
+                           if (!c.integer(u) || u < INT_MIN || u > INT_MAX) return false;
+                           r.units = static_cast<int>(u);
+                           return true;
+                         case 8: return c.num(r.throughput);
+                         case 16: return c.num(r.setup_seconds);
+                         default: return c.skip();
+                       }
+                     },
+                     [&] { return (f & 15) == 15; });
+      } else {
+        ok = c.skip();
+      }
+      if (!ok || !c.next('}', more)) return false;
+    }
+  if (!c.end()) return false;
+  for (SkuRec& r : skus) {
+    HardwareSku sku;
+    sku.id = std::move(r.id);
+    sku.hardware_class = class_of(r.cls);
+    sku.busy_watts_per_unit = r.busy;
+    sku.idle_watts_per_unit = r.idle;
+    sku.dollars_per_unit_hour = r.dollars;
+    lib.add_sku(std::move(sku));
+  }
+  for (std::string& cap : caps) lib.add_capability(std::move(cap));
+  for (ImplRec& r : impls) {
+    Implementation impl;
+    impl.name = std::move(r.name);
+    impl.capability = std::move(r.capability);
+    if (r.quality < INT_MIN || r.quality > INT_MAX) return false;
+    impl.quality = static_cast<int>(r.quality);
+    for (const std::string& cl : r.classes) {
+      if (class_of(cl) == HardwareClass::cpu) impl.supports_cpu = true;
+      else impl.supports_gpu = true;
+    }
+    lib.add_implementation(std::move(impl));
+  }
+  for (ExecutionProfile& pr : profs) lib.add_profile(std::move(pr));
+  return true;
+}
+}  // namespace
+
 AgentLibrary AgentLibrary::from_json_text(const std::string& text) {
+  {
+    AgentLibrary fast;
+    if (read_library_fast(text, fast)) return fast;
+  }
   AgentLibrary lib;
   try {
     const Value j = loomjson::parse(text);

@@ -2649,18 +2649,18 @@ struct FrArgs {
   JobSync* ticket;
   Rec* out;
   cudaGraphConditionalHandle cond;
-  int32_t in_graph;
+  int32_t follow;
   void* params;
   void* ptrs[12];
   void** bind() {
-    void* a[12] = {&blob, &bytes, &bs, &b0, &b1, &cap, &slots, &ticket, &out, &cond, &in_graph, params};
+    void* a[12] = {&blob, &bytes, &bs, &b0, &b1, &cap, &slots, &ticket, &out, &cond, &follow, params};
     for (int i = 0; i < 12; ++i) ptrs[i] = a[i];
     return ptrs;
   }
 };
 
 int launch_fr(loom_ctx* c, FrPlan& f, const Built& b, const JobDesc& d, const uint8_t* d_blob, Rec* d_slots,
-              JobSync* d_ticket, Rec* d_out) {
+              JobSync* d_ticket, Rec* d_out, int32_t follow = kFollowAlways) {
   if (int rc = ensure_bfs(c)) return rc;
   FrontierEntry* b0 = c->d_front;
   FrontierEntry* b1 = c->d_front + c->front_cap;
@@ -2676,8 +2676,7 @@ int launch_fr(loom_ctx* c, FrPlan& f, const Built& b, const JobDesc& d, const ui
     pp = &f.p32;
   }
   cudaGraphConditionalHandle none = 0;
-  int32_t in_graph = 0;
-  void* args[] = {&d_blob, &bytes, &bs, &b0, &b1, &cap, &d_slots, &d_ticket, &d_out, &none, &in_graph, pp};
+  void* args[] = {&d_blob, &bytes, &bs, &b0, &b1, &cap, &d_slots, &d_ticket, &d_out, &none, &follow, pp};
   LOOM_CUDA(cudaLaunchCooperativeKernel(fr_fn(f.variant, f.cl), dim3(f.ctas), dim3(kFrBlock), args,
                                         fr_smem_bytes(b.blob.size()), c->stream));
   ++c->launches;
@@ -2963,12 +2962,27 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   if (int rc = ensure_host(c, 1)) return rc;
   if (int rc = set_smem(fn, smem_bytes(b.blob.size(), p->n_nodes, lazy_of(b)))) return rc;
   tr.mark("plan + buffers");
-  LOOM_CUDA(cudaMemcpyAsync(c->d_arena, b.blob.data(), b.blob.size(), cudaMemcpyHostToDevice, c->stream));
-  LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, &d, sizeof d, cudaMemcpyHostToDevice, c->stream));
+  // stage the image and the job descriptor in the pinned arena: async copies
+  // without the driver's pageable bounce (the previous call synchronised)
+  const size_t job_at = (b.blob.size() + 255) & ~size_t(255);
+  if (int rc = ensure_host_arena(c, job_at + sizeof d)) return rc;
+  std::memcpy(c->h_arena, b.blob.data(), b.blob.size());
+  std::memcpy(c->h_arena + job_at, &d, sizeof d);
+  LOOM_CUDA(cudaMemcpyAsync(c->d_arena, c->h_arena, b.blob.size(), cudaMemcpyHostToDevice, c->stream));
+  LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, c->h_arena + job_at, sizeof d, cudaMemcpyHostToDevice, c->stream));
   FrPlan fr;
   if (algo == kAlgoAuto) prepare_fr(c, b, fr);
   if (fr.variant) {
-    if (int rc = launch_fr(c, fr, b, d, c->d_arena, c->d_scratch, c->d_tickets, c->d_out)) return rc;
+    // the frontier search alone; the fallback kernels only if it overflowed
+    // (the host waits for the result anyway: one read of JobSync.pad decides)
+    if (int rc = launch_fr(c, fr, b, d, c->d_arena, c->d_scratch, c->d_tickets, c->d_out, kFollowHost)) return rc;
+    if (int rc = ensure_host(c, 2)) return rc;
+    LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+    LOOM_CUDA(cudaMemcpyAsync(&c->h_out[1].found, &c->d_tickets[0].pad, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                              c->stream));
+    LOOM_CUDA(cudaStreamSynchronize(c->stream));
+    tr.mark("frontier search");
+    if (static_cast<unsigned>(c->h_out[1].found) != kBfsOverflow) return finish_winner(p, c->h_out[0], out);
   } else if (algo == kAlgoAuto) {
     g_last_default_bfs = 0;
   }
@@ -3216,7 +3230,7 @@ int fr_graph_launch(loom_ctx* c, loom_device_problem* dp, const JobDesc& d, int 
   FrPlan& f = *dp->fr;
   if (int rc = ensure_bfs(c)) return rc;
   FrArgs A{dp->d_blob, static_cast<uint32_t>(dp->built.blob.size()), c->d_bfs, c->d_front, c->d_front + c->front_cap,
-           static_cast<uint64_t>(c->front_cap), dp->d_scratch, dp->d_ticket, dp->d_out, 0, 1, nullptr, {}};
+           static_cast<uint64_t>(c->front_cap), dp->d_scratch, dp->d_ticket, dp->d_out, 0, kFollowGraph, nullptr, {}};
   if (f.variant == 1) {
     set_fr_job(dp->built, d, f.p16);
     A.params = &f.p16;

@@ -786,7 +786,7 @@ def _json_call(fn, handle, dag: Any, library: Any, objective_: Any, bounds: Any)
     if isinstance(objective_, str) and not objective_.lstrip().startswith("{"):
         objective_ = {"constraint": objective_}
     need = C.c_size_t(0)
-    cap = 1 << 16
+    cap = 1 << 14  # grown on demand (the needed size comes back)
     buf = C.create_string_buffer(cap)
     rc = fn(handle, _text(dag), _text(library), _text(objective_), _text(bounds), buf, cap, C.byref(need))
     if rc != LOOM_OK and need.value > cap:
@@ -807,7 +807,7 @@ def exhaustive_search(dag: Any, library: Any, objective_: Any, bounds: Any, ctx:
     if isinstance(objective_, str) and not objective_.lstrip().startswith("{"):
         objective_ = {"constraint": objective_}
     need = C.c_size_t(0)
-    cap = 1 << 16
+    cap = 1 << 14  # grown on demand (the needed size comes back)
     buf = C.create_string_buffer(cap)
     rc = lib().loom_exhaustive_search_json(ctx.handle, _text(dag), _text(library), _text(objective_),
                                            _text(bounds), buf, cap, C.byref(need))
@@ -826,7 +826,7 @@ def estimate_config(dag: Any, library: Any, config: Any) -> dict:
     (config.hpp:66-117) + estimate (estimator.hpp:43-78) of one config point on
     the host; the ConfigEstimate as a dict (no plan_index)."""
     need = C.c_size_t(0)
-    cap = 1 << 16
+    cap = 1 << 14  # grown on demand (the needed size comes back)
     buf = C.create_string_buffer(cap)
     rc = lib().loom_estimate_config_json(_text(dag), _text(library), _text(config), buf, cap, C.byref(need))
     if rc != LOOM_OK and need.value > cap:
@@ -846,7 +846,7 @@ def greedy_search(dag: Any, library: Any, objective_: Any, bounds: Any, ctx: Con
     if isinstance(objective_, str) and not objective_.lstrip().startswith("{"):
         objective_ = {"constraint": objective_}
     need = C.c_size_t(0)
-    cap = 1 << 16
+    cap = 1 << 14  # grown on demand (the needed size comes back)
     buf = C.create_string_buffer(cap)
     rc = lib().loom_greedy_search_json(ctx.handle, _text(dag), _text(library), _text(objective_), _text(bounds),
                                        max_sweeps, buf, cap, C.byref(need))

@@ -277,3 +277,36 @@ def test_batch_lowering_cache_equals_plain_lowering(loomlib):
                     assert got.option(node, opt) == plain.option(node, opt)
             plain.close()
         batch.close()
+
+
+def test_library_fast_reader_equals_dom_reader(loomlib):
+    """AgentLibrary::from_json_text reads the library bundle with a DOM-free
+    cursor and falls back to the DOM reader on anything unusual; both must
+    give the same lowering (reordered / extra keys, escapes, whitespace) and
+    the same errors (duplicates, dangling references, bad classes)."""
+    import json
+    for w in (W.config1(), W.config2(), W.config3(), W.config5(n_nodes=5)) + tuple(W.config4(2)):
+        ref = loom.Lowered(w.dag, json.dumps(w.library), w.bounds)
+        lib = w.library
+        variants = [
+            json.dumps(lib, indent=2),
+            json.dumps({k: lib[k] for k in reversed(list(lib))}),  # section order: registration order is fixed
+            json.dumps(dict(lib, note="\\u0041 escaped", extra=[{"x": None}])).replace("escaped", "\\u0065"),
+            json.dumps({k: [dict(reversed(list(e.items())), comment="c") if isinstance(e, dict) else e for e in v]
+                        if isinstance(v, list) else v for k, v in lib.items()}),
+        ]
+        for text in variants:
+            got = loom.Lowered(w.dag, text, w.bounds)
+            assert got.radix == ref.radix and _tables(got) == _tables(ref)
+            assert got.config(got.total - 1)["identifier"] == ref.config(ref.total - 1)["identifier"]
+    w = W.config1()
+    lib = json.loads(json.dumps(w.library))
+    bad = []
+    d = json.loads(json.dumps(lib)); d["skus"].append(dict(d["skus"][0])); bad.append((d, loom.LoomError))
+    d = json.loads(json.dumps(lib)); d["profiles"][0]["sku"] = "nope"; bad.append((d, loom.LoomError))
+    d = json.loads(json.dumps(lib)); d["skus"][0]["class"] = "tpu"; bad.append((d, loom.SchemaError))
+    d = json.loads(json.dumps(lib)); del d["profiles"][0]["units"]; bad.append((d, loom.SchemaError))
+    d = json.loads(json.dumps(lib)); d["implementations"][0]["quality"] = 1.5; bad.append((d, loom.SchemaError))
+    for d, cls in bad:
+        with pytest.raises(cls):
+            loom.Lowered(w.dag, json.dumps(d), w.bounds)
