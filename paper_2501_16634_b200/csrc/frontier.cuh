@@ -67,6 +67,10 @@ __device__ unsigned long long g_bfs_trace[2 * (kMaxNodes + 2)];
 #endif
 __device__ unsigned long long g_fr_prof[8 * (kMaxNodes + 1)];
 __device__ unsigned long long g_fr_prof2[16];  // LOOM_FR_PROF=3: marks inside an expansion (depth 3, lane 0)
+#define FR_MARKH(i)                                                                                   \
+  do {                                                                                                \
+    if (LOOM_FR_PROF == 4 && blockIdx.x == 0 && threadIdx.x == 0) g_fr_prof2[i] = clock64();          \
+  } while (0)
 #define FR_MARK2(i)                                                                                   \
   do {                                                                                                \
     if (LOOM_FR_PROF == 3 && blockIdx.x == 0 && threadIdx.x == 0 && k == 3) g_fr_prof2[i] = clock64(); \
@@ -115,6 +119,8 @@ struct BfsParams {
   uint64_t seed_dig;  // its digits, packed like FrontierEntry.dig
   int32_t n_qlev;     // distinct option qualities (descending, at most 8): targets of the quality-first heuristic
   int32_t qlev[8];
+  double lam_lo;         // heuristic lambda grid: 0, then lam_lo .. lam_lo * 2^lam_log2_span geometrically
+  double lam_log2_span;
   // by topological position t
   int32_t tnode[NB];    // node at position t
   // pm[t][p] = ~0 if position p precedes position t by an edge, else 0;
@@ -157,6 +163,8 @@ struct FrTab {
   const int64_t* wall;
   const int32_t* q;
   const uint64_t* lexw;
+  const int32_t* optoff;  // per node (also in the parameters; these are for per-lane indexing)
+  const int32_t* nok;
 };
 
 // A parent being expanded: its prefix and the latency terms of the next node.
@@ -181,6 +189,8 @@ struct FrShared {
   int32_t last;
   int32_t flag;
   uint64_t hdig;  // packed digits of `best` during the incumbent heuristic
+  int32_t shift[kMaxNodes];  // BfsParams.shift / bits, for per-lane indexing
+  uint32_t bits[kMaxNodes];
   unsigned long long evals;
   unsigned long long leaves;
   unsigned long long maxf;
@@ -540,10 +550,10 @@ __device__ __forceinline__ Rec fr_block_best(const BfsParams<NB>& P, Rec r, bool
 // and only the pruning improves).  A good incumbent from the start shrinks
 // every frontier: searched from the true optimum, C3 under the 40 s SLO
 // evaluates 0.18M children instead of 2.0M.
-//   H1 (FP-primary objectives): thread t picks, per node, the option
-//       minimising primary term + lambda_t x wall (a Lagrangian relaxation of
-//       "min energy s.t. latency <= SLO"; lambda_0 = 0, the others a
-//       geometric grid over 1e-10 .. 1) and offers the plan.  Quality-primary
+//   H1 (FP-primary objectives): 64 plans, each picking per node the option
+//       minimising primary term + lambda x wall (a Lagrangian relaxation of
+//       "min energy s.t. latency <= SLO"; lambda = 0 and a geometric grid
+//       over 1e-10 .. 1; one warp per plan, one lane per node).  Quality-primary
 //       objectives do the same per quality target (options below the target
 //       skipped) with the next FP criterion as the primary term.
 //   H2: best-improvement 1-opt from the incumbent, one (node, option) swap
@@ -551,6 +561,7 @@ __device__ __forceinline__ Rec fr_block_best(const BfsParams<NB>& P, Rec r, bool
 template <int CL, int NB, typename L>
 __device__ void fr_incumbent(const BfsParams<NB>& P, const FrTab& T, FrShared& S) {
   const int n = P.n;
+  FR_MARKH(0);
   Rec cand = S.best;
   uint64_t cdig = S.hdig;
   const int32_t c0 = fr_crit<CL>(P, 0);
@@ -558,44 +569,83 @@ __device__ void fr_incumbent(const BfsParams<NB>& P, const FrTab& T, FrShared& S
   const bool fp_first = P.n_crit > 0 && (c0 == kFpA || c0 == kFpB);
   const bool q_first = P.n_crit > 0 && c0 == kQual && P.n_qlev > 0;
   if (fp_first || q_first) {
-    // quality first: thread t targets quality level t mod n_qlev (options
-    // below it are skipped where a node has one at or above it) and trades
-    // the next FP criterion against walls
+    // kHR rounds; in round r warp w takes combination r * warps + w (a
+    // lambda and, quality first, a quality target: options below it are
+    // skipped where a node has one at or above it; the next FP criterion is
+    // the primary term), lane i chooses node i's option, and lane r keeps
+    // the round's plan; then lanes 0..kHR-1 evaluate their plans at once
+    constexpr int kHR = 4;
+    constexpr int kCombos = kHR * kFrWarps;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nq = q_first ? P.n_qlev : 1;
-    const int li = static_cast<int>(threadIdx.x) / nq;
-    const int nl = (kFrBlock + nq - 1) / nq;
-    const int32_t qt = q_first ? P.qlev[threadIdx.x % nq] : INT_MIN;
-    const double lam = li == 0 ? 0.0 : 1e-10 * exp10(10.0 * li / max(1, nl - 1));
+    const int nl = (kCombos + nq - 1) / nq;
     const int32_t cg = fp_first ? c0 : (c1 == kFpA || c1 == kFpB ? c1 : kFrNone);
     const double* g = cg == kFpB ? T.gb : T.ga;
     const double gs = cg == kFrNone ? 0.0 : 1.0;
-    uint64_t dig = 0;
-    for (int i = 0; i < n; ++i) {
-      const int base = P.optoff[i];
-      double bv = INFINITY;
-      int64_t bw = INT64_MAX;
-      int bc = -1;
-      for (int pass = 0; pass < 2 && bc < 0; ++pass)  // pass 1: the node has no option at the target
-        for (int sl = 0; sl < P.nok[i]; ++sl) {
-          const int c = T.perm[base + sl];
-          if (pass == 0 && T.q[base + c] < qt) continue;
-          const int64_t w = T.wall[base + c];
-          const double v = gs * g[base + c] + lam * static_cast<double>(w);
-          if (v < bv || (v == bv && w < bw)) {
-            bv = v;
-            bw = w;
-            bc = c;
+    const int base = lane < n ? T.optoff[lane] : 0;
+    const int nr = lane < n ? T.optoff[lane + 1] - base : 0;  // raw options: the floor-failing ones carry
+    const int sh = lane < n ? S.shift[lane] : 0;              // walls above any SLO and are skipped
+    double lam[kHR];
+    int32_t qt[kHR];
+#pragma unroll
+    for (int r = 0; r < kHR; ++r) {
+      const int combo = r * kFrWarps + warp;
+      const int li = combo / nq;
+      qt[r] = q_first ? P.qlev[combo % nq] : INT_MIN;
+      lam[r] = li == 0 ? 0.0 : P.lam_lo * exp2(P.lam_log2_span * li / max(1, nl - 1));
+    }
+    double bv[kHR];
+    int64_t bw[kHR];
+    int bc[kHR];
+#pragma unroll
+    for (int r = 0; r < kHR; ++r) {
+      bv[r] = INFINITY;
+      bw[r] = INT64_MAX;
+      bc[r] = -1;
+    }
+    // one scan of the node's options serves the kHR plans
+    for (int relax = 0; relax < 2; ++relax) {  // relax 1: plans whose target no option of the node meets
+#pragma unroll 4
+      for (int o = 0; o < nr; ++o) {
+        const int64_t w = T.wall[base + o];
+        if (w > P.slo_eff) continue;
+        const double gv = gs * g[base + o];
+        const int32_t qo = T.q[base + o];
+#pragma unroll
+        for (int r = 0; r < kHR; ++r) {
+          if (relax ? bc[r] >= 0 : qo < qt[r]) continue;
+          const double v = gv + lam[r] * static_cast<double>(w);
+          if (v < bv[r] || (v == bv[r] && w < bw[r])) {
+            bv[r] = v;
+            bw[r] = w;
+            bc[r] = o;
           }
         }
-      dig |= static_cast<uint64_t>(bc) << P.shift[i];
+      }
+      bool all = true;
+#pragma unroll
+      for (int r = 0; r < kHR; ++r) all &= bc[r] >= 0 || nr == 0;
+      if (__all_sync(0xffffffffu, all)) break;
     }
-    const uint64_t before = cand.index;
-    const int32_t bf = cand.found;
-    fr_offer_plan<CL, NB, L>(P, T, dig, cand);
-    if (cand.found && (!bf || cand.index != before)) cdig = dig;
+    uint64_t mine = 0;
+#pragma unroll
+    for (int r = 0; r < kHR; ++r) {
+      const uint64_t part = bc[r] > 0 ? static_cast<uint64_t>(bc[r]) << sh : 0;  // (option 0 packs as 0)
+      const uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(part));
+      const uint32_t hi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(part >> 32));
+      if (lane == r) mine = static_cast<uint64_t>(hi) << 32 | lo;
+    }
+    FR_MARKH(1);
+    if (lane < kHR) {
+      const uint64_t before = cand.index;
+      const int32_t bf = cand.found;
+      fr_offer_plan<CL, NB, L>(P, T, mine, cand);
+      if (cand.found && (!bf || cand.index != before)) cdig = mine;
+    }
+    FR_MARKH(2);
   }
   int slots = 0;
-  for (int i = 0; i < n; ++i) slots += P.nok[i];
+  for (int i = 0; i < n; ++i) slots += T.nok[i];
 #pragma unroll 1
   for (int pass = 0; pass <= LOOM_FR_HPASS; ++pass) {
     // the block's best; its owner publishes the packed digits
@@ -609,6 +659,7 @@ __device__ void fr_incumbent(const BfsParams<NB>& P, const FrTab& T, FrShared& S
     if (!S.flag && pass > 0) break;
     if (S.flag && cand.found && cand.index == S.best.index) S.hdig = cdig;
     __syncthreads();
+    FR_MARKH(3 + 2 * pass);
     if (pass == LOOM_FR_HPASS || !S.best.found) break;
     // H2: one swap per thread from the incumbent
     const uint64_t D = S.hdig;
@@ -616,16 +667,17 @@ __device__ void fr_incumbent(const BfsParams<NB>& P, const FrTab& T, FrShared& S
     cdig = D;
     for (int u = threadIdx.x; u < slots; u += kFrBlock) {
       int i = 0, acc = 0;
-      while (u >= acc + P.nok[i]) acc += P.nok[i++];
-      const int c = T.perm[P.optoff[i] + (u - acc)];
-      const uint64_t dig = (D & ~(static_cast<uint64_t>(P.bits[i]) << P.shift[i])) |
-                           (static_cast<uint64_t>(c) << P.shift[i]);
+      while (u >= acc + T.nok[i]) acc += T.nok[i++];  // (shared memory: lanes index different nodes)
+      const int c = T.perm[T.optoff[i] + (u - acc)];
+      const uint64_t dig = (D & ~(static_cast<uint64_t>(S.bits[i]) << S.shift[i])) |
+                           (static_cast<uint64_t>(c) << S.shift[i]);
       if (dig == D) continue;
       const uint64_t before = cand.index;
       const int32_t bf = cand.found;
       fr_offer_plan<CL, NB, L>(P, T, dig, cand);
       if (cand.found && (!bf || cand.index != before)) cdig = dig;
     }
+    FR_MARKH(4 + 2 * pass);
   }
 }
 
@@ -683,6 +735,11 @@ __device__ __forceinline__ void fr_flush(FrOut& o) {
   __syncwarp();
 }
 
+// What a warp does with its batch of parents (fr_batch).
+constexpr int kBatchAll = 0;       // expansion (three jobs) and children
+constexpr int kBatchExpand = 1;    // job 0 and the children
+constexpr int kBatchComplete = 2;  // the two completions only
+
 // How the depth-first and sweep kernels follow a frontier launch.
 constexpr int32_t kFollowAlways = 0;  // launched after it on the stream; they retire at once unless it overflowed
 constexpr int32_t kFollowGraph = 1;   // behind the search graph's conditional node (cudaGraphSetConditional)
@@ -692,16 +749,19 @@ constexpr int32_t kFollowHost = 2;    // launched by the host only after reading
 // their children.  redundant: children go to o.sparse by child index.
 template <int CL, int NB, typename L>
 __device__ __forceinline__ void fr_batch(const BfsParams<NB>& P, const FrTab& T, const FrontierEntry* parents,
-                                         uint64_t p0, int np, int d, bool leaf, bool redundant, unsigned magic, FrPar* pb, Rec& cand,
-                                         FrOut& o, unsigned long long& evals, unsigned long long& leaves) {
+                                         uint64_t p0, int np, int d, bool leaf, bool redundant, int mode,
+                                         unsigned magic, FrPar* pb, Rec& cand, FrOut& o, unsigned long long& evals,
+                                         unsigned long long& leaves) {
   const int lane = threadIdx.x & 31;
   { const int k = d; FR_MARK2(0); }
   const Rec before = cand;
-  // a small batch gives each parent three lanes (one job each), else one
-  const bool split = np * 3 <= 32;
-  const int pl = split ? lane / 3 : lane;
-  const int j0 = split ? lane - 3 * pl : 0;
-  const int j1 = split ? j0 : 2;
+  // mode kBatchAll: a small batch gives each parent three lanes (one job
+  // each), else one lane runs the three jobs; kBatchExpand: job 0 and the
+  // children only; kBatchComplete: jobs 1 and 2 (two lanes per parent) only
+  const bool split = mode == kBatchAll && np * 3 <= 32;
+  const int pl = mode == kBatchComplete ? lane >> 1 : split ? lane / 3 : lane;
+  const int j0 = mode == kBatchComplete ? 1 + (lane & 1) : split ? lane - 3 * pl : 0;
+  const int j1 = mode == kBatchAll && !split ? 2 : j0;
   FrPar fp;
   fp.live = 0;
   if (pl < np) {
@@ -715,6 +775,7 @@ __device__ __forceinline__ void fr_batch(const BfsParams<NB>& P, const FrTab& T,
   }
   FR_MARK(d, 1);
   { const int k = d; FR_MARK2(6); }
+  if (mode == kBatchComplete) return;  // its plans reach the level's reduction through cand
   if (j0 == 0 && pl < 32) pb[pl] = fp;
   // plans found while expanding prune the children of the whole warp
   if (__any_sync(0xffffffffu, cand.index != before.index || cand.found != before.found)) fr_warp_best<CL>(P, cand);
@@ -762,9 +823,11 @@ __global__ void __launch_bounds__(kFrBlock, 1)
                cudaGraphConditionalHandle fallback, int32_t follow, const __grid_constant__ BfsParams<NB> P) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ FrShared S;
+  FR_MARKH(14);
   load_blob(smem, blob, blob_bytes, &S.mbar);
+  FR_MARKH(15);
   const BnbView B = make_bnb_view(smem);
-  const FrTab T{B.perm, B.v.ga, B.v.gb, B.v.wall, B.v.q, B.v.lexw};
+  const FrTab T{B.perm, B.v.ga, B.v.gb, B.v.wall, B.v.q, B.v.lexw, B.v.optoff, B.nok};
   const int n = P.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t img = (blob_bytes + 127) & ~127u;
@@ -780,6 +843,10 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     }
     S.best = P.has_seed ? P.seed : Rec{0, 0, 0, 0, 0, 0, 0};
     S.hdig = P.seed_dig;
+    for (int i = 0; i < n; ++i) {
+      S.shift[i] = P.shift[i];
+      S.bits[i] = P.bits[i];
+    }
     S.stop = 0;
     S.ncur = 1;
     S.evals = S.leaves = S.maxf = 0;
@@ -788,7 +855,9 @@ __global__ void __launch_bounds__(kFrBlock, 1)
   bool empty = n == 0;
   for (int i = 0; i < n; ++i) empty |= P.nok[i] == 0;
   __syncthreads();
+  FR_MARKH(12);
   if (!empty && LOOM_FR_HEUR) fr_incumbent<CL, NB, L>(P, T, S);
+  FR_MARKH(13);
 
   unsigned long long evals = 0, leaves = 0;
   const FrontierEntry* cur = sA;  // parents of the level
@@ -818,11 +887,21 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     // parents, the first one static (warp id), the rest dealt by an atomic
     // counter.
     uint64_t p, lim, npb;
+    // a small distributed level (at most one parent per two warps): one
+    // warp expands a parent while another evaluates its two completions,
+    // so neither waits for the other's divergent path
+    const bool sep = !redundant && 2 * n_cur <= nwarps;
+    int mode = kBatchAll;
     if (redundant) {
       const uint64_t per = (n_cur + kFrWarps - 1) / kFrWarps;
       p = static_cast<uint64_t>(warp) * per;
       lim = umin64(n_cur, p + per);
       npb = 32;
+    } else if (sep) {
+      npb = 1;
+      mode = gwarp < n_cur ? kBatchExpand : kBatchComplete;
+      p = gwarp < n_cur ? gwarp : gwarp - n_cur;
+      lim = gwarp < 2 * n_cur ? p + 1 : 0;
     } else {
       // about two batches per warp: the dynamic deal evens out the tail
       npb = umin64(32, umax64(1, (n_cur + 2 * nwarps - 1) / (2 * nwarps)));
@@ -833,11 +912,12 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     // distributed: the next batch is claimed before this one is processed,
     // so the atomic's round trip overlaps the work
     unsigned long long g = 0;
-    if (!redundant && lane == 0 && p < lim) g = atomicAdd(&bs->next[d], static_cast<unsigned long long>(npb));
+    const bool dyn = !redundant && !sep;
+    if (dyn && lane == 0 && p < lim) g = atomicAdd(&bs->next[d], static_cast<unsigned long long>(npb));
     while (p < lim) {
-      fr_batch<CL, NB, L>(P, T, cur, p, static_cast<int>(umin64(npb, lim - p)), d, leaf, redundant, magic, pb, cand, o,
-                      e0, l0);
-      if (redundant) {
+      fr_batch<CL, NB, L>(P, T, cur, p, static_cast<int>(umin64(npb, lim - p)), d, leaf, redundant, mode, magic, pb,
+                          cand, o, e0, l0);
+      if (!dyn) {
         p += npb;
       } else {
         p = nwarps * npb + __shfl_sync(0xffffffffu, g, 0);

@@ -2557,6 +2557,9 @@ void fill_fr_params(const Built& b, BfsParams<NB>& P) {
     ql.erase(std::unique(ql.begin(), ql.end()), ql.end());
     P.n_qlev = static_cast<int32_t>(std::min<size_t>(8, ql.size()));
     for (int i = 0; i < P.n_qlev; ++i) P.qlev[i] = ql[i];
+    // lambda grid of the heuristic: 1e-10 .. 1 over its plans (frontier.cuh fr_incumbent)
+    P.lam_lo = 1e-10;
+    P.lam_log2_span = std::log2(1e10);
   }
   uint64_t lp = 0, lw = 0, ip = 0, iw = 0;
   double sa = 0.0, sb = 0.0, fac = 1.0;
