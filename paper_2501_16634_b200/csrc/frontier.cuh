@@ -61,19 +61,16 @@ __device__ unsigned long long g_bfs_last[6];  // evidence of the last frontier l
 __device__ unsigned long long g_bfs_trace[2 * (kMaxNodes + 2)];
 
 // LOOM_FR_PROF=1 (experiment builds): clock64() marks of CTA 0 / thread 0 at
-// phase boundaries, g_fr_prof[8 * depth + mark] (loom_debug_fr_prof).
+// phase boundaries, g_fr_prof[8 * depth + mark] (loom_debug_fr_prof); =4
+// also marks the incumbent heuristic's phases (loom_debug_fr_prof2).
 #ifndef LOOM_FR_PROF
 #define LOOM_FR_PROF 0
 #endif
 __device__ unsigned long long g_fr_prof[8 * (kMaxNodes + 1)];
-__device__ unsigned long long g_fr_prof2[16];  // LOOM_FR_PROF=3: marks inside an expansion (depth 3, lane 0)
+__device__ unsigned long long g_fr_prof2[16];  // LOOM_FR_PROF=4: marks of the incumbent heuristic (CTA 0, thread 0)
 #define FR_MARKH(i)                                                                                   \
   do {                                                                                                \
     if (LOOM_FR_PROF == 4 && blockIdx.x == 0 && threadIdx.x == 0) g_fr_prof2[i] = clock64();          \
-  } while (0)
-#define FR_MARK2(i)                                                                                   \
-  do {                                                                                                \
-    if (LOOM_FR_PROF == 3 && blockIdx.x == 0 && threadIdx.x == 0 && k == 3) g_fr_prof2[i] = clock64(); \
   } while (0)
 #define FR_MARK(d, i)                                                                                   \
   do {                                                                                                  \
@@ -354,7 +351,6 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
     }
     if (pj && fr_worse_before_lat<CL>(P, quantize_dev(a), quantize_dev(b), q, cand)) return;
   }
-  FR_MARK2(1);
   if (job == 2 && have_terms) {  // job 0 ran on this lane: the smallest-wall completion's latency is the bound
     const int64_t lat = max(out.lnot, out.head + P.twmin[xpos] + out.tail);
     fr_offer<CL>(P, T, e.dig, k, 2, a, b, q, lat, cand);
@@ -369,7 +365,6 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
     if (P.tnode[t] < k)
       W[t] = static_cast<L>(T.wall[P.toptoff[t] + static_cast<int>((e.dig >> P.tshift[t]) & P.tbits[t])]);
   }
-  FR_MARK2(2);
   // forward; job 0 removes node k
   L F[NB];
   L lmax = 0, head = 0;
@@ -385,7 +380,6 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
     F[t] = x ? kGone : st + W[t];
     lmax = max(lmax, F[t]);
   }
-  FR_MARK2(3);
   if (job != 0) {
     fr_offer<CL>(P, T, e.dig, k, job, a, b, q, static_cast<int64_t>(lmax), cand);
     return;
@@ -400,7 +394,6 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
       F[t] = m + W[t];
     }
   }
-  FR_MARK2(4);
   L tail = 0;
 #pragma unroll
   for (int s2 = 1; s2 < NB; ++s2)
@@ -413,7 +406,6 @@ __device__ __forceinline__ void fr_job(const BfsParams<NB>& P, const FrTab& T, c
   out.head = head;
   out.tail = tail;
   out.live = 1;
-  FR_MARK2(5);
 }
 
 // Exact record of the complete plan `dig` (every digit set), offered to
@@ -753,7 +745,6 @@ __device__ __forceinline__ void fr_batch(const BfsParams<NB>& P, const FrTab& T,
                                          unsigned magic, FrPar* pb, Rec& cand, FrOut& o, unsigned long long& evals,
                                          unsigned long long& leaves) {
   const int lane = threadIdx.x & 31;
-  { const int k = d; FR_MARK2(0); }
   const Rec before = cand;
   // mode kBatchAll: a small batch gives each parent three lanes (one job
   // each), else one lane runs the three jobs; kBatchExpand: job 0 and the
@@ -774,7 +765,6 @@ __device__ __forceinline__ void fr_batch(const BfsParams<NB>& P, const FrTab& T,
     }
   }
   FR_MARK(d, 1);
-  { const int k = d; FR_MARK2(6); }
   if (mode == kBatchComplete) return;  // its plans reach the level's reduction through cand
   if (j0 == 0 && pl < 32) pb[pl] = fp;
   // plans found while expanding prune the children of the whole warp

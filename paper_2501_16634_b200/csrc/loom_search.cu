@@ -2452,9 +2452,10 @@ struct FrPlan {
   BfsParams<16> p16;
   BfsParams<32> p32;
   // Search graph of a device problem: frontier kernel -> conditional node
-  // {depth-first kernel -> sweep kernel} (taken only on frontier overflow)
-  // -> D2H of the winner.  One graph launch per search instead of three
-  // kernel launches and a copy; rebuilt when the sweep's grid changes.
+  // {depth-first kernel -> sweep kernel} (taken only on frontier overflow).
+  // The winner record is mapped pinned memory, so no copy follows.  One
+  // graph launch per search instead of three kernel launches and a copy;
+  // rebuilt when the sweep's grid changes.
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraphNode_t kn = nullptr;
@@ -3001,6 +3002,7 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
   ++c->launches;
   LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
   tr.mark("copies + launches");
+  tr.mark("enqueue");
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   tr.mark("device");
   return finish_winner(p, c->h_out[0], out);
@@ -3090,6 +3092,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
       all.push_back(d);
     }
   }
+  tr.mark("descriptors");
   LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, all.data(), all.size() * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
   // Branch and bound over every job (one CTA per job, `all` order); each
   // group's sweep launch below then retires the jobs it settled.
@@ -3123,6 +3126,7 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
     first += nj;
   }
   LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, all.size() * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+  tr.mark("enqueue");
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   tr.mark("device");
   std::vector<std::pair<int, size_t>> order;  // (job, slot in h_out)
@@ -3191,7 +3195,10 @@ int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective
              cudaMalloc(&dp->d_bsync, sizeof(BnbSync)) == cudaSuccess &&
              cudaMemset(dp->d_bsync, 0, sizeof(BnbSync)) == cudaSuccess &&
              cudaMalloc(&dp->d_ticket, sizeof(JobSync)) == cudaSuccess &&
-             cudaMalloc(&dp->d_out, sizeof(Rec)) == cudaSuccess && cudaMallocHost(&dp->h_out, sizeof(Rec)) == cudaSuccess &&
+             // the winner record lives in mapped pinned memory: the kernels write it
+             // straight to the host (no copy node / copy launch per search)
+             cudaHostAlloc(&dp->h_out, sizeof(Rec), cudaHostAllocMapped) == cudaSuccess &&
+             cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp->d_out), dp->h_out, 0) == cudaSuccess &&
              cudaEventCreateWithFlags(&dp->done, cudaEventDisableTiming) == cudaSuccess &&
              cudaMemcpy(dp->d_blob, dp->built.blob.data(), dp->built.blob.size(), cudaMemcpyHostToDevice) ==
                  cudaSuccess &&
@@ -3211,8 +3218,7 @@ int loom_problem_release(loom_device_problem* dp) {
   cudaFree(dp->d_scratch);
   cudaFree(dp->d_ticket);
   cudaFree(dp->d_bsync);
-  cudaFree(dp->d_out);
-  if (dp->h_out) cudaFreeHost(dp->h_out);
+  if (dp->h_out) cudaFreeHost(dp->h_out);  // (d_out is its device alias)
   if (dp->done) cudaEventDestroy(dp->done);
   delete dp->fr;
   delete dp;
@@ -3297,8 +3303,6 @@ int fr_graph_launch(loom_ctx* c, loom_device_problem* dp, const JobDesc& d, int 
     sp.sharedMemBytes = static_cast<unsigned>(smem_bytes(dp->built.blob.size(), dp->host.n_nodes, lazy_of(dp->built)));
     sp.kernelParams = sa;
     LOOM_CUDA(cudaGraphAddKernelNode(&b2, body, b1 ? &b1 : nullptr, b1 ? 1 : 0, &sp));
-    cudaGraphNode_t mn = nullptr;
-    LOOM_CUDA(cudaGraphAddMemcpyNode1D(&mn, f.graph, &cn, 1, dp->h_out, dp->d_out, sizeof(Rec), cudaMemcpyDeviceToHost));
     LOOM_CUDA(cudaGraphInstantiate(&f.exec, f.graph, 0));
     f.sweep_ctas = sweep_ctas;
   } else {  // the same graph, this search's job fields (range, incumbent)
@@ -3350,8 +3354,7 @@ int search_async_impl(loom_ctx* c, loom_device_problem* dp, uint64_t begin, uint
                                                              dp->d_ticket, dp->d_out, dp->built.ip);
   LOOM_CUDA(cudaGetLastError());
   ++c->launches;
-  LOOM_CUDA(cudaMemcpyAsync(dp->h_out, dp->d_out, sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
-  LOOM_CUDA(cudaEventRecord(dp->done, c->stream));
+  LOOM_CUDA(cudaEventRecord(dp->done, c->stream));  // the winner reaches dp->h_out directly (mapped)
   return LOOM_OK;
 }
 

@@ -37,12 +37,8 @@ for d in range(lw.problem.n_nodes):
     print(d, " | ".join(segs), "| to next level", (nxt - prev) if nxt > prev else "")
 
 b2 = (C.c_uint64 * 16)()
-if loom.lib().loom_debug_fr_prof2(b2) == 0 and b2[0]:
-    m = list(b2)
-    print("depth-3 expansion, lane 0 (job 0): batch start -> folds", m[1] - m[0], "| W", m[2] - m[1],
-          "| forward", m[3] - m[2], "| backward", m[4] - m[3], "| tail+store", m[5] - m[4], "| warp done", m[6] - m[5])
-
-if b2[14] and b2[12]:
+lib_ok = loom.lib().loom_debug_fr_prof2(b2) == 0
+if lib_ok and b2[14] and b2[12]:
     m = list(b2)
     d = lambda a, b: (m[b] - m[a]) if m[a] and m[b] and m[b] >= m[a] else None  # noqa: E731
     print("LOOM_FR_PROF=4 (cycles): blob load", d(14, 15), "| prologue", d(15, 12), "| heuristic", d(12, 13),
