@@ -572,7 +572,10 @@ def other_configs(ctx, loom, W, issue: float) -> dict:
         out[name] = {"time_to_plan_ms": 1e3 * min(ts), "plans": r["plans"], "identifier": r["identifier"],
                      "latency_us": r["latency_us"], "gpu_wh": r["gpu_wh"]}
     jobs = W.config4(10_000)
-    dags = [json.dumps(j.dag) for j in jobs]
+    # the tenants' dag.json texts as the bytes a caller hands the C ABI (a
+    # Python str would be re-encoded per call: ~5 ms of interpreter work for
+    # 10,000 texts that is not the library's)
+    dags = [json.dumps(j.dag).encode() for j in jobs]
     lib_t, bounds_t = json.dumps(jobs[0].library), json.dumps(jobs[0].bounds)
     gold_p = ROOT / "tests" / "golden" / "c4" / "all_jobs.json"
     gold = json.loads(gold_p.read_text())["objectives"] if gold_p.exists() else {}

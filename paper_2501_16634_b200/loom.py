@@ -244,6 +244,10 @@ def _check(rc: int) -> None:
 
 
 def _text(x: Any) -> bytes:
+    """JSON text for the C ABI: bytes pass through, str is encoded, anything
+    else is serialised."""
+    if isinstance(x, (bytes, bytearray)):
+        return bytes(x)
     return (x if isinstance(x, str) else json.dumps(x)).encode()
 
 
