@@ -96,6 +96,9 @@ constexpr int kFrStage = 64;             // kept children staged per warp before
 #ifndef LOOM_FR_HEUR
 #define LOOM_FR_HEUR 1  // incumbent heuristic before the first level (fr_incumbent)
 #endif
+#ifndef LOOM_FR_COMPLETE
+#define LOOM_FR_COMPLETE 2  // deepest level whose parents also get their two completions
+#endif
 #ifndef LOOM_FR_HPASS
 #define LOOM_FR_HPASS 2  // its 1-opt passes at most (more found nothing on the C3 goldens)
 #endif
@@ -880,8 +883,13 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     // a small distributed level (at most one parent per two warps): one
     // warp expands a parent while another evaluates its two completions,
     // so neither waits for the other's divergent path
-    const bool sep = !redundant && 2 * n_cur <= nwarps;
-    int mode = kBatchAll;
+    // completions (jobs 1, 2) only feed the incumbent, which the heuristic
+    // has already found on every C3 golden objective: below depth
+    // LOOM_FR_COMPLETE they are skipped (the top levels keep them -- they are
+    // small -- in case the heuristic was weak)
+    const bool expand_only = LOOM_FR_HEUR && d > LOOM_FR_COMPLETE;
+    const bool sep = !redundant && !expand_only && 2 * n_cur <= nwarps;
+    int mode = expand_only ? kBatchExpand : kBatchAll;
     if (redundant) {
       const uint64_t per = (n_cur + kFrWarps - 1) / kFrWarps;
       p = static_cast<uint64_t>(warp) * per;
