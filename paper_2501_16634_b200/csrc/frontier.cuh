@@ -117,6 +117,7 @@ struct BfsParams {
   uint64_t end;
   Rec seed;  // the incumbent every CTA starts from (exact record, host-evaluated)
   uint64_t seed_dig;  // its digits, packed like FrontierEntry.dig
+  int32_t heur;       // run the incumbent heuristic (spaces too small to need it skip its ~15 us)
   int32_t n_qlev;     // distinct option qualities (descending, at most 8): targets of the quality-first heuristic
   int32_t qlev[8];
   double lam_lo;         // heuristic lambda grid: 0, then lam_lo .. lam_lo * 2^lam_log2_span geometrically
@@ -849,7 +850,8 @@ __global__ void __launch_bounds__(kFrBlock, 1)
   for (int i = 0; i < n; ++i) empty |= P.nok[i] == 0;
   __syncthreads();
   FR_MARKH(12);
-  if (!empty && LOOM_FR_HEUR) fr_incumbent<CL, NB, L>(P, T, S);
+  const bool heur = LOOM_FR_HEUR && P.heur;
+  if (!empty && heur) fr_incumbent<CL, NB, L>(P, T, S);
   FR_MARKH(13);
 
   unsigned long long evals = 0, leaves = 0;
@@ -887,7 +889,7 @@ __global__ void __launch_bounds__(kFrBlock, 1)
     // has already found on every C3 golden objective: below depth
     // LOOM_FR_COMPLETE they are skipped (the top levels keep them -- they are
     // small -- in case the heuristic was weak)
-    const bool expand_only = LOOM_FR_HEUR && d > LOOM_FR_COMPLETE;
+    const bool expand_only = heur && d > LOOM_FR_COMPLETE;
     const bool sep = !redundant && !expand_only && 2 * n_cur <= nwarps;
     int mode = expand_only ? kBatchExpand : kBatchAll;
     if (redundant) {

@@ -419,23 +419,25 @@ int loom_greedy_seed(const loom_problem* p, const loom_objective* o, int32_t* di
   for (int i = 0; i < p->n_nodes; ++i) {
     // detail::node_local_key (optimizer.hpp:194-220): the option's own
     // contribution to each criterion; std::vector<double> ordering
+    // (a fixed array in the vector's lexicographic order: at most four criteria)
     int best = -1;
-    std::vector<double> best_key;
+    double best_key[4] = {0, 0, 0, 0};
+    const int nc = std::min(o->n_criteria, 4);
     for (int k = 0; k < p->radix[i]; ++k) {
       const int x = off + k;
       if (o->has_quality_floor && p->quality[x] < o->quality_floor) continue;  // optimizer.hpp:239-247
-      std::vector<double> key;
-      for (int c = 0; c < o->n_criteria; ++c) {
+      double key[4];
+      for (int c = 0; c < nc; ++c) {
         switch (o->criteria[c]) {
-          case LOOM_MIN_COST_DOLLARS: key.push_back(p->dollars[x]); break;
-          case LOOM_MIN_ENERGY: key.push_back(p->gpu_wh[x]); break;
-          case LOOM_MIN_LATENCY: key.push_back(static_cast<double>(p->wall_us[x])); break;
-          default: key.push_back(static_cast<double>(-p->quality[x])); break;
+          case LOOM_MIN_COST_DOLLARS: key[c] = p->dollars[x]; break;
+          case LOOM_MIN_ENERGY: key[c] = p->gpu_wh[x]; break;
+          case LOOM_MIN_LATENCY: key[c] = static_cast<double>(p->wall_us[x]); break;
+          default: key[c] = static_cast<double>(-p->quality[x]); break;
         }
       }
-      if (best < 0 || key < best_key) {
+      if (best < 0 || std::lexicographical_compare(key, key + nc, best_key, best_key + nc)) {
         best = k;
-        best_key = std::move(key);
+        std::copy(key, key + nc, best_key);
       }
     }
     if (best < 0)

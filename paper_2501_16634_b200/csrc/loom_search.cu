@@ -2557,6 +2557,7 @@ void fill_fr_params(const Built& b, BfsParams<NB>& P) {
     std::sort(ql.begin(), ql.end(), std::greater<int32_t>());
     ql.erase(std::unique(ql.begin(), ql.end()), ql.end());
     P.n_qlev = static_cast<int32_t>(std::min<size_t>(8, ql.size()));
+    P.heur = b.total >= (uint64_t(1) << 16);  // a few thousand plans: the levels alone are faster
     for (int i = 0; i < P.n_qlev; ++i) P.qlev[i] = ql[i];
     // lambda grid of the heuristic: 1e-10 .. 1 over its plans (frontier.cuh fr_incumbent)
     P.lam_lo = 1e-10;
