@@ -1879,26 +1879,33 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   int nv = inner_radix <= 8 ? 8 : inner_radix <= 16 ? 16 : 0;
   if (const char* f = std::getenv("LOOM_FORCE_NV")) nv = std::atoi(f) == 0 ? 0 : nv;  // experiments
 
-  // topology: Kahn order + predecessor CSR
-  std::vector<int32_t> indeg(n, 0), topo;
-  std::vector<std::vector<int32_t>> succ(n), preds(n);
-  for (int e = 0; e < p->n_edges; ++e) {
-    succ[p->edge_from[e]].push_back(p->edge_to[e]);
-    preds[p->edge_to[e]].push_back(p->edge_from[e]);
+  // topology: Kahn order + predecessor CSR (counting sort of the edges: the
+  // edge order is kept within a node; no per-node vectors)
+  const int ne = p->n_edges;
+  std::vector<int32_t> indeg(n, 0), topo, predoff(n + 1, 0), succoff(n + 1, 0), pred(ne), succ(ne);
+  topo.reserve(n);
+  for (int e = 0; e < ne; ++e) {
+    ++predoff[p->edge_to[e] + 1];
+    ++succoff[p->edge_from[e] + 1];
     ++indeg[p->edge_to[e]];
+  }
+  for (int i = 0; i < n; ++i) {
+    predoff[i + 1] += predoff[i];
+    succoff[i + 1] += succoff[i];
+  }
+  {
+    std::vector<int32_t> pc(predoff.begin(), predoff.end() - 1), sc(succoff.begin(), succoff.end() - 1);
+    for (int e = 0; e < ne; ++e) {
+      pred[pc[p->edge_to[e]]++] = p->edge_from[e];
+      succ[sc[p->edge_from[e]]++] = p->edge_to[e];
+    }
   }
   for (int i = 0; i < n; ++i)
     if (!indeg[i]) topo.push_back(i);
   for (std::size_t t = 0; t < topo.size(); ++t)
-    for (int s : succ[topo[t]])
-      if (--indeg[s] == 0) topo.push_back(s);
+    for (int e = succoff[topo[t]]; e < succoff[topo[t] + 1]; ++e)
+      if (--indeg[succ[e]] == 0) topo.push_back(succ[e]);
   if (static_cast<int>(topo.size()) != n) return loomi::fail(LOOM_INVALID, "CycleError: dag has a cycle");
-  std::vector<int32_t> predoff(n + 1, 0), pred;
-  for (int i = 0; i < n; ++i) {
-    predoff[i] = static_cast<int32_t>(pred.size());
-    pred.insert(pred.end(), preds[i].begin(), preds[i].end());
-  }
-  predoff[n] = static_cast<int32_t>(pred.size());
 
   // layout
   BlobHeader hd;
@@ -1926,26 +1933,29 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
   hd.off_nok = take(4 * n);
   hd.off_bmin = take(static_cast<int>(sizeof(BnbMin)) * n);
   hd.off_rk = take(8 * (n + 1));
-  // settled-node lists (bnb.cuh): anc[x] = x and its ancestors
-  std::vector<std::vector<int32_t>> uns(n), nset(n);
+  // settled-node lists (bnb.cuh): anc[x] = x and its ancestors; CSR per depth k
+  std::vector<int32_t> uns_off(n + 1, 0), uns, ns_off(n + 1, 0), nset;
   {
-    std::vector<uint64_t> anc(n, 0);  // n <= 32 nodes: bit sets
+    uint64_t anc[kMaxNodes] = {};  // n <= 32 nodes: bit sets
     for (int x : topo) {
       anc[x] |= uint64_t(1) << x;
       for (int e = predoff[x]; e < predoff[x + 1]; ++e) anc[x] |= anc[pred[e]];
     }
     auto settled = [&](int x, int k) { return (anc[x] >> k) == 0; };  // every ancestor-or-self < k
-    for (int k = 0; k < n; ++k)
+    uns.reserve(static_cast<size_t>(n) * n);
+    nset.reserve(n);
+    for (int k = 0; k < n; ++k) {
+      uns_off[k] = static_cast<int32_t>(uns.size());
+      ns_off[k] = static_cast<int32_t>(nset.size());
       for (int x : topo) {
-        if (!settled(x, k)) uns[k].push_back(x);
-        if (settled(x, k + 1) && !settled(x, k)) nset[k].push_back(x);
+        if (!settled(x, k)) uns.push_back(x);
+        if (settled(x, k + 1) && !settled(x, k)) nset.push_back(x);
       }
+    }
+    uns_off[n] = static_cast<int32_t>(uns.size());
+    ns_off[n] = static_cast<int32_t>(nset.size());
   }
-  auto csr_bytes = [&](const std::vector<std::vector<int32_t>>& v) {
-    std::size_t m = n + 1;
-    for (auto& x : v) m += x.size();
-    return static_cast<int>(4 * m);
-  };
+  auto csr_bytes = [&](const std::vector<int32_t>& data) { return static_cast<int>(4 * (n + 1 + data.size())); };
   hd.off_uns = take(csr_bytes(uns));
   hd.off_nsettle = take(csr_bytes(nset));
   if (off > kMaxBlobBytes) return loomi::fail(LOOM_INVALID, "InvalidConfigError: problem image exceeds shared memory");
@@ -2026,17 +2036,13 @@ int build_image(const loom_problem* p, const loom_objective* o, uint64_t target_
     uint64_t* rk = reinterpret_cast<uint64_t*>(base + hd.off_rk);
     rk[n] = 1;
     for (int i = n - 1; i >= 0; --i) rk[i] = rk[i + 1] * static_cast<uint64_t>(p->radix[i]);
-    auto put_csr = [&](int at, const std::vector<std::vector<int32_t>>& v) {
-      int32_t* o = reinterpret_cast<int32_t*>(base + at);
-      int32_t m = n + 1;
-      for (int k = 0; k < n; ++k) {
-        o[k] = m;
-        for (int32_t x : v[k]) o[m++] = x;
-      }
-      o[n] = m;
+    auto put_csr = [&](int at, const std::vector<int32_t>& offs, const std::vector<int32_t>& data) {
+      int32_t* o = reinterpret_cast<int32_t*>(base + at);  // offsets relative to o, entries after them
+      for (int k = 0; k <= n; ++k) o[k] = n + 1 + offs[k];
+      std::copy(data.begin(), data.end(), o + n + 1);
     };
-    put_csr(hd.off_uns, uns);
-    put_csr(hd.off_nsettle, nset);
+    put_csr(hd.off_uns, uns_off, uns);
+    put_csr(hd.off_nsettle, ns_off, nset);
     for (int i = 0; i < n; ++i) {
       std::vector<int32_t> ord;
       BnbMin m{INFINITY, INFINITY, INT64_MAX, UINT64_MAX, INT_MIN, -1, {0, 0}};
