@@ -3071,7 +3071,9 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
       off[j] = arena;
       arena += built[j].blob.size();
     }
-  if (int rc = ensure_host_arena(c, arena)) return rc;
+  // the pinned arena also stages the job descriptors, after the images
+  const size_t desc_at = (arena + 255) & ~size_t(255);
+  if (int rc = ensure_host_arena(c, desc_at + sizeof(JobDesc) * static_cast<size_t>(n_jobs))) return rc;
   uint8_t* host_arena = c->h_arena;  // pinned: the copy below runs at full link speed
   parallel_for(n_jobs, [&](int j) {
     if (ok[j]) std::memcpy(host_arena + off[j], built[j].blob.data(), built[j].blob.size());
@@ -3100,7 +3102,9 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
     }
   }
   tr.mark("descriptors");
-  LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, all.data(), all.size() * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
+  std::memcpy(c->h_arena + desc_at, all.data(), all.size() * sizeof(JobDesc));
+  LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, c->h_arena + desc_at, all.size() * sizeof(JobDesc), cudaMemcpyHostToDevice,
+                            c->stream));
   // Branch and bound over every job (one CTA per job, `all` order); each
   // group's sweep launch below then retires the jobs it settled.
   if (!all.empty()) {

@@ -11,7 +11,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2501_16634_b200 import loom, workloads as W  # noqa: E402
 
 jobs = W.config4(10_000)
-dags = [json.dumps(j.dag) for j in jobs]
+dags = [json.dumps(j.dag).encode() for j in jobs]  # bytes, as the bench passes them
 lib_t, bounds_t = json.dumps(jobs[0].library), json.dumps(jobs[0].bounds)
 ctx = loom.Context(0)
 for token in sys.argv[1:] or ["MIN_LATENCY"]:
