@@ -43,6 +43,7 @@ struct loom_ctx {
   size_t h_out_cap = 0;
   uint8_t* h_arena = nullptr;  // pinned staging of batch problem images
   size_t h_arena_cap = 0;
+  size_t batch_image_hint = 0;  // largest mean image bytes per job seen in a batch
   // Device scratch pool (grow-only size classes, reused across calls; all
   // work of a ctx is ordered on its one stream, so reuse needs no sync).
   std::mutex pool_mu;

@@ -2,6 +2,7 @@
 // libloom_b200.so.  Not part of the public ABI.
 #pragma once
 
+#include <functional>
 #include <string>
 
 #include "loom_b200.h"
@@ -19,5 +20,15 @@ int check_problem(const loom_problem* p, uint64_t* total);
 // Fills every metric of *w from w->plan_index with the reference's exact
 // arithmetic (estimator.hpp:43-78).  Sets found = 1.
 int fill_winner(const loom_problem* p, loom_winner* w);
+
+// The batch search (loom_search_argmin_batch) with its jobs produced on the
+// host threads that build the problem images: produce(j, worker, &problems[j],
+// &objectives[j]) fills job j (worker < threads, for per-thread caches) or
+// returns its failure status; retire(j) runs once job j's winner is final.
+// Either callback may be empty (problems/objectives are then read as given).
+using BatchProduce = std::function<int(int job, int worker, loom_problem* p, loom_objective* o)>;
+using BatchRetire = std::function<void(int job)>;
+int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, loom_objective* objectives,
+                 const BatchProduce& produce, const BatchRetire& retire, loom_winner* out, int32_t* status);
 
 }  // namespace loomi

@@ -694,7 +694,8 @@ int search_lowered(loom_ctx* ctx, const loom_lowered* const* lowered, int32_t n,
 int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const char* bounds_json,
                                  const char* const* dag_jsons, int32_t n, const char* objective_json,
                                  int32_t threads, loom_winner* out, int32_t* status) {
-  if (!ctx || !objective_json || (n > 0 && (!out || !status)) || n < 0)
+  if (!ctx || !objective_json || !library_json || !bounds_json || (n > 0 && (!out || !status || !dag_jsons)) ||
+      n < 0)
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
   std::vector<loom_objective> objs;
   try {
@@ -702,40 +703,49 @@ int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const 
   } catch (const loom::Error& e) {
     return loomi::fail(status_of(e), e.what());
   }
-  const bool trace = std::getenv("LOOM_TRACE") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  auto mark = [&](const char* what) {
-    if (!trace) return;
-    const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[loom trace] search_batch %s %.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(t - t0).count());
-    t0 = t;
-  };
-  std::vector<loom_lowered*> lw(n, nullptr);
-  std::vector<int32_t> lst(n, LOOM_OK);
-  int rc = loom_lower_batch(library_json, bounds_json, dag_jsons, n, threads, lw.data(), lst.data());
-  mark("lower");
-  if (rc == LOOM_OK) {
-    rc = search_lowered(ctx, lw.data(), n, objs.data(), objs.size() == static_cast<size_t>(n) && n > 1, out, status);
+  try {
+    const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json ? library_json : "");
+    const loom::SearchBounds bounds = loom::SearchBounds::from_json_text(bounds_json ? bounds_json : "");
+    const bool per_job = objs.size() == static_cast<size_t>(n) && n > 1;
+    // Each job is lowered on the host thread that then builds and stages its
+    // image (loomi::argmin_batch), with one option-set cache per thread, and
+    // released on the thread that finishes it.
+    std::vector<loom_lowered*> lw(n, nullptr);
+    std::vector<std::string> errors(n);
+    std::vector<std::shared_ptr<loom::LowerCache>> caches(threads > 0 ? threads : 32);
+    std::vector<loom_problem> probs(n);
+    std::vector<loom_objective> objv(n);
+    const loomi::BatchProduce produce = [&](int j, int w, loom_problem* p, loom_objective* o) -> int {
+      if (!caches[w]) caches[w] = loom::make_lower_cache();
+      try {
+        auto x = std::make_unique<loom_lowered>();
+        x->L = loom::lower(loom::WorkflowDag::from_json_text(dag_jsons[j] ? dag_jsons[j] : ""), lib, bounds,
+                           *caches[w]);
+        x->view = x->L.view();
+        *p = x->view;
+        *o = objs[per_job ? j : 0];
+        lw[j] = x.release();
+        return LOOM_OK;
+      } catch (const loom::Error& e) {
+        errors[j] = e.what();
+        return status_of(e);
+      } catch (const std::exception& e) {
+        errors[j] = std::string("InvalidConfigError: ") + e.what();
+        return LOOM_INVALID;
+      }
+    };
+    const loomi::BatchRetire retire = [&](int j) {
+      loom_lowered_destroy(lw[j]);
+      lw[j] = nullptr;
+    };
+    const int rc = loomi::argmin_batch(ctx, n, threads, probs.data(), objv.data(), produce, retire, out, status);
+    for (loom_lowered* h : lw) loom_lowered_destroy(h);  // the jobs an early error left
     for (int i = 0; i < n; ++i)
-      if (lst[i] != LOOM_OK) status[i] = lst[i];
+      if (!errors[i].empty()) loomi::set_error(errors[i]);
+    return rc;
+  } catch (const loom::Error& e) {
+    return loomi::fail(status_of(e), e.what());
   }
-  mark("search");
-  // the lowered problems hold ~100 small allocations each: free them on the
-  // same host threads that made them
-  const int t = std::max(1, std::min<int>(n, threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()))));
-  if (t > 1 && n >= 256) {
-    std::vector<std::thread> pool;
-    for (int w = 0; w < t; ++w)
-      pool.emplace_back([&, w] {
-        for (int i = w; i < n; i += t) loom_lowered_destroy(lw[i]);
-      });
-    for (auto& th : pool) th.join();
-  } else {
-    for (loom_lowered* h : lw) loom_lowered_destroy(h);
-  }
-  mark("free");
-  return rc;
 }
 
 int loom_lowered_config_json(const loom_lowered* lw, uint64_t plan_index, char* buf, size_t cap, size_t* needed) {

@@ -3017,6 +3017,211 @@ int search_argmin_impl(loom_ctx* c, const loom_problem* p, const loom_objective*
 
 }  // namespace
 
+namespace loomi {
+
+// The batch search (C4): one branch-and-bound CTA per job, then each kernel
+// instantiation's sweep retires the jobs it left.  The host side is one pass
+// over blocks of jobs: a host thread produces (lowers) a block, builds its
+// images, packs them into the pinned arena and queues the block's
+// host-to-device copy at once, so the copy of one block overlaps the work on
+// the next.  A block takes its arena range with one atomic add; the arena is
+// sized from the largest image bytes per job seen before, and blocks past it
+// ("late") are staged and copied after the others.
+int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, loom_objective* objectives,
+                 const BatchProduce& produce, const BatchRetire& retire, loom_winner* out, int32_t* status) {
+  if (n_jobs == 0) return LOOM_OK;
+  LOOM_CUDA(cudaSetDevice(c->device));
+  Trace tr("argmin_batch");
+  constexpr int kJobsPerBlock = 64;
+  const int n_blocks = (n_jobs + kJobsPerBlock - 1) / kJobsPerBlock;
+  int t = threads > 0 ? threads
+                      : static_cast<int>(std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency())));
+  t = std::max(1, std::min(t, n_blocks));
+  const size_t hint = std::max<size_t>(c->batch_image_hint, 4096);
+  const size_t cap = (hint + hint / 8) * static_cast<size_t>(n_jobs);
+  const size_t descs = sizeof(JobDesc) * static_cast<size_t>(n_jobs);
+  // every device buffer first: a reallocation later would wait on the copies
+  if (int rc = ensure_host_arena(c, ((cap + 255) & ~size_t(255)) + descs)) return rc;
+  if (int rc = ensure(c->d_arena, c->arena_cap, cap)) return rc;
+  if (int rc = ensure(c->d_jobs, c->jobs_cap, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure_tickets(c, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure(c->d_out, c->out_cap, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure_host(c, static_cast<size_t>(n_jobs))) return rc;
+  if (int rc = ensure_bsync(c, static_cast<size_t>(n_jobs))) return rc;
+  tr.mark("buffers");
+
+  std::vector<Built> built(n_jobs);  // blobs are released once packed
+  std::vector<JobDesc> desc(n_jobs);
+  std::vector<KernelFn> kern(n_jobs, nullptr);  // nullptr: the job failed
+  std::vector<size_t> smem(n_jobs, 0), bsmem(n_jobs, 0);
+  std::vector<uint8_t> late(n_blocks, 0);
+  std::atomic<size_t> top{0};
+  std::atomic<int> next{0}, copy_err{0};
+  uint8_t* const h_arena = c->h_arena;
+  uint8_t* const d_arena = c->d_arena;
+  auto stage = [&](int w) {
+    bool device_set = false;
+    for (int blk; (blk = next.fetch_add(1)) < n_blocks;) {
+      const int lo = blk * kJobsPerBlock, hi = std::min(n_jobs, lo + kJobsPerBlock);
+      size_t bytes = 0;
+      for (int j = lo; j < hi; ++j) {
+        std::memset(&out[j], 0, sizeof out[j]);
+        int rc = produce ? produce(j, w, &problems[j], &objectives[j]) : LOOM_OK;
+        if (rc == LOOM_OK) rc = build_image(&problems[j], &objectives[j], kBlock, built[j]);
+        if (rc == LOOM_OK && built[j].total == 0)
+          rc = loomi::fail(LOOM_INFEASIBLE,
+                           "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
+        if (status) status[j] = rc;
+        if (rc != LOOM_OK) continue;
+        const Built& b = built[j];
+        kern[j] = pick_kernel(b.K, b.prim, b.nv, false);
+        smem[j] = smem_bytes(b.blob.size(), problems[j].n_nodes, lazy_of(b));
+        bsmem[j] = bnb_smem_bytes(b.blob.size(), problems[j].n_nodes);
+        JobDesc d = make_desc(b, 0, b.total, false);
+        if (b.blob.size() && !b.seed.empty()) {  // whole space: the greedy seed is in range
+          const BlobHeader* bh = reinterpret_cast<const BlobHeader*>(b.blob.data());
+          d.has_seed = bh->has_seed;
+          d.seed = bh->seed_index;
+        }
+        d.blob_off = bytes;
+        desc[j] = d;
+        bytes += b.blob.size();
+      }
+      const size_t base = top.fetch_add(bytes);
+      for (int j = lo; j < hi; ++j)
+        if (kern[j]) desc[j].blob_off += base;
+      if (base + bytes > cap) {  // staged after the others
+        late[blk] = 1;
+        continue;
+      }
+      for (int j = lo; j < hi; ++j)
+        if (kern[j]) {
+          std::memcpy(h_arena + desc[j].blob_off, built[j].blob.data(), built[j].blob.size());
+          std::vector<uint8_t>().swap(built[j].blob);
+        }
+      if (!bytes) continue;
+      if (!device_set) {
+        cudaSetDevice(c->device);
+        device_set = true;
+      }
+      if (cudaMemcpyAsync(d_arena + base, h_arena + base, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        copy_err.store(1);
+    }
+  };
+  if (t <= 1) {
+    stage(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < t; ++w) pool.emplace_back(stage, w);
+    for (auto& th : pool) th.join();
+  }
+  if (copy_err.load()) return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: problem image copy failed");
+  const size_t used = top.load();
+  int n_ok = 0;
+  for (int j = 0; j < n_jobs; ++j) n_ok += kern[j] != nullptr;
+  if (n_ok) c->batch_image_hint = std::max(c->batch_image_hint, (used + n_ok - 1) / n_ok);
+  tr.mark("produce + images + pack + copy");
+  size_t desc_at = (cap + 255) & ~size_t(255);
+  if (used > cap) {
+    // Late blocks: grow both arenas (the staged copies are complete after
+    // the sync), keep the device prefix, stage and copy the late range.
+    LOOM_CUDA(cudaStreamSynchronize(c->stream));
+    uint8_t* grown = nullptr;
+    LOOM_CUDA(cudaMalloc(&grown, used));
+    LOOM_CUDA(cudaMemcpyAsync(grown, c->d_arena, cap, cudaMemcpyDeviceToDevice, c->stream));
+    LOOM_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(c->d_arena);
+    c->d_arena = grown;
+    c->arena_cap = used;
+    desc_at = (used + 255) & ~size_t(255);
+    if (int rc = ensure_host_arena(c, desc_at + descs)) return rc;
+    size_t first = used;
+    for (int blk = 0; blk < n_blocks; ++blk) {
+      if (!late[blk]) continue;
+      for (int j = blk * kJobsPerBlock; j < std::min(n_jobs, (blk + 1) * kJobsPerBlock); ++j)
+        if (kern[j]) {
+          std::memcpy(c->h_arena + desc[j].blob_off, built[j].blob.data(), built[j].blob.size());
+          first = std::min<size_t>(first, desc[j].blob_off);
+          std::vector<uint8_t>().swap(built[j].blob);
+        }
+    }
+    if (first < used)
+      LOOM_CUDA(cudaMemcpyAsync(c->d_arena + first, c->h_arena + first, used - first, cudaMemcpyHostToDevice,
+                                c->stream));
+    tr.mark("late blocks");
+  }
+  // Group the jobs by kernel instantiation; descriptors in group order.
+  struct Group {
+    KernelFn fn;
+    std::vector<int> jobs;
+    size_t smem = 0;
+  };
+  std::vector<Group> groups;
+  size_t bmax = 0;
+  for (int j = 0; j < n_jobs; ++j) {
+    if (!kern[j]) continue;
+    Group* g = nullptr;
+    for (auto& x : groups)
+      if (x.fn == kern[j]) g = &x;
+    if (!g) {
+      groups.push_back({kern[j], {}, 0});
+      g = &groups.back();
+    }
+    g->jobs.push_back(j);
+    g->smem = std::max(g->smem, smem[j]);
+    bmax = std::max(bmax, bsmem[j]);
+  }
+  JobDesc* staged = reinterpret_cast<JobDesc*>(c->h_arena + desc_at);
+  std::vector<std::pair<int, size_t>> order;  // (job, slot in h_out)
+  order.reserve(n_ok);
+  for (auto& g : groups)
+    for (int j : g.jobs) {
+      staged[order.size()] = desc[j];
+      order.emplace_back(j, order.size());
+    }
+  if (!order.empty()) {
+    LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, staged, order.size() * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
+    // Branch and bound over every job (one CTA per job, group order); each
+    // group's sweep launch below then retires the jobs it settled.
+    if (smem_attr(reinterpret_cast<const void*>(bnb_kernel), bmax) == cudaSuccess) {
+      bnb_kernel<<<static_cast<int>(order.size()), kBlock, bmax, c->stream>>>(c->d_arena, c->d_jobs, 1, c->d_scratch,
+                                                                             c->d_tickets, c->d_bsync, c->d_out);
+      LOOM_CUDA(cudaGetLastError());
+      ++c->launches;
+    } else {
+      cudaGetLastError();
+    }
+    size_t first = 0;
+    for (auto& g : groups) {
+      if (int rc = set_smem(g.fn, g.smem)) return rc;
+      const int nj = static_cast<int>(g.jobs.size());
+      g.fn<<<nj, kBlock, g.smem, c->stream>>>(c->d_arena, c->d_jobs + first, 1, c->d_scratch + first,
+                                               c->d_tickets + first, c->d_out + first, InnerParams{});
+      LOOM_CUDA(cudaGetLastError());
+      ++c->launches;
+      first += nj;
+    }
+    LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, order.size() * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+  }
+  tr.mark("enqueue");
+  LOOM_CUDA(cudaStreamSynchronize(c->stream));
+  tr.mark("device");
+  parallel_for(static_cast<int>(order.size()), [&](int i) {
+    const int j = order[i].first;
+    const int rc = finish_winner(&problems[j], c->h_out[order[i].second], &out[j]);
+    if (status) status[j] = rc;
+    if (retire) retire(j);
+  });
+  if (retire)
+    for (int j = 0; j < n_jobs; ++j)
+      if (!kern[j]) retire(j);
+  tr.mark("finish");
+  return LOOM_OK;
+}
+
+}  // namespace loomi
+
 extern "C" {
 
 int loom_search_argmin(loom_ctx* c, const loom_problem* p, const loom_objective* o, uint64_t begin, uint64_t end,
@@ -3028,129 +3233,9 @@ int loom_search_argmin_batch(loom_ctx* c, const loom_problem* problems, const lo
                              int32_t n_jobs, loom_winner* out, int32_t* status) {
   if (!c || (!problems && n_jobs) || !objectives || (!out && n_jobs) || n_jobs < 0)
     return loomi::fail(LOOM_INVALID, "InvalidConfigError: null argument");
-  if (n_jobs == 0) return LOOM_OK;
-  LOOM_CUDA(cudaSetDevice(c->device));
-  Trace tr("argmin_batch");
-  // Build every image (host threads); group jobs by kernel instantiation.
-  std::vector<Built> built(n_jobs);
-  std::vector<int> ok(n_jobs, 0);
-  parallel_for(n_jobs, [&](int j) {
-    std::memset(&out[j], 0, sizeof out[j]);
-    int rc = build_image(&problems[j], &objectives[j], kBlock, built[j]);
-    if (rc == LOOM_OK && built[j].total == 0) {
-      rc = loomi::fail(LOOM_INFEASIBLE, "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
-    }
-    if (status) status[j] = rc;
-    ok[j] = rc == LOOM_OK;
-  });
-  tr.mark("build_images");
-  struct Group {
-    KernelFn fn;
-    std::vector<int> jobs;
-    size_t smem = 0;
-  };
-  std::vector<Group> groups;
-  for (int j = 0; j < n_jobs; ++j) {
-    if (!ok[j]) continue;
-    KernelFn fn = pick_kernel(built[j].K, built[j].prim, built[j].nv, false);
-    Group* g = nullptr;
-    for (auto& x : groups)
-      if (x.fn == fn) g = &x;
-    if (!g) {
-      groups.push_back({fn, {}, 0});
-      g = &groups.back();
-    }
-    g->jobs.push_back(j);
-    g->smem = std::max(g->smem, smem_bytes(built[j].blob.size(), problems[j].n_nodes, lazy_of(built[j])));
-  }
-  // One arena for all images; one launch per group, one CTA per job.
-  std::vector<uint64_t> off(n_jobs, 0);
-  size_t arena = 0;
-  for (int j = 0; j < n_jobs; ++j)
-    if (ok[j]) {
-      off[j] = arena;
-      arena += built[j].blob.size();
-    }
-  // the pinned arena also stages the job descriptors, after the images
-  const size_t desc_at = (arena + 255) & ~size_t(255);
-  if (int rc = ensure_host_arena(c, desc_at + sizeof(JobDesc) * static_cast<size_t>(n_jobs))) return rc;
-  uint8_t* host_arena = c->h_arena;  // pinned: the copy below runs at full link speed
-  parallel_for(n_jobs, [&](int j) {
-    if (ok[j]) std::memcpy(host_arena + off[j], built[j].blob.data(), built[j].blob.size());
-  });
-  tr.mark("pack");
-  if (int rc = ensure(c->d_arena, c->arena_cap, arena)) return rc;
-  if (int rc = ensure(c->d_jobs, c->jobs_cap, static_cast<size_t>(n_jobs))) return rc;
-  if (int rc = ensure(c->d_scratch, c->scratch_cap, static_cast<size_t>(n_jobs))) return rc;
-  if (int rc = ensure_tickets(c, static_cast<size_t>(n_jobs))) return rc;
-  if (int rc = ensure(c->d_out, c->out_cap, static_cast<size_t>(n_jobs))) return rc;
-  if (int rc = ensure_host(c, static_cast<size_t>(n_jobs))) return rc;
-  LOOM_CUDA(cudaMemcpyAsync(c->d_arena, host_arena, arena, cudaMemcpyHostToDevice, c->stream));
-  std::vector<JobDesc> all;
-  for (auto& g : groups) {
-    for (int j : g.jobs) {
-      JobDesc d = make_desc(built[j], 0, built[j].total, false);
-      if (built[j].blob.size() && !built[j].seed.empty()) {  // whole space: the greedy seed is in range
-        uint64_t x = 0;
-        const BlobHeader* bh = reinterpret_cast<const BlobHeader*>(built[j].blob.data());
-        x = bh->seed_index;
-        d.has_seed = bh->has_seed;
-        d.seed = x;
-      }
-      d.blob_off = off[j];
-      all.push_back(d);
-    }
-  }
-  tr.mark("descriptors");
-  std::memcpy(c->h_arena + desc_at, all.data(), all.size() * sizeof(JobDesc));
-  LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, c->h_arena + desc_at, all.size() * sizeof(JobDesc), cudaMemcpyHostToDevice,
-                            c->stream));
-  // Branch and bound over every job (one CTA per job, `all` order); each
-  // group's sweep launch below then retires the jobs it settled.
-  if (!all.empty()) {
-    size_t bsmem = 0;
-    int nmax = 0;
-    for (auto& g : groups)
-      for (int j : g.jobs) {
-        bsmem = std::max(bsmem, bnb_smem_bytes(built[j].blob.size(), problems[j].n_nodes));
-        nmax = std::max(nmax, problems[j].n_nodes);
-      }
-    if (int rc = ensure_bsync(c, all.size())) return rc;
-    if (smem_attr(reinterpret_cast<const void*>(bnb_kernel), static_cast<size_t>(bsmem)) == cudaSuccess) {
-      bnb_kernel<<<static_cast<int>(all.size()), kBlock, bsmem, c->stream>>>(c->d_arena, c->d_jobs, 1, c->d_scratch,
-                                                                          c->d_tickets, c->d_bsync, c->d_out);
-      LOOM_CUDA(cudaGetLastError());
-      ++c->launches;
-    } else {
-      cudaGetLastError();
-    }
-    (void)nmax;
-  }
-  size_t first = 0;
-  for (auto& g : groups) {
-    if (int rc = set_smem(g.fn, g.smem)) return rc;
-    const int nj = static_cast<int>(g.jobs.size());
-    g.fn<<<nj, kBlock, g.smem, c->stream>>>(c->d_arena, c->d_jobs + first, 1, c->d_scratch + first,
-                                             c->d_tickets + first, c->d_out + first, InnerParams{});
-    LOOM_CUDA(cudaGetLastError());
-    ++c->launches;
-    first += nj;
-  }
-  LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, all.size() * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
-  tr.mark("enqueue");
-  LOOM_CUDA(cudaStreamSynchronize(c->stream));
-  tr.mark("device");
-  std::vector<std::pair<int, size_t>> order;  // (job, slot in h_out)
-  order.reserve(all.size());
-  for (auto& g : groups)
-    for (int j : g.jobs) order.emplace_back(j, order.size());
-  parallel_for(static_cast<int>(order.size()), [&](int i) {
-    const int j = order[i].first;
-    const int rc = finish_winner(&problems[j], c->h_out[order[i].second], &out[j]);
-    if (status) status[j] = rc;
-  });
-  tr.mark("finish");
-  return LOOM_OK;
+  // read-only without a producer
+  return loomi::argmin_batch(c, n_jobs, 0, const_cast<loom_problem*>(problems),
+                             const_cast<loom_objective*>(objectives), {}, {}, out, status);
 }
 
 int loom_problem_upload(loom_ctx* c, const loom_problem* p, const loom_objective* o, loom_device_problem** out) {
