@@ -334,139 +334,4 @@ std::string Value::dump() const {
 
 Value parse(const std::string& text) { return Parser(text).document(); }
 
-// ---- Cursor ---------------------------------------------------------------
-void Cursor::ws() {
-  while (p_ < n_ && (s_[p_] == ' ' || s_[p_] == '\n' || s_[p_] == '\t' || s_[p_] == '\r')) ++p_;
-}
-bool Cursor::open(char c) {
-  ws();
-  if (p_ >= n_ || s_[p_] != c || ++depth_ > 64) return false;
-  ++p_;
-  return true;
-}
-bool Cursor::empty(char close) {
-  ws();
-  if (p_ < n_ && s_[p_] == close) {
-    ++p_;
-    --depth_;
-    return true;
-  }
-  return false;
-}
-bool Cursor::next(char close, bool& more) {
-  ws();
-  if (p_ >= n_) return false;
-  if (s_[p_] == ',') {
-    ++p_;
-    more = true;
-    return true;
-  }
-  if (s_[p_] == close) {
-    ++p_;
-    --depth_;
-    more = false;
-    return true;
-  }
-  return false;
-}
-bool Cursor::raw_string(std::string_view& out) {
-  ws();
-  if (p_ >= n_ || s_[p_] != '"') return false;
-  const std::size_t b = ++p_;
-  while (p_ < n_ && s_[p_] != '"') {
-    if (s_[p_] == '\\' || static_cast<unsigned char>(s_[p_]) < 0x20) return false;
-    ++p_;
-  }
-  if (p_ >= n_) return false;
-  out = std::string_view(s_ + b, p_ - b);
-  ++p_;
-  return true;
-}
-bool Cursor::key(std::string_view& k) {
-  if (!raw_string(k)) return false;
-  ws();
-  if (p_ >= n_ || s_[p_] != ':') return false;
-  ++p_;
-  return true;
-}
-bool Cursor::str(std::string& out) {
-  std::string_view v;
-  if (!raw_string(v)) return false;
-  out.assign(v.data(), v.size());
-  return true;
-}
-bool Cursor::num(double& out) {
-  ws();
-  const std::size_t b = p_;
-  while (p_ < n_ && (std::isdigit(static_cast<unsigned char>(s_[p_])) || s_[p_] == '-' || s_[p_] == '+' ||
-                     s_[p_] == '.' || s_[p_] == 'e' || s_[p_] == 'E'))
-    ++p_;
-  if (p_ == b) return false;
-  const auto r = std::from_chars(s_ + b, s_ + p_, out);
-  return r.ec == std::errc() && r.ptr == s_ + p_;
-}
-bool Cursor::integer(long long& out) {
-  ws();
-  const std::size_t b = p_;
-  while (p_ < n_ && (std::isdigit(static_cast<unsigned char>(s_[p_])) || s_[p_] == '-')) ++p_;
-  if (p_ == b || (p_ < n_ && (s_[p_] == '.' || s_[p_] == 'e' || s_[p_] == 'E'))) return false;
-  const auto r = std::from_chars(s_ + b, s_ + p_, out);
-  return r.ec == std::errc() && r.ptr == s_ + p_;
-}
-bool Cursor::boolean(bool& out) {
-  ws();
-  if (n_ - p_ >= 4 && std::memcmp(s_ + p_, "true", 4) == 0) {
-    p_ += 4;
-    out = true;
-    return true;
-  }
-  if (n_ - p_ >= 5 && std::memcmp(s_ + p_, "false", 5) == 0) {
-    p_ += 5;
-    out = false;
-    return true;
-  }
-  return false;
-}
-bool Cursor::null() {
-  ws();
-  if (n_ - p_ >= 4 && std::memcmp(s_ + p_, "null", 4) == 0) {
-    p_ += 4;
-    return true;
-  }
-  return false;
-}
-bool Cursor::skip() {
-  ws();
-  if (p_ >= n_) return false;
-  const char c = s_[p_];
-  if (c == '"') {
-    std::string_view v;
-    return raw_string(v);
-  }
-  if (c == '{' || c == '[') {
-    const char close = c == '{' ? '}' : ']';
-    if (!open(c)) return false;
-    if (empty(close)) return true;
-    for (bool more = true; more;) {
-      if (c == '{') {
-        std::string_view k;
-        if (!key(k)) return false;
-      }
-      if (!skip() || !next(close, more)) return false;
-    }
-    return true;
-  }
-  if (c == 't' || c == 'f') {
-    bool b;
-    return boolean(b);
-  }
-  if (c == 'n') return null();
-  double d;
-  return num(d);
-}
-bool Cursor::end() {
-  ws();
-  return p_ == n_;
-}
-
 }  // namespace loomjson

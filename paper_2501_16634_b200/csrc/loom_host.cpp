@@ -390,6 +390,8 @@ namespace {
 // canonical errors.
 bool read_dag_fast(const std::string& text, WorkflowDag& dag) {
   loomjson::Cursor c(text);
+  dag.nodes.reserve(8);
+  dag.edges.reserve(16);
   if (!c.open('{') || c.empty('}')) return false;
   bool have_nodes = false, have_edges = false;
   for (bool more = true; more;) {
@@ -873,6 +875,7 @@ class LowerCache {
   std::map<std::string, std::vector<Impl>, std::less<>> caps;
   std::map<std::string, Set, std::less<>> sets;
   std::string key;  // scratch
+  std::size_t opts_hint = 0;  // most options of one lowered problem so far (table reservations)
 };
 
 std::shared_ptr<LowerCache> make_lower_cache() { return std::make_shared<LowerCache>(); }
@@ -1080,38 +1083,79 @@ LoweredProblem lower_impl(const WorkflowDag& dag, const AgentLibrary& library, c
                           LowerCache* cache) {
   LoweredProblem L;
   const int n = static_cast<int>(dag.nodes.size());
-  std::map<std::string, int> index;
-  for (int i = 0; i < n; ++i) {
-    if (!index.emplace(dag.nodes[i].id, i).second)
-      throw InvalidConfigError("duplicate node id '" + dag.nodes[i].id + "'");
-    L.node_ids.push_back(dag.nodes[i].id);
-  }
-  for (const Edge& e : dag.edges) {
-    auto f = index.find(e.from), t = index.find(e.to);
-    if (f == index.end() || t == index.end()) throw CycleError("edge references unknown node");
-    L.edge_from.push_back(f->second);
-    L.edge_to.push_back(t->second);
-  }
-  topo_order(n, L.edge_from, L.edge_to);  // throws CycleError like topological_order
-  {
-    // the reference's topological_order: Kahn with ready peers popped in node-id
-    // order (workflow.hpp:467-498); greedy_search sweeps nodes in this order
-    std::vector<int> indeg(n, 0);
-    std::vector<std::vector<int>> succ(n);
-    for (std::size_t e = 0; e < L.edge_from.size(); ++e) {
-      succ[L.edge_from[e]].push_back(L.edge_to[e]);
-      ++indeg[L.edge_to[e]];
+  L.node_ids.reserve(n);
+  if (n <= 64) {
+    // Small dags (every batch job): no maps or queues.  Duplicate ids are
+    // reported at their first repeat in dag order, edges resolve by binary
+    // search over the id-sorted nodes, and the id-ordered Kahn sweep runs on
+    // predecessor masks (the node popped next is the smallest-id ready one,
+    // as with the priority queue); an incomplete sweep is the cycle.
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < i; ++j)
+        if (dag.nodes[j].id == dag.nodes[i].id) throw InvalidConfigError("duplicate node id '" + dag.nodes[i].id + "'");
+      L.node_ids.push_back(dag.nodes[i].id);
     }
-    auto by_id = [&](int a, int b) { return L.node_ids[a] > L.node_ids[b]; };
-    std::priority_queue<int, std::vector<int>, decltype(by_id)> ready(by_id);
-    for (int i = 0; i < n; ++i)
-      if (!indeg[i]) ready.push(i);
-    while (!ready.empty()) {
-      const int v = ready.top();
-      ready.pop();
+    int by_id[64];
+    std::iota(by_id, by_id + n, 0);
+    std::sort(by_id, by_id + n, [&](int a, int b) { return L.node_ids[a] < L.node_ids[b]; });
+    auto find = [&](const std::string& id) {
+      const int* it = std::lower_bound(by_id, by_id + n, id, [&](int a, const std::string& v) { return L.node_ids[a] < v; });
+      return it != by_id + n && L.node_ids[*it] == id ? *it : -1;
+    };
+    uint64_t pred[64] = {};
+    L.edge_from.reserve(dag.edges.size());
+    L.edge_to.reserve(dag.edges.size());
+    for (const Edge& e : dag.edges) {
+      const int f = find(e.from), t = find(e.to);
+      if (f < 0 || t < 0) throw CycleError("edge references unknown node");
+      L.edge_from.push_back(f);
+      L.edge_to.push_back(t);
+      pred[t] |= uint64_t(1) << f;
+    }
+    L.sweep_order.reserve(n);
+    uint64_t done = 0;
+    for (int step = 0; step < n; ++step) {
+      int v = -1;
+      for (int k = 0; k < n && v < 0; ++k)
+        if (!(done >> by_id[k] & 1) && !(pred[by_id[k]] & ~done)) v = by_id[k];
+      if (v < 0) throw CycleError("dag has a cycle");
+      done |= uint64_t(1) << v;
       L.sweep_order.push_back(v);
-      for (int s2 : succ[v])
-        if (--indeg[s2] == 0) ready.push(s2);
+    }
+  } else {
+    std::map<std::string, int> index;
+    for (int i = 0; i < n; ++i) {
+      if (!index.emplace(dag.nodes[i].id, i).second)
+        throw InvalidConfigError("duplicate node id '" + dag.nodes[i].id + "'");
+      L.node_ids.push_back(dag.nodes[i].id);
+    }
+    for (const Edge& e : dag.edges) {
+      auto f = index.find(e.from), t = index.find(e.to);
+      if (f == index.end() || t == index.end()) throw CycleError("edge references unknown node");
+      L.edge_from.push_back(f->second);
+      L.edge_to.push_back(t->second);
+    }
+    topo_order(n, L.edge_from, L.edge_to);  // throws CycleError like topological_order
+    {
+      // the reference's topological_order: Kahn with ready peers popped in node-id
+      // order (workflow.hpp:467-498); greedy_search sweeps nodes in this order
+      std::vector<int> indeg(n, 0);
+      std::vector<std::vector<int>> succ(n);
+      for (std::size_t e = 0; e < L.edge_from.size(); ++e) {
+        succ[L.edge_from[e]].push_back(L.edge_to[e]);
+        ++indeg[L.edge_to[e]];
+      }
+      auto by_id = [&](int a, int b) { return L.node_ids[a] > L.node_ids[b]; };
+      std::priority_queue<int, std::vector<int>, decltype(by_id)> ready(by_id);
+      for (int i = 0; i < n; ++i)
+        if (!indeg[i]) ready.push(i);
+      while (!ready.empty()) {
+        const int v = ready.top();
+        ready.pop();
+        L.sweep_order.push_back(v);
+        for (int s2 : succ[v])
+          if (--indeg[s2] == 0) ready.push(s2);
+      }
     }
   }
 
@@ -1134,7 +1178,14 @@ LoweredProblem lower_impl(const WorkflowDag& dag, const AgentLibrary& library, c
   impls.reserve(32);
   L.radix.reserve(n);
   L.options.reserve(n);
-  if (cache) L.shared_options.reserve(n);
+  std::vector<Worker> workers;
+  if (cache) {
+    L.shared_options.reserve(n);
+    for (auto* v : {&L.gpu_wh, &L.cpu_wh, &L.dollars}) v->reserve(cache->opts_hint);
+    L.wall_us.reserve(cache->opts_hint);
+    L.quality.reserve(cache->opts_hint);
+    L.lexrank.reserve(cache->opts_hint);
+  }
   for (int i = 0; i < n; ++i) {
     const DagNode& node = dag.nodes[i];
     check_name(node.id);
@@ -1147,7 +1198,6 @@ LoweredProblem lower_impl(const WorkflowDag& dag, const AgentLibrary& library, c
         throw InvalidConfigError("plan space exceeds 2^64 plans");
       else L.total *= static_cast<uint64_t>(r);
       NodePlan plan;
-      std::vector<Worker> workers;
       for (int o = 0; o < r; ++o) {
         const NodeAssignment& a = (*set.opts)[o];
         if (o == 0 || set.base[o] != set.base[o - 1]) {  // == plan_node_execution(node, a, library)
@@ -1212,6 +1262,8 @@ LoweredProblem lower_impl(const WorkflowDag& dag, const AgentLibrary& library, c
     L.lexrank.insert(L.lexrank.end(), rank.begin(), rank.end());
     L.options.push_back(std::move(opts));
   }
+
+  if (cache) cache->opts_hint = std::max(cache->opts_hint, L.wall_us.size());
 
   // Mixed-radix weights in std::map (sorted node id) order: the identifier
   // concatenates nodes in that order, so the first sorted node is the most
