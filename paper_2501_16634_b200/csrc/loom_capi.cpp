@@ -91,11 +91,67 @@ std::vector<int> topo(const loom_problem* p) {
 
 }  // namespace
 
+// fill_winner for dags of <= 64 nodes (every batch job): no allocations;
+// predecessor masks give the critical path in any topological order (max
+// and + over int64 are exact, so the order does not change the result).
+static int fill_winner_small(const loom_problem* p, loom_winner* w) {
+  const int n = p->n_nodes;
+  int opt[64];
+  uint64_t x = w->plan_index;
+  int off = 0;
+  for (int i = 0; i < n; ++i) off += p->radix[i];
+  for (int i = n - 1; i >= 0; --i) {
+    off -= p->radix[i];
+    opt[i] = off + static_cast<int>(x % static_cast<uint64_t>(p->radix[i]));
+    x /= static_cast<uint64_t>(p->radix[i]);
+  }
+  // estimator.hpp:46-67: left folds in dag.nodes order starting from 0.0
+  double gpu = 0.0, cpu = 0.0, dol = 0.0;
+  int q = INT_MAX;
+  uint64_t lex = 0;
+  for (int i = 0; i < n; ++i) {
+    gpu += p->gpu_wh[opt[i]];
+    cpu += p->cpu_wh[opt[i]];
+    dol += p->dollars[opt[i]];
+    q = std::min(q, p->quality[opt[i]]);
+    lex += static_cast<uint64_t>(p->lexrank[opt[i]]) * p->lex_weight[i];
+  }
+  // estimator.hpp:69-76: finish(v) = max over in-edges of finish(u) + wall(v)
+  uint64_t pred[64] = {};
+  for (int e = 0; e < p->n_edges; ++e) pred[p->edge_to[e]] |= uint64_t(1) << p->edge_from[e];
+  int64_t fin[64];
+  int64_t lat = 0;
+  uint64_t done = 0;
+  const uint64_t all = n == 64 ? ~uint64_t(0) : (uint64_t(1) << n) - 1;
+  while (done != all) {
+    const uint64_t before = done;
+    for (int v = 0; v < n; ++v) {
+      if ((done >> v & 1) || (pred[v] & ~done)) continue;
+      int64_t s = 0;
+      for (uint64_t m = pred[v]; m; m &= m - 1) s = std::max(s, fin[__builtin_ctzll(m)]);
+      fin[v] = s + p->wall_us[opt[v]];
+      lat = std::max(lat, fin[v]);
+      done |= uint64_t(1) << v;
+    }
+    if (done == before) return fail(LOOM_INVALID, "CycleError: dag has a cycle");
+  }
+  w->latency_us = lat;
+  w->gpu_wh = gpu;
+  w->cpu_wh = cpu;
+  w->total_wh = gpu + cpu;
+  w->dollars = dol;
+  w->quality = q;
+  w->lexkey = lex;
+  w->found = 1;
+  return LOOM_OK;
+}
+
 int fill_winner(const loom_problem* p, loom_winner* w) {
   uint64_t total = 0;
   if (int rc = check_problem(p, &total)) return rc;
   if (w->plan_index >= total) return fail(LOOM_INVALID, "InvalidConfigError: plan index out of range");
   const int n = p->n_nodes;
+  if (n <= 64) return fill_winner_small(p, w);
   std::vector<int> opt(n), off(n + 1, 0);
   for (int i = 0; i < n; ++i) off[i + 1] = off[i] + p->radix[i];
   uint64_t x = w->plan_index;

@@ -3037,7 +3037,8 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   int t = threads > 0 ? threads
                       : static_cast<int>(std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency())));
   t = std::max(1, std::min(t, n_blocks));
-  const size_t hint = std::max<size_t>(c->batch_image_hint, 4096);
+  size_t hint = std::max<size_t>(c->batch_image_hint, 4096);
+  if (const char* h = std::getenv("LOOM_BATCH_HINT")) hint = std::strtoull(h, nullptr, 10);  // test knob: late blocks
   const size_t cap = (hint + hint / 8) * static_cast<size_t>(n_jobs);
   const size_t descs = sizeof(JobDesc) * static_cast<size_t>(n_jobs);
   // every device buffer first: a reallocation later would wait on the copies
@@ -3051,30 +3052,39 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   if (int rc = ensure_bsync(c, static_cast<size_t>(n_jobs))) return rc;
   tr.mark("buffers");
 
-  std::vector<Built> built(n_jobs);  // blobs are released once packed
   std::vector<JobDesc> desc(n_jobs);
   std::vector<KernelFn> kern(n_jobs, nullptr);  // nullptr: the job failed
   std::vector<size_t> smem(n_jobs, 0), bsmem(n_jobs, 0);
   std::vector<uint8_t> late(n_blocks, 0);
+  std::vector<std::pair<size_t, std::vector<uint8_t>>> late_pack(n_blocks);  // (arena offset, images)
+  std::vector<int> owner(n_blocks, 0);  // the thread that staged a block also finishes it
   std::atomic<size_t> top{0};
   std::atomic<int> next{0}, copy_err{0};
   uint8_t* const h_arena = c->h_arena;
   uint8_t* const d_arena = c->d_arena;
   auto stage = [&](int w) {
     bool device_set = false;
+    Built b;                    // reused per job; its image buffer keeps its capacity
+    std::vector<uint8_t> pack;  // the block's images back to back
     for (int blk; (blk = next.fetch_add(1)) < n_blocks;) {
       const int lo = blk * kJobsPerBlock, hi = std::min(n_jobs, lo + kJobsPerBlock);
-      size_t bytes = 0;
+      owner[blk] = w;
+      pack.clear();
       for (int j = lo; j < hi; ++j) {
         std::memset(&out[j], 0, sizeof out[j]);
         int rc = produce ? produce(j, w, &problems[j], &objectives[j]) : LOOM_OK;
-        if (rc == LOOM_OK) rc = build_image(&problems[j], &objectives[j], kBlock, built[j]);
-        if (rc == LOOM_OK && built[j].total == 0)
+        if (rc == LOOM_OK) {
+          std::vector<uint8_t> keep = std::move(b.blob);
+          b = Built{};
+          b.blob = std::move(keep);
+          b.blob.clear();
+          rc = build_image(&problems[j], &objectives[j], kBlock, b);
+        }
+        if (rc == LOOM_OK && b.total == 0)
           rc = loomi::fail(LOOM_INFEASIBLE,
                            "NoFeasibleConfigError: no configuration satisfies the quality floor and bounds");
         if (status) status[j] = rc;
         if (rc != LOOM_OK) continue;
-        const Built& b = built[j];
         kern[j] = pick_kernel(b.K, b.prim, b.nv, false);
         smem[j] = smem_bytes(b.blob.size(), problems[j].n_nodes, lazy_of(b));
         bsmem[j] = bnb_smem_bytes(b.blob.size(), problems[j].n_nodes);
@@ -3084,23 +3094,21 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
           d.has_seed = bh->has_seed;
           d.seed = bh->seed_index;
         }
-        d.blob_off = bytes;
+        d.blob_off = pack.size();
         desc[j] = d;
-        bytes += b.blob.size();
+        pack.insert(pack.end(), b.blob.begin(), b.blob.end());
       }
+      const size_t bytes = pack.size();
       const size_t base = top.fetch_add(bytes);
       for (int j = lo; j < hi; ++j)
         if (kern[j]) desc[j].blob_off += base;
       if (base + bytes > cap) {  // staged after the others
         late[blk] = 1;
+        late_pack[blk] = {base, pack};
         continue;
       }
-      for (int j = lo; j < hi; ++j)
-        if (kern[j]) {
-          std::memcpy(h_arena + desc[j].blob_off, built[j].blob.data(), built[j].blob.size());
-          std::vector<uint8_t>().swap(built[j].blob);
-        }
       if (!bytes) continue;
+      std::memcpy(h_arena + base, pack.data(), bytes);
       if (!device_set) {
         cudaSetDevice(c->device);
         device_set = true;
@@ -3121,6 +3129,8 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   int n_ok = 0;
   for (int j = 0; j < n_jobs; ++j) n_ok += kern[j] != nullptr;
   if (n_ok) c->batch_image_hint = std::max(c->batch_image_hint, (used + n_ok - 1) / n_ok);
+  if (tr.on) std::fprintf(stderr, "[loom trace] argmin_batch arena %.2f MB (%d jobs, %zu late)\n", used / 1e6, n_jobs,
+                         static_cast<size_t>(std::count(late.begin(), late.end(), 1)));
   tr.mark("produce + images + pack + copy");
   size_t desc_at = (cap + 255) & ~size_t(255);
   if (used > cap) {
@@ -3138,13 +3148,9 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
     if (int rc = ensure_host_arena(c, desc_at + descs)) return rc;
     size_t first = used;
     for (int blk = 0; blk < n_blocks; ++blk) {
-      if (!late[blk]) continue;
-      for (int j = blk * kJobsPerBlock; j < std::min(n_jobs, (blk + 1) * kJobsPerBlock); ++j)
-        if (kern[j]) {
-          std::memcpy(c->h_arena + desc[j].blob_off, built[j].blob.data(), built[j].blob.size());
-          first = std::min<size_t>(first, desc[j].blob_off);
-          std::vector<uint8_t>().swap(built[j].blob);
-        }
+      if (!late[blk] || late_pack[blk].second.empty()) continue;
+      std::memcpy(c->h_arena + late_pack[blk].first, late_pack[blk].second.data(), late_pack[blk].second.size());
+      first = std::min(first, late_pack[blk].first);
     }
     if (first < used)
       LOOM_CUDA(cudaMemcpyAsync(c->d_arena + first, c->h_arena + first, used - first, cudaMemcpyHostToDevice,
@@ -3207,15 +3213,30 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   tr.mark("enqueue");
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   tr.mark("device");
-  parallel_for(static_cast<int>(order.size()), [&](int i) {
-    const int j = order[i].first;
-    const int rc = finish_winner(&problems[j], c->h_out[order[i].second], &out[j]);
-    if (status) status[j] = rc;
-    if (retire) retire(j);
-  });
-  if (retire)
-    for (int j = 0; j < n_jobs; ++j)
-      if (!kern[j]) retire(j);
+  // Winners re-evaluated and jobs retired on the thread that produced them
+  // (a producer's cache shares data between its jobs: no cross-thread
+  // reference-count traffic when they are released).
+  std::vector<int32_t> slot(n_jobs, -1);
+  for (const auto& [j, k] : order) slot[j] = static_cast<int32_t>(k);
+  auto finish = [&](int w) {
+    for (int blk = 0; blk < n_blocks; ++blk) {
+      if (owner[blk] != w) continue;
+      for (int j = blk * kJobsPerBlock; j < std::min(n_jobs, (blk + 1) * kJobsPerBlock); ++j) {
+        if (slot[j] >= 0) {
+          const int rc = finish_winner(&problems[j], c->h_out[slot[j]], &out[j]);
+          if (status) status[j] = rc;
+        }
+        if (retire) retire(j);
+      }
+    }
+  };
+  if (t <= 1) {
+    finish(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < t; ++w) pool.emplace_back(finish, w);
+    for (auto& th : pool) th.join();
+  }
   tr.mark("finish");
   return LOOM_OK;
 }
