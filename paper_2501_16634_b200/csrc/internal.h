@@ -2,8 +2,12 @@
 // libloom_b200.so.  Not part of the public ABI.
 #pragma once
 
+#include <sched.h>
+
+#include <algorithm>
 #include <functional>
 #include <string>
+#include <thread>
 
 #include "loom_b200.h"
 
@@ -20,6 +24,18 @@ int check_problem(const loom_problem* p, uint64_t* total);
 // Fills every metric of *w from w->plan_index with the reference's exact
 // arithmetic (estimator.hpp:43-78).  Sets found = 1.
 int fill_winner(const loom_problem* p, loom_winner* w);
+
+// Host threads this process may run on (its CPU affinity mask; the machine's
+// count when unavailable): the default width of the host-side batch work
+// (more threads than cores only add switching, measured on C4).
+inline int host_threads() {
+  cpu_set_t set;
+  if (sched_getaffinity(0, sizeof set, &set) == 0) {
+    const int n = CPU_COUNT(&set);
+    if (n > 0) return n;
+  }
+  return static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+}
 
 // The batch search (loom_search_argmin_batch) with its jobs produced on the
 // host threads that build the problem images: produce(j, worker, &problems[j],

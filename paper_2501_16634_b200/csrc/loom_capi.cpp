@@ -665,7 +665,7 @@ int loom_lower_batch(const char* library_json, const char* bounds_json, const ch
   try {
     const loom::AgentLibrary lib = loom::AgentLibrary::from_json_text(library_json);
     const loom::SearchBounds bounds = loom::SearchBounds::from_json_text(bounds_json);
-    int t = threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    int t = threads > 0 ? threads : loomi::host_threads();
     t = std::max(1, std::min(t, n));
     std::vector<std::string> errors(n);
     std::vector<std::thread> pool;
@@ -768,7 +768,7 @@ int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const 
     // released on the thread that finishes it.
     std::vector<loom_lowered*> lw(n, nullptr);
     std::vector<std::string> errors(n);
-    std::vector<std::shared_ptr<loom::LowerCache>> caches(threads > 0 ? threads : 32);
+    std::vector<std::shared_ptr<loom::LowerCache>> caches(threads > 0 ? threads : 64);
     std::vector<loom_problem> probs(n);
     std::vector<loom_objective> objv(n);
     const loomi::BatchProduce produce = [&](int j, int w, loom_problem* p, loom_objective* o) -> int {

@@ -2746,7 +2746,7 @@ void winner_from_rec(const Rec& r, loom_winner* w) {
 // Host work over many jobs on up to 32 threads (small batches stay inline).
 template <class F>
 void parallel_for(int n, F&& f) {
-  const int t = n < 64 ? 1 : static_cast<int>(std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency())));
+  const int t = n < 64 ? 1 : std::min(32, loomi::host_threads());
   if (t <= 1) {
     for (int i = 0; i < n; ++i) f(i);
     return;
@@ -3034,8 +3034,7 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   Trace tr("argmin_batch");
   constexpr int kJobsPerBlock = 64;
   const int n_blocks = (n_jobs + kJobsPerBlock - 1) / kJobsPerBlock;
-  int t = threads > 0 ? threads
-                      : static_cast<int>(std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency())));
+  int t = threads > 0 ? threads : std::min(64, loomi::host_threads());
   t = std::max(1, std::min(t, n_blocks));
   size_t hint = std::max<size_t>(c->batch_image_hint, 4096);
   if (const char* h = std::getenv("LOOM_BATCH_HINT")) hint = std::strtoull(h, nullptr, 10);  // test knob: late blocks
