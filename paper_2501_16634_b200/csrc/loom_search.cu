@@ -46,6 +46,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <queue>
 #include <string>
@@ -3061,6 +3062,17 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   std::atomic<int> next{0}, copy_err{0};
   uint8_t* const h_arena = c->h_arena;
   uint8_t* const d_arena = c->d_arena;
+  // Waves of consecutive blocks: the calling thread launches a wave's
+  // searches as soon as its blocks are staged, while the host threads stage
+  // the next ones (blocks are taken in order, so waves complete roughly in
+  // order).  A wave holding a late block waits for the end of the pass.
+  const int n_waves = std::min(n_blocks, 4);
+  std::vector<int> wave_of(n_blocks), wave_blk(n_waves + 1);
+  for (int k = 0; k <= n_waves; ++k) wave_blk[k] = static_cast<int>(static_cast<int64_t>(n_blocks) * k / n_waves);
+  for (int k = 0; k < n_waves; ++k)
+    for (int blk = wave_blk[k]; blk < wave_blk[k + 1]; ++blk) wave_of[blk] = k;
+  std::unique_ptr<std::atomic<int>[]> wave_left(new std::atomic<int>[n_waves]);
+  for (int k = 0; k < n_waves; ++k) wave_left[k].store(wave_blk[k + 1] - wave_blk[k]);
   auto stage = [&](int w) {
     bool device_set = false;
     Built b;                    // reused per job; its image buffer keeps its capacity
@@ -3104,37 +3116,108 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
       if (base + bytes > cap) {  // staged after the others
         late[blk] = 1;
         late_pack[blk] = {base, pack};
-        continue;
+      } else if (bytes) {
+        std::memcpy(h_arena + base, pack.data(), bytes);
+        if (!device_set) {
+          cudaSetDevice(c->device);
+          device_set = true;
+        }
+        if (cudaMemcpyAsync(d_arena + base, h_arena + base, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+          copy_err.store(1);
       }
-      if (!bytes) continue;
-      std::memcpy(h_arena + base, pack.data(), bytes);
-      if (!device_set) {
-        cudaSetDevice(c->device);
-        device_set = true;
-      }
-      if (cudaMemcpyAsync(d_arena + base, h_arena + base, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
-        copy_err.store(1);
+      wave_left[wave_of[blk]].fetch_sub(1, std::memory_order_release);  // after the copy is queued
     }
   };
+  // One wave's searches: descriptors staged in group order after the
+  // previous waves', one branch-and-bound launch over the wave, then each
+  // group's sweep retires the jobs it left (pointers offset to the wave).
+  std::vector<int32_t> slot(n_jobs, -1);  // job -> position in d_jobs / h_out
+  size_t pos = 0;
+  size_t desc_at = (cap + 255) & ~size_t(255);
+  struct Group {
+    KernelFn fn;
+    std::vector<int> jobs;
+    size_t smem = 0;
+  };
+  auto launch_wave = [&](int k) -> int {
+    std::vector<Group> groups;
+    size_t bmax = 0;
+    const int jlo = wave_blk[k] * kJobsPerBlock, jhi = std::min(n_jobs, wave_blk[k + 1] * kJobsPerBlock);
+    for (int j = jlo; j < jhi; ++j) {
+      if (!kern[j]) continue;
+      Group* g = nullptr;
+      for (auto& x : groups)
+        if (x.fn == kern[j]) g = &x;
+      if (!g) {
+        groups.push_back({kern[j], {}, 0});
+        g = &groups.back();
+      }
+      g->jobs.push_back(j);
+      g->smem = std::max(g->smem, smem[j]);
+      bmax = std::max(bmax, bsmem[j]);
+    }
+    const size_t p0 = pos;
+    JobDesc* staged = reinterpret_cast<JobDesc*>(c->h_arena + desc_at);
+    for (auto& g : groups)
+      for (int j : g.jobs) {
+        staged[pos] = desc[j];
+        slot[j] = static_cast<int32_t>(pos++);
+      }
+    const int nw = static_cast<int>(pos - p0);
+    if (!nw) return LOOM_OK;
+    LOOM_CUDA(cudaMemcpyAsync(c->d_jobs + p0, staged + p0, nw * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
+    if (smem_attr(reinterpret_cast<const void*>(bnb_kernel), bmax) == cudaSuccess) {
+      bnb_kernel<<<nw, kBlock, bmax, c->stream>>>(c->d_arena, c->d_jobs + p0, 1, c->d_scratch + p0, c->d_tickets + p0,
+                                                  c->d_bsync + p0, c->d_out + p0);
+      LOOM_CUDA(cudaGetLastError());
+      ++c->launches;
+    } else {
+      cudaGetLastError();
+    }
+    size_t first = p0;
+    for (auto& g : groups) {
+      if (int rc = set_smem(g.fn, g.smem)) return rc;
+      const int nj = static_cast<int>(g.jobs.size());
+      g.fn<<<nj, kBlock, g.smem, c->stream>>>(c->d_arena, c->d_jobs + first, 1, c->d_scratch + first,
+                                               c->d_tickets + first, c->d_out + first, InnerParams{});
+      LOOM_CUDA(cudaGetLastError());
+      ++c->launches;
+      first += nj;
+    }
+    return LOOM_OK;
+  };
+  auto wave_late = [&](int k) {
+    for (int blk = wave_blk[k]; blk < wave_blk[k + 1]; ++blk)
+      if (late[blk]) return true;
+    return false;
+  };
+  int launched = 0, rc_wave = LOOM_OK;
   if (t <= 1) {
     stage(0);
   } else {
     std::vector<std::thread> pool;
     for (int w = 0; w < t; ++w) pool.emplace_back(stage, w);
-    for (auto& th : pool) th.join();
+    for (; launched < n_waves && rc_wave == LOOM_OK; ++launched) {
+      while (wave_left[launched].load(std::memory_order_acquire) > 0)
+        std::this_thread::sleep_for(std::chrono::microseconds(10));
+      if (copy_err.load() || wave_late(launched)) break;
+      rc_wave = launch_wave(launched);
+    }
+    for (auto& th : pool) th.join();  // always: no early return with host threads running
   }
+  if (rc_wave != LOOM_OK) return rc_wave;
   if (copy_err.load()) return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: problem image copy failed");
   const size_t used = top.load();
   int n_ok = 0;
   for (int j = 0; j < n_jobs; ++j) n_ok += kern[j] != nullptr;
   if (n_ok) c->batch_image_hint = std::max(c->batch_image_hint, (used + n_ok - 1) / n_ok);
-  if (tr.on) std::fprintf(stderr, "[loom trace] argmin_batch arena %.2f MB (%d jobs, %zu late)\n", used / 1e6, n_jobs,
-                         static_cast<size_t>(std::count(late.begin(), late.end(), 1)));
-  tr.mark("produce + images + pack + copy");
-  size_t desc_at = (cap + 255) & ~size_t(255);
+  if (tr.on) std::fprintf(stderr, "[loom trace] argmin_batch arena %.2f MB (%d jobs, %zu late, %d of %d waves launched during the pass)\n",
+                          used / 1e6, n_jobs, static_cast<size_t>(std::count(late.begin(), late.end(), 1)), launched, n_waves);
+  tr.mark("produce + images + pack + copy (+ early waves)");
   if (used > cap) {
-    // Late blocks: grow both arenas (the staged copies are complete after
-    // the sync), keep the device prefix, stage and copy the late range.
+    // Late blocks: grow both arenas (the staged copies and the launched
+    // waves are complete after the sync), keep the device prefix, stage and
+    // copy the late range; the pinned descriptors restart after it.
     LOOM_CUDA(cudaStreamSynchronize(c->stream));
     uint8_t* grown = nullptr;
     LOOM_CUDA(cudaMalloc(&grown, used));
@@ -3156,67 +3239,15 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
                                 c->stream));
     tr.mark("late blocks");
   }
-  // Group the jobs by kernel instantiation; descriptors in group order.
-  struct Group {
-    KernelFn fn;
-    std::vector<int> jobs;
-    size_t smem = 0;
-  };
-  std::vector<Group> groups;
-  size_t bmax = 0;
-  for (int j = 0; j < n_jobs; ++j) {
-    if (!kern[j]) continue;
-    Group* g = nullptr;
-    for (auto& x : groups)
-      if (x.fn == kern[j]) g = &x;
-    if (!g) {
-      groups.push_back({kern[j], {}, 0});
-      g = &groups.back();
-    }
-    g->jobs.push_back(j);
-    g->smem = std::max(g->smem, smem[j]);
-    bmax = std::max(bmax, bsmem[j]);
-  }
-  JobDesc* staged = reinterpret_cast<JobDesc*>(c->h_arena + desc_at);
-  std::vector<std::pair<int, size_t>> order;  // (job, slot in h_out)
-  order.reserve(n_ok);
-  for (auto& g : groups)
-    for (int j : g.jobs) {
-      staged[order.size()] = desc[j];
-      order.emplace_back(j, order.size());
-    }
-  if (!order.empty()) {
-    LOOM_CUDA(cudaMemcpyAsync(c->d_jobs, staged, order.size() * sizeof(JobDesc), cudaMemcpyHostToDevice, c->stream));
-    // Branch and bound over every job (one CTA per job, group order); each
-    // group's sweep launch below then retires the jobs it settled.
-    if (smem_attr(reinterpret_cast<const void*>(bnb_kernel), bmax) == cudaSuccess) {
-      bnb_kernel<<<static_cast<int>(order.size()), kBlock, bmax, c->stream>>>(c->d_arena, c->d_jobs, 1, c->d_scratch,
-                                                                             c->d_tickets, c->d_bsync, c->d_out);
-      LOOM_CUDA(cudaGetLastError());
-      ++c->launches;
-    } else {
-      cudaGetLastError();
-    }
-    size_t first = 0;
-    for (auto& g : groups) {
-      if (int rc = set_smem(g.fn, g.smem)) return rc;
-      const int nj = static_cast<int>(g.jobs.size());
-      g.fn<<<nj, kBlock, g.smem, c->stream>>>(c->d_arena, c->d_jobs + first, 1, c->d_scratch + first,
-                                               c->d_tickets + first, c->d_out + first, InnerParams{});
-      LOOM_CUDA(cudaGetLastError());
-      ++c->launches;
-      first += nj;
-    }
-    LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, order.size() * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
-  }
+  for (; launched < n_waves; ++launched)
+    if (int rc = launch_wave(launched)) return rc;
+  if (pos) LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, pos * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
   tr.mark("enqueue");
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   tr.mark("device");
   // Winners re-evaluated and jobs retired on the thread that produced them
   // (a producer's cache shares data between its jobs: no cross-thread
   // reference-count traffic when they are released).
-  std::vector<int32_t> slot(n_jobs, -1);
-  for (const auto& [j, k] : order) slot[j] = static_cast<int32_t>(k);
   auto finish = [&](int w) {
     for (int blk = 0; blk < n_blocks; ++blk) {
       if (owner[blk] != w) continue;
