@@ -5,15 +5,73 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
 #include "loom_b200.h"
 #include "search_common.h"
+
+// Host threads kept by a context for the batch calls (spawning and joining
+// 16 threads costs ~0.5 ms, twice per C4 call).  start(n, fn) runs fn(w) on
+// workers w = 0..n-1 while the caller goes on; wait() returns when all n are
+// done.  One job at a time (a context is used by one thread at a time).
+struct HostPool {
+  std::mutex mu;
+  std::condition_variable cv_work, cv_done;
+  std::vector<std::thread> threads;
+  const std::function<void(int)>* fn = nullptr;
+  int active = 0, pending = 0;
+  uint64_t gen = 0;
+  bool stop = false;
+
+  void start(int n, const std::function<void(int)>& f) {
+    while (static_cast<int>(threads.size()) < n) {
+      const int w = static_cast<int>(threads.size());
+      threads.emplace_back([this, w] { loop(w); });
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    fn = &f;
+    active = pending = n;
+    ++gen;
+    cv_work.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv_done.wait(lk, [&] { return pending == 0; });
+  }
+  void loop(int w) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f = nullptr;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_work.wait(lk, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+        if (w >= active) continue;
+        f = fn;
+      }
+      (*f)(w);
+      std::lock_guard<std::mutex> lk(mu);
+      if (--pending == 0) cv_done.notify_one();
+    }
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv_work.notify_all();
+    for (auto& t : threads) t.join();
+  }
+};
 
 struct loom_ctx {
   int device = 0;
@@ -53,6 +111,7 @@ struct loom_ctx {
   std::vector<loom_point> pareto_cache;
   uint64_t pareto_key = 0;
   bool pareto_valid = false;
+  HostPool host;  // batch host threads (argmin_batch)
 };
 
 namespace loomi {

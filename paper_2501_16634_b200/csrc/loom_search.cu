@@ -3192,18 +3192,18 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
     return false;
   };
   int launched = 0, rc_wave = LOOM_OK;
+  const std::function<void(int)> stage_fn = stage;
   if (t <= 1) {
     stage(0);
   } else {
-    std::vector<std::thread> pool;
-    for (int w = 0; w < t; ++w) pool.emplace_back(stage, w);
+    c->host.start(t, stage_fn);
     for (; launched < n_waves && rc_wave == LOOM_OK; ++launched) {
       while (wave_left[launched].load(std::memory_order_acquire) > 0)
         std::this_thread::sleep_for(std::chrono::microseconds(10));
       if (copy_err.load() || wave_late(launched)) break;
       rc_wave = launch_wave(launched);
     }
-    for (auto& th : pool) th.join();  // always: no early return with host threads running
+    c->host.wait();  // always: no early return with host threads running
   }
   if (rc_wave != LOOM_OK) return rc_wave;
   if (copy_err.load()) return loomi::fail(LOOM_DEVICE_ERROR, "DeviceError: problem image copy failed");
@@ -3260,12 +3260,12 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
       }
     }
   };
+  const std::function<void(int)> finish_fn = finish;
   if (t <= 1) {
     finish(0);
   } else {
-    std::vector<std::thread> pool;
-    for (int w = 0; w < t; ++w) pool.emplace_back(finish, w);
-    for (auto& th : pool) th.join();
+    c->host.start(t, finish_fn);
+    c->host.wait();
   }
   tr.mark("finish");
   return LOOM_OK;
