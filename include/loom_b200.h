@@ -151,7 +151,8 @@ int loom_objective_parse(const char* objective_json, loom_objective* out);
 int loom_lower(const char* dag_json, const char* library_json, const char* bounds_json,
                loom_lowered** out);
 /* Many DAGs against one library bundle and bounds (config 4: the library is
- * parsed once and the DAGs are lowered on `threads` host threads; 0 = all).
+ * parsed once and the DAGs are lowered on `threads` host threads; 0 = the
+ * CPUs this process may run on).
  * out[i] receives a handle or NULL; status[i] the per-DAG status. */
 int loom_lower_batch(const char* library_json, const char* bounds_json, const char* const* dag_jsons,
                      int32_t n, int32_t threads, loom_lowered** out, int32_t* status);
@@ -257,8 +258,11 @@ int loom_search_argmin_lowered_each(loom_ctx* ctx, const loom_lowered* const* lo
 
 /* The whole multi-tenant call on reference-format JSON: n DAGs against one
  * library bundle, bounds and objective -> n winners (a loop of
- * exhaustive_search, optimizer.hpp:173-188, with lowering on `threads` host
- * threads and one batched device search).  status[i] is the job's status. */
+ * exhaustive_search, optimizer.hpp:173-188).  On `threads` host threads
+ * (0 = the CPUs this process may run on, at most 64, kept by the context),
+ * blocks of 64 jobs are lowered, imaged and copied to the device while the
+ * searches of the blocks already staged run.  status[i] is the job's status.
+ * A context runs one batch at a time. */
 /* objective_json is one objective for every job, or a JSON array of n
  * per-job objectives (e.g. per-tenant latency SLOs). */
 int loom_exhaustive_search_batch(loom_ctx* ctx, const char* library_json, const char* bounds_json,
