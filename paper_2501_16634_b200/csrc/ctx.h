@@ -112,6 +112,11 @@ struct loom_ctx {
   uint64_t pareto_key = 0;
   bool pareto_valid = false;
   HostPool host;  // batch host threads (argmin_batch)
+  // batch image copies run on their own stream, so a wave's searches on
+  // `stream` do not hold up the copies of the next blocks; the searches wait
+  // on copy_done, recorded after their wave's copies
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_done = nullptr;
 };
 
 namespace loomi {

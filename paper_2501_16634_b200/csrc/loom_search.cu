@@ -2853,6 +2853,11 @@ int loom_ctx_destroy(loom_ctx* c) {
   for (void* q : c->pool_all) cudaFree(q);
   if (c->h_out) cudaFreeHost(c->h_out);
   if (c->h_arena) cudaFreeHost(c->h_arena);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  if (c->copy_done) cudaEventDestroy(c->copy_done);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return LOOM_OK;
@@ -3050,6 +3055,12 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   if (int rc = ensure(c->d_out, c->out_cap, static_cast<size_t>(n_jobs))) return rc;
   if (int rc = ensure_host(c, static_cast<size_t>(n_jobs))) return rc;
   if (int rc = ensure_bsync(c, static_cast<size_t>(n_jobs))) return rc;
+  if (c->copy_stream) LOOM_CUDA(cudaStreamSynchronize(c->copy_stream));  // idle unless a call failed midway
+  if (!c->copy_stream) LOOM_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!c->copy_done) LOOM_CUDA(cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming));
+  // the copy stream starts after everything queued on the ctx's stream
+  LOOM_CUDA(cudaEventRecord(c->copy_done, c->stream));
+  LOOM_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_done, 0));
   tr.mark("buffers");
 
   std::vector<JobDesc> desc(n_jobs);
@@ -3062,11 +3073,12 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   std::atomic<int> next{0}, copy_err{0};
   uint8_t* const h_arena = c->h_arena;
   uint8_t* const d_arena = c->d_arena;
-  // Waves of consecutive blocks: the calling thread launches a wave's
+  // Waves of consecutive blocks (8: the last wave's kernels are what remains
+  // after the pass): the calling thread launches a wave's
   // searches as soon as its blocks are staged, while the host threads stage
   // the next ones (blocks are taken in order, so waves complete roughly in
   // order).  A wave holding a late block waits for the end of the pass.
-  const int n_waves = std::min(n_blocks, 4);
+  const int n_waves = std::min(n_blocks, 8);
   std::vector<int> wave_of(n_blocks), wave_blk(n_waves + 1);
   for (int k = 0; k <= n_waves; ++k) wave_blk[k] = static_cast<int>(static_cast<int64_t>(n_blocks) * k / n_waves);
   for (int k = 0; k < n_waves; ++k)
@@ -3122,7 +3134,8 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
           cudaSetDevice(c->device);
           device_set = true;
         }
-        if (cudaMemcpyAsync(d_arena + base, h_arena + base, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        if (cudaMemcpyAsync(d_arena + base, h_arena + base, bytes, cudaMemcpyHostToDevice, c->copy_stream) !=
+            cudaSuccess)
           copy_err.store(1);
       }
       wave_left[wave_of[blk]].fetch_sub(1, std::memory_order_release);  // after the copy is queued
@@ -3139,7 +3152,13 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
     std::vector<int> jobs;
     size_t smem = 0;
   };
+  auto after_copies = [&]() -> int {  // `stream` waits for the copies queued so far
+    LOOM_CUDA(cudaEventRecord(c->copy_done, c->copy_stream));
+    LOOM_CUDA(cudaStreamWaitEvent(c->stream, c->copy_done, 0));
+    return LOOM_OK;
+  };
   auto launch_wave = [&](int k) -> int {
+    if (int rc = after_copies()) return rc;
     std::vector<Group> groups;
     size_t bmax = 0;
     const int jlo = wave_blk[k] * kJobsPerBlock, jhi = std::min(n_jobs, wave_blk[k + 1] * kJobsPerBlock);
@@ -3216,8 +3235,9 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   tr.mark("produce + images + pack + copy (+ early waves)");
   if (used > cap) {
     // Late blocks: grow both arenas (the staged copies and the launched
-    // waves are complete after the sync), keep the device prefix, stage and
+    // waves are complete after the syncs), keep the device prefix, stage and
     // copy the late range; the pinned descriptors restart after it.
+    LOOM_CUDA(cudaStreamSynchronize(c->copy_stream));
     LOOM_CUDA(cudaStreamSynchronize(c->stream));
     uint8_t* grown = nullptr;
     LOOM_CUDA(cudaMalloc(&grown, used));
@@ -3242,6 +3262,7 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   for (; launched < n_waves; ++launched)
     if (int rc = launch_wave(launched)) return rc;
   if (pos) LOOM_CUDA(cudaMemcpyAsync(c->h_out, c->d_out, pos * sizeof(Rec), cudaMemcpyDeviceToHost, c->stream));
+  if (int rc = after_copies()) return rc;  // the pinned arena is reused by the next call
   tr.mark("enqueue");
   LOOM_CUDA(cudaStreamSynchronize(c->stream));
   tr.mark("device");
