@@ -50,6 +50,7 @@
 #include <mutex>
 #include <queue>
 #include <string>
+#include <system_error>
 #include <tuple>
 #include <vector>
 
@@ -3212,10 +3213,19 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
   };
   int launched = 0, rc_wave = LOOM_OK;
   const std::function<void(int)> stage_fn = stage;
-  if (t <= 1) {
+  // host threads unavailable (thread creation failed): the calling thread
+  // stages every block, then launches every wave
+  const auto pooled = [&](const std::function<void(int)>& f) {
+    try {
+      c->host.start(t, f);
+      return true;
+    } catch (const std::system_error&) {
+      return false;
+    }
+  };
+  if (t <= 1 || !pooled(stage_fn)) {
     stage(0);
   } else {
-    c->host.start(t, stage_fn);
     for (; launched < n_waves && rc_wave == LOOM_OK; ++launched) {
       while (wave_left[launched].load(std::memory_order_acquire) > 0)
         std::this_thread::sleep_for(std::chrono::microseconds(10));
@@ -3282,11 +3292,10 @@ int argmin_batch(loom_ctx* c, int n_jobs, int threads, loom_problem* problems, l
     }
   };
   const std::function<void(int)> finish_fn = finish;
-  if (t <= 1) {
-    finish(0);
-  } else {
-    c->host.start(t, finish_fn);
+  if (t > 1 && pooled(finish_fn)) {
     c->host.wait();
+  } else {
+    for (int w = 0; w < t; ++w) finish(w);
   }
   tr.mark("finish");
   return LOOM_OK;
